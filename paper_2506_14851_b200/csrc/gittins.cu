@@ -1,0 +1,311 @@
+// K1: Gittins-rank scorers for sm_100a.
+//
+// Reference: pdgsim.sched.gittins_rank_batch (sched.py:102-129) and the
+// batched refresh around it (sched.py:271-305).  For one row with support
+// values v_j (ascending), masses p_j and attained service a:
+//   d_j = v_j - a,  alive_j = d_j > 0,  m_j = alive_j ? p_j : 0,  Z = sum m
+//   rank = min over alive j with S_j > 0 of (P_j + d_j * T_j) / S_j
+// where S_j = sum_{k<=j} m_k, P_j = sum_{k<=j} m_k d_k, T_j = Z - S_j.  This is
+// the reference's num/cum_p with the 1/Z normalisation cancelled; exhausted
+// rows (Z <= 0) give NaN, or age*penalty in the fused refresh.
+//
+// Two kernels:
+//   K1a gittins_f64_kernel  -- drop-in for gittins_rank_batch on arbitrary
+//        float64 rows: everything in float64, same formula order as numpy.
+//   K1b gittins_hist_kernel -- the device-resident queue: one warp per app,
+//        u16 bucket counts (exact: p_j = count_j / n), d_j formed bit-exactly
+//        in float64 at the alive boundary, scans in int32 (S, T exact) and
+//        float32 (P); HBM-bound, 128-bit loads of 8 counts per lane.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace pdg {
+
+// ---------------------------------------------------------------------------
+// K1a
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gittins_f64_kernel(
+    const double* __restrict__ V, const double* __restrict__ P,
+    const double* __restrict__ A, int64_t N, int B, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = gw; r < N; r += nw) {
+    const double* v = V + r * B;
+    const double* p = P + r * B;
+    const double age = A[r];
+    double z = 0.0;
+    for (int j = lane; j < B; j += 32) {
+      double d = dsub(v[j], age);
+      if (d > 0.0) z = dadd(z, p[j]);
+    }
+    z = warp_sum(z);
+    if (!(z > 0.0)) {                      // sched.py:117-118,129
+      if (lane == 0) out[r] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
+    double cp_carry = 0.0, cpv_carry = 0.0, best = __longlong_as_double(0x7ff0000000000000ll);
+    for (int base = 0; base < B; base += 32) {
+      const int j = base + lane;
+      double dl = 0.0, c = 0.0;
+      bool live = false;
+      if (j < B) {
+        double d = dsub(v[j], age);
+        live = d > 0.0;
+        if (live) {
+          dl = d;
+          c = __ddiv_rn(p[j], z);         // cond = mass / z  (sched.py:120)
+        }
+      }
+      double cp = dadd(warp_incl_scan(c, lane), cp_carry);
+      double cpv = dadd(warp_incl_scan(dmul(c, dl), lane), cpv_carry);
+      double num = dadd(cpv, dmul(dl, dsub(1.0, cp)));   // sched.py:124
+      if (live && cp > 0.0) best = fmin(best, __ddiv_rn(num, cp));
+      cp_carry = __shfl_sync(kFull, cp, 31);
+      cpv_carry = __shfl_sync(kFull, cpv, 31);
+    }
+    best = warp_min(best);
+    if (lane == 0) out[r] = best;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1b
+// ---------------------------------------------------------------------------
+struct HistArgs {
+  const double* __restrict__ lo;
+  const double* __restrict__ width;
+  const double* __restrict__ est;
+  const int32_t* __restrict__ nbins;
+  const uint16_t* __restrict__ counts;
+  int64_t stride;
+  const double* __restrict__ age;
+  int64_t n;
+  double penalty;
+  float* __restrict__ out_f32;
+  uint8_t* __restrict__ out_flags;
+  const uint32_t* __restrict__ tiebreak;
+  uint64_t* __restrict__ out_key;
+};
+
+// Exact d = fl(fl(mid_j + est) - age), as sched.py:179 then sched.py:114.
+__device__ __forceinline__ double exact_d(double lo, double w, double est,
+                                          double age, int j) {
+  return dsub(dadd(bucket_mid(lo, w, j), est), age);
+}
+
+// One lane's segment of 8 consecutive buckets starting at j0.  Produces
+// integer masses and float32 offsets d for the alive buckets.  Values ascend,
+// so the alive buckets are a suffix; its first bucket i0 is located with
+// bit-exact float64 tests and d_i = d_{i0} + (i - i0)*w is then a sum of
+// positive terms, which float32 carries to ~1e-7 relative accuracy.
+__device__ __forceinline__ void lane_segment(const uint4 raw, int j0, int k,
+                                             double lo, double w, double est,
+                                             double age, int (&m)[8],
+                                             float (&d)[8]) {
+  int i0 = 8;
+  double d0 = 0.0;
+  if (j0 < k) {
+    const int last = min(7, k - 1 - j0);
+    const double ef = exact_d(lo, w, est, age, j0);
+    if (ef > 0.0) {
+      i0 = 0;
+      d0 = ef;
+    } else if (exact_d(lo, w, est, age, j0 + last) > 0.0) {
+#pragma unroll 1
+      for (int i = 1; i <= last; ++i) {
+        const double e = exact_d(lo, w, est, age, j0 + i);
+        if (e > 0.0) { i0 = i; d0 = e; break; }
+      }
+    }
+    if (i0 < 8) {
+      // buckets past the row's last real bucket are excluded (they would be
+      // zero-mass padding in the reference, sched.py:282-291)
+      const float df = float(d0), wf = float(w);
+      const uint32_t wd[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = int((wd[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+        const bool on = (i >= i0) && (i <= last);
+        m[i] = on ? c : 0;
+        d[i] = on ? fmaf(float(i - i0), wf, df) : 0.f;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { m[i] = 0; d[i] = 0.f; }
+}
+
+template <int CH>   // row holds up to 256*CH buckets
+__global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(HistArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  if (gw >= a.n) return;
+
+  // software pipeline: counts of the next row are in flight while the current
+  // row is scored
+  uint4 nxt[CH];
+  auto load = [&](int64_t r, uint4 (&dst)[CH]) {
+    const uint4* row = reinterpret_cast<const uint4*>(a.counts + r * a.stride);
+    const int k = __ldg(a.nbins + r);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int j0 = 256 * c + 8 * lane;
+      dst[c] = (j0 < k) ? __ldcs(row + 32 * c + lane) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  load(gw, nxt);
+  for (int64_t r = gw; r < a.n; r += nw) {
+    uint4 cur[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) cur[c] = nxt[c];
+    const double lo = __ldg(a.lo + r), w = __ldg(a.width + r);
+    const double est = __ldg(a.est + r), age = __ldg(a.age + r);
+    const int k = __ldg(a.nbins + r);
+    if (r + nw < a.n) load(r + nw, nxt);
+
+    int m[CH][8];
+    float d[CH][8];
+    int lane_m[CH];
+    float lane_pv[CH];
+    int ztot = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      lane_segment(cur[c], 256 * c + 8 * lane, k, lo, w, est, age, m[c], d[c]);
+      int sm = 0;
+      float sp = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { sm += m[c][i]; sp = fmaf(float(m[c][i]), d[c][i], sp); }
+      lane_m[c] = sm;
+      lane_pv[c] = sp;
+      ztot += sm;
+    }
+    const int Z = warp_sum(ztot);
+    float key;
+    uint8_t flags = 0;
+    if (Z <= 0) {                                   // exhausted: sched.py:295-300
+      key = float(dmul(age, a.penalty));
+      flags = PDG_FLAG_OVERRUN;
+    } else {
+      int s_carry = 0;
+      float pv_carry = 0.f;
+      float best = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int s_incl = warp_incl_scan(lane_m[c], lane);
+        const float pv_incl = warp_incl_scan(lane_pv[c], lane);
+        int S = s_carry + s_incl - lane_m[c];
+        float Pv = pv_carry + (pv_incl - lane_pv[c]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int mi = m[c][i];
+          S += mi;
+          Pv = fmaf(float(mi), d[c][i], Pv);
+          // zero-mass buckets never beat the previous positive one (and give
+          // +inf before any mass), so only positive-mass buckets are scored
+          if (mi > 0) {
+            const float T = float(Z - S);
+            best = fminf(best, __fdiv_rn(fmaf(d[c][i], T, Pv), float(S)));
+          }
+        }
+        s_carry += __shfl_sync(kFull, s_incl, 31);
+        pv_carry += __shfl_sync(kFull, pv_incl, 31);
+      }
+      key = warp_min(best);
+    }
+    if (lane == 0) {
+      if (!(key > 0.f)) key = 0.f;                  // canonical +0 for the sort key
+      if (a.out_f32) a.out_f32[r] = key;
+      if (a.out_flags) a.out_flags[r] = flags;
+      if (a.out_key) {
+        const uint32_t tb = a.tiebreak ? a.tiebreak[r] : uint32_t(r);
+        a.out_key[r] = (uint64_t(__float_as_uint(key)) << 32) | tb;
+      }
+    }
+  }
+}
+
+}  // namespace pdg
+
+using namespace pdg;
+
+extern "C" int pdg_gittins_rank_f64(const double* values, const double* probs,
+                                    const double* ages, int64_t n_rows,
+                                    int32_t n_bins, double* out_rank,
+                                    void* stream) {
+  if (n_rows < 0 || n_bins <= 0 || (n_rows > 0 && (!values || !probs || !ages || !out_rank))) {
+    set_error("pdg_gittins_rank_f64: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (n_rows == 0) return PDG_OK;
+  const int threads = 256;
+  int64_t warps_needed = n_rows;
+  int64_t blocks = (warps_needed * 32 + threads - 1) / threads;
+  const int64_t cap = int64_t(sm_count()) * 8;
+  if (blocks > cap) blocks = cap;
+  gittins_f64_kernel<<<unsigned(blocks), threads, 0, (cudaStream_t)stream>>>(
+      values, probs, ages, n_rows, n_bins, out_rank);
+  return launch_status("gittins_f64_kernel");
+}
+
+extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* age,
+                                      int64_t n, double penalty, float* out_key_f32,
+                                      uint8_t* out_flags, const uint32_t* tiebreak,
+                                      uint64_t* out_key, void* stream) {
+  if (!rows || n < 0 || (n > 0 && (!age || !rows->lo || !rows->width || !rows->est_age ||
+                                   !rows->nbins || !rows->counts))) {
+    set_error("pdg_gittins_score_hist: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (rows->stride % 8 != 0 || (reinterpret_cast<uintptr_t>(rows->counts) & 15)) {
+    set_error("pdg_gittins_score_hist: counts must be 16-byte aligned, stride %% 8 == 0");
+    return PDG_EINVAL;
+  }
+  if (n == 0) return PDG_OK;
+  HistArgs a{rows->lo, rows->width, rows->est_age, rows->nbins, rows->counts,
+             rows->stride, age, n, penalty, out_key_f32, out_flags, tiebreak, out_key};
+  const int threads = 256;
+  int64_t blocks = (n * 32 + threads - 1) / threads;
+  const int64_t cap = int64_t(sm_count()) * 4;
+  if (blocks > cap) blocks = cap;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t maxb = rows->stride;   // buckets per row are bounded by the stride
+  if (maxb <= 256) gittins_hist_kernel<1><<<unsigned(blocks), threads, 0, s>>>(a);
+  else if (maxb <= 512) gittins_hist_kernel<2><<<unsigned(blocks), threads, 0, s>>>(a);
+  else if (maxb <= 1024) gittins_hist_kernel<4><<<unsigned(blocks), threads, 0, s>>>(a);
+  else {
+    set_error("pdg_gittins_score_hist: more than 1024 buckets per row");
+    return PDG_EUNSUPPORTED;
+  }
+  return launch_status("gittins_hist_kernel");
+}
+
+extern "C" size_t pdg_order_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr,
+                                  (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, n, 0, 64);
+  return bytes;
+}
+
+extern "C" int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
+                         const uint32_t* slots_in, uint32_t* slots_out, int64_t n,
+                         void* temp, size_t temp_bytes, void* stream) {
+  if (n < 0 || (n > 0 && (!keys_in || !keys_out || !slots_in || !slots_out || !temp))) {
+    set_error("pdg_order: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (n == 0) return PDG_OK;
+  size_t need = pdg_order_temp_bytes(n);
+  if (temp_bytes < need) {
+    set_error("pdg_order: temp_bytes %zu < %zu", temp_bytes, need);
+    return PDG_EINVAL;
+  }
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out,
+                                                  slots_in, slots_out, n, 0, 64,
+                                                  (cudaStream_t)stream);
+  return cuda_status(e, "pdg_order");
+}

@@ -1,0 +1,117 @@
+"""Device-resident scoring queue: the struct-of-arrays form of the histograms
+the reference caches per application (``ApplicationInstance.set_remaining``,
+sched.py:170-181) plus the per-refresh attained service.
+
+HBM layout (one row per queued application, row = queue slot):
+
+    lo, width, est_age, age : float64 [N]      bucket grid + ages
+    nbins, nsamp            : int32   [N]      bucket count k (1 = point mass), n
+    counts                  : uint16  [N, S]   bucket counts, S = ceil(B/8)*8
+    tiebreak                : int32   [N]      arrival-order position (sched.py:168)
+
+p_j = counts_j / n reproduces the reference's float64 probabilities exactly
+and the bucket values are rebuilt bit-exactly from (lo, width, est_age), so a
+256-bucket row costs 512 + 40 bytes instead of the 4 KB of float64 rows.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+
+PDG_FLAG_OVERRUN = 0x1
+
+
+def round8(b: int) -> int:
+    return (int(b) + 7) // 8 * 8
+
+
+class HistQueue:
+    def __init__(self, capacity: int, max_bins: int = 256, device: str = "cuda"):
+        _lib.lib()      # loud failure without the CUDA library / device
+        if capacity < 1 or max_bins < 1 or max_bins > 1024:
+            raise ValueError("capacity >= 1 and 1 <= max_bins <= 1024 required")
+        self.capacity = int(capacity)
+        self.max_bins = int(max_bins)
+        self.stride = round8(max_bins)
+        dev = torch.device(device)
+        f64 = dict(dtype=torch.float64, device=dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.lo = torch.zeros(capacity, **f64)
+        self.width = torch.zeros(capacity, **f64)
+        self.est_age = torch.zeros(capacity, **f64)
+        self.age = torch.zeros(capacity, **f64)
+        self.nbins = torch.ones(capacity, **i32)
+        self.nsamp = torch.ones(capacity, **i32)
+        self.counts = torch.zeros(capacity, self.stride, dtype=torch.uint16, device=dev)
+        self.tiebreak = torch.arange(capacity, **i32)
+        self.key_f32 = torch.zeros(capacity, dtype=torch.float32, device=dev)
+        self.flags = torch.zeros(capacity, dtype=torch.uint8, device=dev)
+        self.keys = torch.zeros(capacity, dtype=torch.int64, device=dev)
+        self.slots = torch.arange(capacity, **i32)
+        self.sorted_keys = torch.zeros(capacity, dtype=torch.int64, device=dev)
+        self.sorted_slots = torch.zeros(capacity, **i32)
+        tb = _lib.load().pdg_order_temp_bytes(capacity)
+        self._temp = torch.empty(max(int(tb), 16), dtype=torch.uint8, device=dev)
+        self.n = 0
+        self._rows = _lib.HistRows()
+        self._bind()
+
+    def _bind(self):
+        r = self._rows
+        r.lo, r.width, r.est_age = (_lib.ptr(self.lo), _lib.ptr(self.width),
+                                    _lib.ptr(self.est_age))
+        r.nbins, r.nsamp, r.counts = (_lib.ptr(self.nbins), _lib.ptr(self.nsamp),
+                                      _lib.ptr(self.counts))
+        r.stride = self.stride
+
+    # -- host loading (tests / bench; the engine fills rows on device) --------
+    def load_rows(self, lo, width, est_age, nbins, nsamp, counts, age=None,
+                  tiebreak=None, start: int = 0) -> None:
+        m = len(lo)
+        if start + m > self.capacity:
+            raise ValueError("queue capacity exceeded")
+        sl = slice(start, start + m)
+        self.lo[sl] = torch.as_tensor(np.asarray(lo, dtype=np.float64))
+        self.width[sl] = torch.as_tensor(np.asarray(width, dtype=np.float64))
+        self.est_age[sl] = torch.as_tensor(np.asarray(est_age, dtype=np.float64))
+        self.nbins[sl] = torch.as_tensor(np.asarray(nbins, dtype=np.int32))
+        self.nsamp[sl] = torch.as_tensor(np.asarray(nsamp, dtype=np.int32))
+        c = np.asarray(counts)
+        if c.shape[1] > self.stride:
+            raise ValueError("row wider than max_bins")
+        buf = np.zeros((m, self.stride), dtype=np.uint16)
+        buf[:, :c.shape[1]] = c
+        self.counts[sl] = torch.as_tensor(buf)
+        if age is not None:
+            self.age[sl] = torch.as_tensor(np.asarray(age, dtype=np.float64))
+        if tiebreak is not None:
+            self.tiebreak[sl] = torch.as_tensor(np.asarray(tiebreak, dtype=np.int64).astype(np.int32))
+        self.n = max(self.n, start + m)
+
+    # -- scoring ---------------------------------------------------------------
+    def score(self, penalty: float = 2.0, n: Optional[int] = None, stream=None,
+              keys: bool = True) -> None:
+        """K1b over the first n rows: key_f32, flags and packed sort keys."""
+        n = self.n if n is None else int(n)
+        L = _lib.lib()
+        _lib.check(L.pdg_gittins_score_hist(
+            C.byref(self._rows), _lib.ptr(self.age), n, float(penalty),
+            _lib.ptr(self.key_f32), _lib.ptr(self.flags), _lib.ptr(self.tiebreak),
+            _lib.ptr(self.keys) if keys else None, _lib.stream_ptr(stream)),
+            "pdg_gittins_score_hist")
+
+    def order(self, n: Optional[int] = None, stream=None) -> torch.Tensor:
+        """K5 (single GPU): queue slots sorted by (key, arrival order)."""
+        n = self.n if n is None else int(n)
+        L = _lib.lib()
+        _lib.check(L.pdg_order(_lib.ptr(self.keys), _lib.ptr(self.sorted_keys),
+                               _lib.ptr(self.slots), _lib.ptr(self.sorted_slots), n,
+                               _lib.ptr(self._temp), self._temp.numel(),
+                               _lib.stream_ptr(stream)), "pdg_order")
+        return self.sorted_slots[:n]

@@ -1,0 +1,220 @@
+"""Drop-in Gittins scheduling API backed by the sm_100a scorers.
+
+Mirrors the reference module ``pdgsim.sched`` (sched.py:24-318): same names,
+argument meaning, NaN/penalty conventions and error types.  Functions accept
+the reference's own ``ApplicationInstance`` / ``Policy`` objects (duck-typed:
+only attributes are read, policies compare by ``.value``), so they can be
+patched into ``pdgsim.sched`` / ``pdgsim.simcore``.
+
+All ranking arithmetic runs in kernel K1a (``pdg_gittins_rank_f64``); the
+host side only marshals rows, exactly as the reference does around its numpy
+call.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+from enum import Enum
+from typing import Iterable, NamedTuple, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import EstimationError, ExhaustedDistributionError
+
+OVERRUN_PENALTY_FACTOR = 2.0     # sched.py:24
+
+
+class Policy(Enum):
+    """Same values as the reference enum (sched.py:27-42)."""
+    GITTINS = "gittins"
+    LSTF = "lstf"
+    FCFS_REQUEST = "fcfs-request"
+    FCFS_APP = "fcfs-app"
+    SRPT_MEAN = "srpt-mean"
+    EDF = "edf"
+    FAIR_SHARE = "fair-share"
+
+    @property
+    def needs_estimate(self) -> bool:
+        return self in (Policy.GITTINS, Policy.LSTF, Policy.SRPT_MEAN)
+
+    @property
+    def needs_deadline(self) -> bool:
+        return self in (Policy.LSTF, Policy.EDF)
+
+
+def _pv(policy) -> str:
+    return getattr(policy, "value", policy)
+
+
+class Priority(NamedTuple):
+    """Scheduling key; lower is served first (sched.py:184-192)."""
+    policy: object
+    key: float
+    tiebreak: tuple
+
+    def sort_key(self) -> tuple:
+        return (self.key, *self.tiebreak)
+
+
+@dataclass
+class RefreshResult:
+    refreshed: list
+    elapsed_ns: int
+    priorities: dict
+
+
+# ---------------------------------------------------------------------------
+# a1: batched rank (sched.py:102-129)
+# ---------------------------------------------------------------------------
+
+def gittins_rank_batch(values, probs, ages) -> np.ndarray:
+    """Gittins ranks of N aligned support rows; NaN marks exhausted rows."""
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
+    p = np.ascontiguousarray(np.asarray(probs, dtype=np.float64))
+    a = np.ascontiguousarray(np.asarray(ages, dtype=np.float64))
+    if v.ndim != 2 or p.shape != v.shape or a.shape != (v.shape[0],):
+        raise ValueError(f"shape mismatch: values {v.shape}, probs {p.shape}, ages {a.shape}")
+    n, b = v.shape
+    if n == 0:
+        return np.empty(0)
+    if b == 0:       # no support at all: every row is exhausted
+        return np.full(n, np.nan)
+    L = _lib.lib()
+    dev = torch.device("cuda")
+    tv = torch.from_numpy(v).to(dev, non_blocking=True)
+    tp = torch.from_numpy(p).to(dev, non_blocking=True)
+    ta = torch.from_numpy(a).to(dev, non_blocking=True)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    _lib.check(L.pdg_gittins_rank_f64(_lib.ptr(tv), _lib.ptr(tp), _lib.ptr(ta), n, b,
+                                      _lib.ptr(out), _lib.stream_ptr()),
+               "pdg_gittins_rank_f64")
+    return out.cpu().numpy()
+
+
+def gittins_rank_points(values: Sequence[float], probs: Sequence[float],
+                        age: float) -> float:
+    """Rank of one weighted discrete distribution (sched.py:88-99)."""
+    r = gittins_rank_batch(np.asarray(values, dtype=float)[None, :],
+                           np.asarray(probs, dtype=float)[None, :], np.array([age]))
+    if np.isnan(r[0]):
+        raise ExhaustedDistributionError(
+            f"no support point exceeds age {age}; distribution exhausted")
+    return float(r[0])
+
+
+def _samples_of(dist) -> list:
+    s = getattr(dist, "samples", dist)
+    return list(s)
+
+
+def gittins_rank(dist, age: float) -> float:
+    """Sample form (sched.py:51-85): the distinct samples weighted by
+    multiplicity form the support; same result as the reference's scan."""
+    samples = _samples_of(dist)
+    if not samples:
+        raise EstimationError("gittins_rank: empty distribution")
+    vals, cnt = np.unique(np.asarray(samples, dtype=float), return_counts=True)
+    return gittins_rank_points(vals, cnt / cnt.sum(), age)
+
+
+def lstf_slack(dist, age: float, deadline: float, now: float) -> float:
+    """Worst-case slack (sched.py:132-140)."""
+    samples = _samples_of(dist)
+    if not samples:
+        raise EstimationError("lstf_slack: empty distribution")
+    return deadline - now - (max(samples) - age)
+
+
+# ---------------------------------------------------------------------------
+# a3: single-instance priority (sched.py:195-234)
+# ---------------------------------------------------------------------------
+
+def compute_priority(policy, app, now: float,
+                     tenant_service: Optional[dict] = None,
+                     overrun_penalty_factor: float = OVERRUN_PENALTY_FACTOR) -> Priority:
+    tiebreak = (app.arrival_time, app.app_instance_id)
+    pv = _pv(policy)
+    if pv in ("fcfs-app", "fcfs-request"):
+        return Priority(policy, app.arrival_time, tiebreak)
+    if pv == "edf":
+        if app.deadline is None:
+            raise EstimationError(f"{app.app_instance_id}: EDF requires a deadline")
+        return Priority(policy, app.deadline, tiebreak)
+    if pv == "fair-share":
+        return Priority(policy, (tenant_service or {}).get(app.tenant_id, 0.0), tiebreak)
+    if app.remaining is None:
+        raise EstimationError(
+            f"{app.app_instance_id}: policy {pv} requires a demand estimate")
+    served_since = app.attained_service - app.estimate_age
+    if pv == "srpt-mean":
+        return Priority(policy, app.remaining.mean() - served_since, tiebreak)
+    if pv == "lstf":
+        if app.deadline is None:
+            raise EstimationError(f"{app.app_instance_id}: LSTF requires a deadline")
+        total = [s + app.estimate_age for s in app.remaining.samples]
+        return Priority(policy, lstf_slack(total, app.attained_service, app.deadline, now),
+                        tiebreak)
+    if pv == "gittins":
+        try:
+            key = gittins_rank_points(app.shifted_values, app.bucket_probs,
+                                      app.attained_service)
+        except ExhaustedDistributionError:
+            key = app.attained_service * overrun_penalty_factor
+            app.overrun_flagged = True
+        return Priority(policy, key, tiebreak)
+    raise ValueError(f"unknown policy {policy!r}")
+
+
+# ---------------------------------------------------------------------------
+# a2: batched periodic refresh (sched.py:244-318)
+# ---------------------------------------------------------------------------
+
+def refresh_priorities(live: Iterable, now: float, bucket_period: float,
+                       policy=Policy.GITTINS, tenant_service: Optional[dict] = None,
+                       overrun_penalty_factor: float = OVERRUN_PENALTY_FACTOR,
+                       force: bool = False) -> RefreshResult:
+    if bucket_period <= 0:
+        raise ValueError("bucket_period must be positive")
+    instances = list(live)
+    due = [a for a in instances
+           if force or a.observation_pending or (now - a.last_refresh) >= bucket_period]
+    priorities: dict = {}
+    start = time.perf_counter_ns()
+    rest = due
+    if _pv(policy) == "gittins" and due:
+        gapps = [a for a in due if a.remaining is not None]
+        rest = [a for a in due if a.remaining is None]
+        if gapps:
+            m = len(gapps)
+            width = max(a.bucket_width for a in gapps)
+            vals = np.zeros((m, width))
+            prbs = np.zeros((m, width))
+            for i, a in enumerate(gapps):     # ragged rows: pad with last value, 0 mass
+                k = a.bucket_width
+                vals[i, :k] = a.shifted_values
+                prbs[i, :k] = a.bucket_probs
+                if k < width:
+                    vals[i, k:] = vals[i, k - 1]
+            ages = np.fromiter((a.attained_service for a in gapps), float, m)
+            ranks = gittins_rank_batch(vals, prbs, ages)
+            nan = np.isnan(ranks)
+            if nan.any():
+                ranks = np.where(nan, ages * overrun_penalty_factor, ranks)
+                for a, flagged in zip(gapps, nan.tolist()):
+                    if flagged:
+                        a.overrun_flagged = True
+            for a, key in zip(gapps, ranks.tolist()):
+                priorities[a.app_instance_id] = Priority(policy, key, a.tiebreak)
+    for a in rest:
+        priorities[a.app_instance_id] = compute_priority(
+            policy, a, now, tenant_service, overrun_penalty_factor)
+    elapsed = time.perf_counter_ns() - start
+    for a in due:
+        a.last_refresh = now
+        a.observation_pending = False
+    return RefreshResult(refreshed=[a.app_instance_id for a in due], elapsed_ns=elapsed,
+                         priorities=priorities)
