@@ -80,14 +80,19 @@ int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* age,
                            uint64_t* out_key, void* stream);
 
 /* ---------------------------------------------------------------------------
- * K5  global order: sort packed 64-bit keys ascending, carrying a u32 payload
- * (the queue slot).  Replaces the Python min()/sort over _task_sort_key
- * (simcore.py:339-344, 512-516).  temp: device scratch of pdg_order_temp_bytes.
+ * K5  global order: stable radix sort of packed 64-bit keys ascending,
+ * carrying a u32 payload (the queue slot).  Replaces the Python min()/sort
+ * over _task_sort_key (simcore.py:339-344, 512-516).
+ * begin_bit = 0 sorts the full (key, tiebreak) word; begin_bit = 32 sorts the
+ * float key only and relies on stability -- valid when the input is already
+ * in arrival (tiebreak) order, e.g. slots filled in arrival order or the
+ * rank-major all-gather of arrival-ordered shards.
+ * temp: device scratch of pdg_order_temp_bytes(n) bytes.
  * ------------------------------------------------------------------------- */
 size_t pdg_order_temp_bytes(int64_t n);
 int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
               const uint32_t* slots_in, uint32_t* slots_out, int64_t n,
-              void* temp, size_t temp_bytes, void* stream);
+              int32_t begin_bit, void* temp, size_t temp_bytes, void* stream);
 
 #ifdef __cplusplus
 }

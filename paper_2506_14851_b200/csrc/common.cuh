@@ -34,11 +34,20 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 
+// Exact int -> double / u16 -> float without the XU conversion pipe.
+__device__ __forceinline__ double small_int_to_double(int j) {   // 0 <= j < 2^31
+  return dsub(__hiloint2double(0x43300000, j), 4503599627370496.0);
+}
+__device__ __forceinline__ float u16_to_float(uint32_t c) {       // c < 2^23
+  return __int_as_float(0x4B000000u | c) - 8388608.f;
+}
+
 // Bucket midpoint exactly as distributions.py:103,131 evaluates it:
 //   ((lo + j*w) + (lo + (j+1)*w)) / 2.0      (each op rounded separately)
 __device__ __forceinline__ double bucket_mid(double lo, double w, int j) {
-  double a = dadd(lo, dmul((double)j, w));
-  double b = dadd(lo, dmul((double)(j + 1), w));
+  const double jd = small_int_to_double(j);
+  double a = dadd(lo, dmul(jd, w));
+  double b = dadd(lo, dmul(dadd(jd, 1.0), w));
   return dmul(dadd(a, b), 0.5);
 }
 

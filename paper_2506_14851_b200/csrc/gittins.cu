@@ -95,47 +95,91 @@ __device__ __forceinline__ double exact_d(double lo, double w, double est,
   return dsub(dadd(bucket_mid(lo, w, j), est), age);
 }
 
-// One lane's segment of 8 consecutive buckets starting at j0.  Produces
-// integer masses and float32 offsets d for the alive buckets.  Values ascend,
-// so the alive buckets are a suffix; its first bucket i0 is located with
-// bit-exact float64 tests and d_i = d_{i0} + (i - i0)*w is then a sum of
-// positive terms, which float32 carries to ~1e-7 relative accuracy.
+// One lane's segment of 8 consecutive buckets starting at j0.  Produces float
+// masses (integer counts, exact) and float32 offsets d for the alive buckets.
+// Values ascend, so the alive buckets are a suffix; its first bucket i0 is
+// located with bit-exact float64 tests and d_i = d_{i0} + (i - i0)*w is then a
+// sum of positive terms, which float32 carries to ~1e-7 relative accuracy.
 __device__ __forceinline__ void lane_segment(const uint4 raw, int j0, int k,
                                              double lo, double w, double est,
-                                             double age, int (&m)[8],
+                                             double age, float (&m)[8],
                                              float (&d)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { m[i] = 0.f; d[i] = 0.f; }
+  if (j0 >= k) return;
+  const int last = min(7, k - 1 - j0);
   int i0 = 8;
   double d0 = 0.0;
-  if (j0 < k) {
-    const int last = min(7, k - 1 - j0);
-    const double ef = exact_d(lo, w, est, age, j0);
-    if (ef > 0.0) {
-      i0 = 0;
-      d0 = ef;
-    } else if (exact_d(lo, w, est, age, j0 + last) > 0.0) {
+  const double ef = exact_d(lo, w, est, age, j0);
+  if (ef > 0.0) {
+    i0 = 0;
+    d0 = ef;
+  } else if (exact_d(lo, w, est, age, j0 + last) > 0.0) {
 #pragma unroll 1
-      for (int i = 1; i <= last; ++i) {
-        const double e = exact_d(lo, w, est, age, j0 + i);
-        if (e > 0.0) { i0 = i; d0 = e; break; }
-      }
-    }
-    if (i0 < 8) {
-      // buckets past the row's last real bucket are excluded (they would be
-      // zero-mass padding in the reference, sched.py:282-291)
-      const float df = float(d0), wf = float(w);
-      const uint32_t wd[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int c = int((wd[i >> 1] >> (16 * (i & 1))) & 0xffffu);
-        const bool on = (i >= i0) && (i <= last);
-        m[i] = on ? c : 0;
-        d[i] = on ? fmaf(float(i - i0), wf, df) : 0.f;
-      }
-      return;
+    for (int i = 1; i <= last; ++i) {
+      const double e = exact_d(lo, w, est, age, j0 + i);
+      if (e > 0.0) { i0 = i; d0 = e; break; }
     }
   }
+  if (i0 == 8) return;
+  // buckets past the row's last real bucket are excluded (they would be
+  // zero-mass padding in the reference, sched.py:282-291)
+  const float df = float(d0), wf = float(w), fi0 = float(i0);
+  const uint32_t wd[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-  for (int i = 0; i < 8; ++i) { m[i] = 0; d[i] = 0.f; }
+  for (int i = 0; i < 8; ++i) {
+    const float c = u16_to_float((wd[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+    const bool on = (i >= i0) && (i <= last);
+    m[i] = on ? c : 0.f;
+    d[i] = on ? fmaf(float(i) - fi0, wf, df) : 0.f;
+  }
+}
+
+// Gittins key of one row held as CH chunks of 8 buckets per lane (chunk c,
+// lane l owns buckets 256c + 8l .. +7).  Masses are integer-valued floats, so
+// S (prefix mass), Z and T = Z - S are exact; P (prefix of m*d) is a float32
+// sum of positive terms.  The min over buckets of (P + d*T)/S is tracked as a
+// fraction (cross-multiplied compares) so each lane divides once.
+template <int CH>
+__device__ __forceinline__ float row_key(const float (&m)[CH][8], const float (&d)[CH][8],
+                                         int lane, bool& exhausted) {
+  float lm[CH], lp[CH], z = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    float sm = 0.f, sp = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { sm += m[c][i]; sp = fmaf(m[c][i], d[c][i], sp); }
+    lm[c] = sm;
+    lp[c] = sp;
+    z += sm;
+  }
+  const float Z = warp_sum(z);
+  exhausted = !(Z > 0.f);
+  if (exhausted) return 0.f;
+  float s_carry = 0.f, p_carry = 0.f, bn = 1.f, bd = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const float s_incl = warp_incl_scan(lm[c], lane);
+    const float p_incl = warp_incl_scan(lp[c], lane);
+    float S = s_carry + (s_incl - lm[c]);
+    float P = p_carry + (p_incl - lp[c]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float mi = m[c][i];
+      S += mi;
+      P = fmaf(mi, d[c][i], P);
+      // zero-mass buckets never beat the previous positive one (and give
+      // +inf before any mass), so only positive-mass buckets are candidates
+      const float num = fmaf(d[c][i], Z - S, P);
+      const bool take = (mi > 0.f) && (num * bd < bn * S);
+      bn = take ? num : bn;
+      bd = take ? S : bd;
+    }
+    s_carry += __shfl_sync(kFull, s_incl, 31);
+    p_carry += __shfl_sync(kFull, p_incl, 31);
+  }
+  const float r = bd > 0.f ? __fdiv_rn(bn, bd) : __int_as_float(0x7f800000);
+  return warp_min(r);
 }
 
 template <int CH>   // row holds up to 256*CH buckets
@@ -148,76 +192,39 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
   // software pipeline: counts of the next row are in flight while the current
   // row is scored
   uint4 nxt[CH];
-  auto load = [&](int64_t r, uint4 (&dst)[CH]) {
+  int knxt;
+  auto load = [&](int64_t r, uint4 (&dst)[CH], int& kk) {
     const uint4* row = reinterpret_cast<const uint4*>(a.counts + r * a.stride);
-    const int k = __ldg(a.nbins + r);
+    kk = __ldg(a.nbins + r);
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const int j0 = 256 * c + 8 * lane;
-      dst[c] = (j0 < k) ? __ldcs(row + 32 * c + lane) : make_uint4(0, 0, 0, 0);
+      dst[c] = (j0 < kk) ? __ldcs(row + 32 * c + lane) : make_uint4(0, 0, 0, 0);
     }
   };
-  load(gw, nxt);
+  load(gw, nxt, knxt);
   for (int64_t r = gw; r < a.n; r += nw) {
     uint4 cur[CH];
 #pragma unroll
     for (int c = 0; c < CH; ++c) cur[c] = nxt[c];
+    const int k = knxt;
     const double lo = __ldg(a.lo + r), w = __ldg(a.width + r);
     const double est = __ldg(a.est + r), age = __ldg(a.age + r);
-    const int k = __ldg(a.nbins + r);
-    if (r + nw < a.n) load(r + nw, nxt);
+    if (r + nw < a.n) load(r + nw, nxt, knxt);
 
-    int m[CH][8];
-    float d[CH][8];
-    int lane_m[CH];
-    float lane_pv[CH];
-    int ztot = 0;
+    float m[CH][8], d[CH][8];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
+    for (int c = 0; c < CH; ++c)
       lane_segment(cur[c], 256 * c + 8 * lane, k, lo, w, est, age, m[c], d[c]);
-      int sm = 0;
-      float sp = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) { sm += m[c][i]; sp = fmaf(float(m[c][i]), d[c][i], sp); }
-      lane_m[c] = sm;
-      lane_pv[c] = sp;
-      ztot += sm;
-    }
-    const int Z = warp_sum(ztot);
-    float key;
+    bool exhausted;
+    float key = row_key<CH>(m, d, lane, exhausted);
     uint8_t flags = 0;
-    if (Z <= 0) {                                   // exhausted: sched.py:295-300
+    if (exhausted) {                                 // sched.py:295-300
       key = float(dmul(age, a.penalty));
       flags = PDG_FLAG_OVERRUN;
-    } else {
-      int s_carry = 0;
-      float pv_carry = 0.f;
-      float best = __int_as_float(0x7f800000);
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int s_incl = warp_incl_scan(lane_m[c], lane);
-        const float pv_incl = warp_incl_scan(lane_pv[c], lane);
-        int S = s_carry + s_incl - lane_m[c];
-        float Pv = pv_carry + (pv_incl - lane_pv[c]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int mi = m[c][i];
-          S += mi;
-          Pv = fmaf(float(mi), d[c][i], Pv);
-          // zero-mass buckets never beat the previous positive one (and give
-          // +inf before any mass), so only positive-mass buckets are scored
-          if (mi > 0) {
-            const float T = float(Z - S);
-            best = fminf(best, __fdiv_rn(fmaf(d[c][i], T, Pv), float(S)));
-          }
-        }
-        s_carry += __shfl_sync(kFull, s_incl, 31);
-        pv_carry += __shfl_sync(kFull, pv_incl, 31);
-      }
-      key = warp_min(best);
     }
     if (lane == 0) {
-      if (!(key > 0.f)) key = 0.f;                  // canonical +0 for the sort key
+      if (!(key > 0.f)) key = 0.f;                   // canonical +0 for the sort key
       if (a.out_f32) a.out_f32[r] = key;
       if (a.out_flags) a.out_flags[r] = flags;
       if (a.out_key) {
@@ -293,9 +300,14 @@ extern "C" size_t pdg_order_temp_bytes(int64_t n) {
 
 extern "C" int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
                          const uint32_t* slots_in, uint32_t* slots_out, int64_t n,
-                         void* temp, size_t temp_bytes, void* stream) {
+                         int32_t begin_bit, void* temp, size_t temp_bytes,
+                         void* stream) {
   if (n < 0 || (n > 0 && (!keys_in || !keys_out || !slots_in || !slots_out || !temp))) {
     set_error("pdg_order: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (begin_bit != 0 && begin_bit != 32) {
+    set_error("pdg_order: begin_bit must be 0 or 32");
     return PDG_EINVAL;
   }
   if (n == 0) return PDG_OK;
@@ -305,7 +317,7 @@ extern "C" int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
     return PDG_EINVAL;
   }
   cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out,
-                                                  slots_in, slots_out, n, 0, 64,
+                                                  slots_in, slots_out, n, begin_bit, 64,
                                                   (cudaStream_t)stream);
   return cuda_status(e, "pdg_order");
 }

@@ -106,12 +106,18 @@ class HistQueue:
             _lib.ptr(self.keys) if keys else None, _lib.stream_ptr(stream)),
             "pdg_gittins_score_hist")
 
-    def order(self, n: Optional[int] = None, stream=None) -> torch.Tensor:
-        """K5 (single GPU): queue slots sorted by (key, arrival order)."""
+    def order(self, n: Optional[int] = None, stream=None,
+              arrival_ordered: bool = False) -> torch.Tensor:
+        """K5 (single GPU): queue slots sorted by (key, arrival order).
+
+        arrival_ordered=True asserts slot order == arrival order, so a stable
+        sort on the 32-bit key alone yields the same order in half the passes.
+        """
         n = self.n if n is None else int(n)
         L = _lib.lib()
         _lib.check(L.pdg_order(_lib.ptr(self.keys), _lib.ptr(self.sorted_keys),
                                _lib.ptr(self.slots), _lib.ptr(self.sorted_slots), n,
+                               32 if arrival_ordered else 0,
                                _lib.ptr(self._temp), self._temp.numel(),
                                _lib.stream_ptr(stream)), "pdg_order")
         return self.sorted_slots[:n]
