@@ -94,6 +94,66 @@ int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
               const uint32_t* slots_in, uint32_t* slots_out, int64_t n,
               int32_t begin_bit, void* temp, size_t temp_bytes, void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * K2 + K3 + a4  demand engine.
+ * Replaces pdgsim.estimator.monte_carlo_remaining_demand (estimator.py:305-362)
+ * including _conditioning_for / conditional_filter (estimator.py:155-233,
+ * 289-302), and ApplicationInstance.set_remaining's bucketing
+ * (sched.py:170-181, distributions.py:79-105).  For the same graph, current
+ * unit, relevant observation, n and seed the samples are bit-identical to the
+ * reference (numpy PCG64 stream reproduced by position).
+ *
+ * The graph bank is compiled by paper_2506_14851_b200/graphs.py; its record
+ * layouts (64-byte unit descriptor, K3 condition/pair records) are private to
+ * that compiler and engine.cu.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const void* units;              /* unit descriptors, 64 B each            */
+  const int32_t* graph_base;      /* [G] first unit of each graph           */
+  const int32_t* graph_n;         /* [G] units per graph (<= 32)            */
+  const int32_t* unit_capacity;   /* [U] FIFO capacity (kept-list cap, K3)  */
+  const double* vals;             /* sample pools (float64)                 */
+  const int32_t* pool_off;        /* own-input per-bucket output pools      */
+  const int32_t* pool_len;
+  const double* succ_cum;         /* cumulative successor probabilities     */
+  const int32_t* succ_nxt;        /* next local unit, -1 = terminate        */
+  const void* conds;              /* K3 (unit, upstream) descriptors        */
+  const void* pairs;              /* K3 joined records                      */
+  const uint64_t* jump;           /* PCG64 jump tables [2][1024][4]         */
+  double prefill_rate, decode_rate; /* RateProfile (pdgraph.py:282-291)     */
+} pdg_graph_bank;
+
+typedef struct {
+  const int32_t* graph;           /* [N] graph index in the bank                      */
+  const int32_t* unit;            /* [N] current unit (index in sorted unit ids)      */
+  const uint64_t* seed;           /* [N] np.random.default_rng seed (>= 0)           */
+  const int32_t* obs_unit;        /* [N] relevant observed upstream unit, -1 = none   */
+  const double* obs_val;          /* [N,3] (input_len, output_len, parallelism)      */
+} pdg_mc_jobs;
+
+typedef struct {
+  double* samples;                /* [N, samples_stride] optional raw samples         */
+  int64_t samples_stride;
+  double* lo;                     /* histogram rows (pdg_hist_rows layout)            */
+  double* width;
+  int32_t* nbins;
+  int32_t* nsamp;
+  uint16_t* counts;
+  int64_t stride;
+  const int32_t* slot;            /* [N] row written for job i (NULL: row i)          */
+  int32_t* capped;                /* [N] walks that hit the visit cap (optional)      */
+  uint8_t* flags;                 /* [N] bit0 conditioned, bit1 override present      */
+} pdg_mc_out;
+
+int pdg_mc_grid_warps(void);
+size_t pdg_mc_scratch_bytes(int32_t n_samples, int32_t max_pairs, int32_t grid_warps);
+int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_jobs* jobs,
+                            int64_t n_jobs, int32_t n_samples, int32_t visit_cap,
+                            int32_t bucket_count, int32_t max_unit_k, int32_t max_pairs,
+                            const pdg_mc_out* out, void* scratch, size_t scratch_bytes,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

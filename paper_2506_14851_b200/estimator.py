@@ -1,0 +1,210 @@
+"""GPU demand engine: drop-in for ``pdgsim.estimator.monte_carlo_remaining_demand``
+(estimator.py:305-362) and the batched, device-resident form behind it.
+
+``DemandEngine.run`` estimates many applications in one launch (one warp per
+application, kernel ``mc_engine_kernel``); each job is (graph, current unit,
+relevant observation, seed).  Outputs are the raw samples (optional) and the
+``set_remaining`` histogram rows (bucket grid + u16 counts) written straight
+into a :class:`~paper_2506_14851_b200.queue.HistQueue`, where K1 scores them.
+
+The drop-in ``monte_carlo_remaining_demand`` keeps the reference signature and
+returns a ``RemainingDemand`` whose samples are bit-identical to the
+reference's for the same inputs.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import EstimationError
+from .graphs import GraphBank, jump_tables
+
+WALK_VISIT_CAP = 64
+
+
+class GraphBankC(C.Structure):
+    _fields_ = [("units", C.c_void_p), ("graph_base", C.c_void_p), ("graph_n", C.c_void_p),
+                ("unit_capacity", C.c_void_p), ("vals", C.c_void_p),
+                ("pool_off", C.c_void_p), ("pool_len", C.c_void_p),
+                ("succ_cum", C.c_void_p), ("succ_nxt", C.c_void_p), ("conds", C.c_void_p),
+                ("pairs", C.c_void_p), ("jump", C.c_void_p), ("prefill_rate", C.c_double),
+                ("decode_rate", C.c_double)]
+
+
+class JobsC(C.Structure):
+    _fields_ = [("graph", C.c_void_p), ("unit", C.c_void_p), ("seed", C.c_void_p),
+                ("obs_unit", C.c_void_p), ("obs_val", C.c_void_p)]
+
+
+class OutC(C.Structure):
+    _fields_ = [("samples", C.c_void_p), ("samples_stride", C.c_int64), ("lo", C.c_void_p),
+                ("width", C.c_void_p), ("nbins", C.c_void_p), ("nsamp", C.c_void_p),
+                ("counts", C.c_void_p), ("stride", C.c_int64), ("slot", C.c_void_p),
+                ("capped", C.c_void_p), ("flags", C.c_void_p)]
+
+
+_JUMP = {}
+
+
+def _jump_tensor(device) -> torch.Tensor:
+    key = str(device)
+    if key not in _JUMP:
+        _JUMP[key] = torch.from_numpy(jump_tables().view(np.int64).reshape(-1).copy()).to(device)
+    return _JUMP[key]
+
+
+@dataclass
+class RemainingDemand:
+    """Mirror of the reference result type (estimator.py:40-59)."""
+    samples: list
+    sample_count: int
+    conditioned: bool = False
+    capped_walks: int = 0
+    hist: Optional[tuple] = field(default=None, repr=False)   # (lo, width, k, counts) from the GPU
+
+    def __post_init__(self):
+        if self.sample_count != len(self.samples) or self.sample_count <= 0:
+            raise EstimationError("sample_count must equal len(samples) and be > 0")
+
+    def mean(self) -> float:
+        return sum(self.samples) / self.sample_count
+
+    def max(self) -> float:
+        return max(self.samples)
+
+
+class DemandEngine:
+    """Resident graph bank + launch wrapper for K2/K3/a4."""
+
+    def __init__(self, graphs: dict, prefill_rate: float = 10000.0, decode_rate: float = 50.0,
+                 device: str = "cuda"):
+        _lib.lib()
+        self.device = torch.device(device)
+        self.bank = GraphBank(graphs, device=device)
+        b = self.bank
+        caps = [b.capacity[nm][uid] for nm in b.names for uid in b.unit_order[nm]]
+        self.unit_capacity = torch.tensor(caps or [1000], dtype=torch.int32, device=self.device)
+        self.jump = _jump_tensor(self.device)
+        self.c_bank = GraphBankC(
+            _lib.ptr(b.units), _lib.ptr(b.graph_base), _lib.ptr(b.graph_n),
+            _lib.ptr(self.unit_capacity), _lib.ptr(b.vals), _lib.ptr(b.pool_off),
+            _lib.ptr(b.pool_len), _lib.ptr(b.succ_cum), _lib.ptr(b.succ_nxt),
+            _lib.ptr(b.conds), _lib.ptr(b.pairs), _lib.ptr(self.jump),
+            float(prefill_rate), float(decode_rate))
+        hu = b.host_units
+        self.max_unit_k = int(hu["ib_k"].max()) if len(hu) else 1
+        self.max_pairs = int(b.host_conds["pair_len"].max()) if len(b.host_conds) else 0
+        self._scratch = None
+
+    # -- job marshalling ------------------------------------------------------
+    def relevant_observation(self, name: str, current: str, observations) -> tuple[int, tuple]:
+        """Latest observation whose unit lists `current` as a successor
+        (estimator.py:295-298); returns (local upstream index or -1, values)."""
+        g = self.bank.graphs[name]
+        for obs in reversed(list(observations)):
+            up = g.units.get(obs.unit_id)
+            if up is None or current not in up.successors:
+                continue
+            return (self.bank.local_unit(name, obs.unit_id),
+                    (float(obs.input_len), float(obs.output_len), float(obs.parallelism)))
+        return -1, (0.0, 0.0, 0.0)
+
+    def _scratch_for(self, n: int) -> torch.Tensor:
+        L = _lib.lib()
+        need = int(L.pdg_mc_scratch_bytes(n, self.max_pairs, L.pdg_mc_grid_warps()))
+        if self._scratch is None or self._scratch.numel() < need:
+            self._scratch = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+        return self._scratch
+
+    def run(self, graph_idx, unit_idx, seeds, obs_unit=None, obs_val=None, *, n: int,
+            bucket_count: int, visit_cap: int = WALK_VISIT_CAP, queue=None, slots=None,
+            samples: bool = False, stream=None):
+        """Launch the engine on device-resident job arrays (torch tensors).
+
+        Writes histogram rows into `queue` (HistQueue) at `slots` (default:
+        rows 0..N-1).  Returns dict(samples=[N,n] f64 or None, capped, flags).
+        """
+        if n < 1:
+            raise EstimationError(f"sample count must be >= 1, got {n}")
+        if queue is not None and n > 65535:
+            raise EstimationError("u16 histogram counts need n <= 65535")
+        N = int(graph_idx.numel())
+        dev = self.device
+        out_samples = torch.empty((N, n), dtype=torch.float64, device=dev) if samples else None
+        capped = torch.empty(N, dtype=torch.int32, device=dev)
+        flags = torch.empty(N, dtype=torch.uint8, device=dev)
+        if queue is None:
+            from .queue import HistQueue
+            queue = HistQueue(max(N, 1), max(bucket_count, 1), device=str(dev))
+        if bucket_count > queue.stride:
+            raise ValueError("queue rows narrower than bucket_count")
+        jobs = JobsC(_lib.ptr(graph_idx), _lib.ptr(unit_idx), _lib.ptr(seeds),
+                     _lib.ptr(obs_unit), _lib.ptr(obs_val))
+        out = OutC(_lib.ptr(out_samples), n, _lib.ptr(queue.lo), _lib.ptr(queue.width),
+                   _lib.ptr(queue.nbins), _lib.ptr(queue.nsamp), _lib.ptr(queue.counts),
+                   queue.stride, _lib.ptr(slots), _lib.ptr(capped), _lib.ptr(flags))
+        scratch = self._scratch_for(n)
+        L = _lib.lib()
+        _lib.check(L.pdg_mc_remaining_demand(
+            C.byref(self.c_bank), C.byref(jobs), N, n, visit_cap, bucket_count,
+            self.max_unit_k, self.max_pairs, C.byref(out), _lib.ptr(scratch),
+            scratch.numel(), _lib.stream_ptr(stream)), "pdg_mc_remaining_demand")
+        if slots is None:
+            queue.n = max(queue.n, N)
+        return {"samples": out_samples, "capped": capped, "flags": flags, "queue": queue}
+
+
+# ---------------------------------------------------------------------------
+# drop-in single-application API (estimator.py:305-362)
+# ---------------------------------------------------------------------------
+
+_ENGINES: dict = {}
+
+
+def _fingerprint(graph) -> tuple:
+    return tuple((uid, len(u.records)) for uid, u in sorted(graph.units.items()))
+
+
+def engine_for(graph, env) -> tuple[DemandEngine, str]:
+    key = (id(graph), float(env.prefill_rate), float(env.decode_rate))
+    fp = _fingerprint(graph)
+    hit = _ENGINES.get(key)
+    if hit is None or hit[1] != fp:
+        eng = DemandEngine({"g": graph}, env.prefill_rate, env.decode_rate)
+        _ENGINES[key] = (eng, fp, graph)
+        hit = _ENGINES[key]
+    return hit[0], "g"
+
+
+def monte_carlo_remaining_demand(graph, current_unit: str, observations: Sequence, env,
+                                 n: int, seed: int,
+                                 visit_cap: int = WALK_VISIT_CAP) -> RemainingDemand:
+    """Same contract as the reference; computed by the sm_100a engine."""
+    if n < 1:
+        raise EstimationError(f"sample count must be >= 1, got {n}")
+    if current_unit not in graph.units:
+        raise EstimationError(f"unknown unit {current_unit!r}")
+    eng, name = engine_for(graph, env)
+    dev = eng.device
+    up, vals = eng.relevant_observation(name, current_unit, observations)
+    t = lambda a, dt: torch.tensor(a, dtype=dt, device=dev)  # noqa: E731
+    k = 1  # histogram not needed by the drop-in caller; smallest row
+    res = eng.run(t([0], torch.int32), t([eng.bank.local_unit(name, current_unit)], torch.int32),
+                  t([int(seed)], torch.int64), t([up], torch.int32),
+                  t([list(vals)], torch.float64), n=n, bucket_count=k, visit_cap=visit_cap,
+                  samples=True)
+    s = res["samples"][0].cpu().numpy()
+    capped = int(res["capped"][0].item())
+    flags = int(res["flags"][0].item())
+    if capped:
+        import logging
+        logging.getLogger(__name__).warning(
+            "%d of %d walks hit the %d-visit cap", capped, n, visit_cap)
+    return RemainingDemand(samples=s.tolist(), sample_count=n, conditioned=bool(flags & 1),
+                           capped_walks=capped)
