@@ -2,21 +2,27 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N=1 workload is BASELINE config 2 ("100k queued apps, depth-8 PDGraphs,
-256-bin demand histograms, full re-score on 1 B200"); under torchrun each rank
-re-scores its own 100k-app shard (weak scaling) and the packed (key, arrival
-position) pairs are all-gathered over NCCL for the global order (config 3's
-exchange step).
+Workload = BASELINE config 2: "100k queued apps, depth-8 PDGraphs, 256-bin
+demand histograms, full re-score on 1 B200".  Every app owns its own depth-8
+PDGraph (tools/synth.py: chain + 3-way branch + self-loop + back-edge loop,
+256 lognormal duration records per unit) and sits at a random unit with a
+random amount of service attained.  Under torchrun each rank re-scores its
+own 100k-app shard (weak scaling) and the packed (key, arrival position)
+pairs are all-gathered over NCCL for the global order (config 3's exchange).
 
-A step = full re-score of the queue: K1b Gittins scorer over every resident
-histogram row (+ overrun penalty + packed sort key) followed by the global
-order (radix sort of the packed keys).  Synthetic data (seeded) -- there is
-no dataset; histograms are multinomial draws of n=512 samples over 256
-equal-width buckets, ages span the whole support (some rows exhausted).
+One step = full re-score of the queue, the reference's policy runtime
+(monte_carlo_remaining_demand(n=512) +
+set_remaining(256) + one gittins_rank_batch row per app) plus the global
+order:
+  K2/a4  mc_engine_kernel     512-walk Monte Carlo from the current unit,
+                              bit-identical to the reference, bucketed to 256
+  K1b    gittins_hist_kernel  Gittins key + overrun penalty + packed sort key
+  K5     radix sort           global order (after the all-gather when N > 1)
+Each step uses fresh per-app seeds (a genuine re-estimate, nothing cached).
 
-Timing: W warm-up steps, then K timed steps; each step is bracketed by CUDA
-events on the launching stream; L2 is flushed (256 MiB write) between steps,
-outside the events.  The step time is the max over ranks.
+Timing: W warm-up steps, then K timed steps, each bracketed by CUDA events on
+the launching stream; L2 flushed (256 MiB write) between steps outside the
+events (the 1.6 GB graph bank exceeds L2 anyway); step time = max over ranks.
 """
 
 from __future__ import annotations
@@ -39,17 +45,21 @@ UNIT = "apps/s"
 N_APPS = 100_000
 N_BINS = 256
 N_SAMP = 512
+N_REC = 256
+VISIT_CAP = 64
 PENALTY = 2.0
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--apps", type=int, default=N_APPS)
     ap.add_argument("--bins", type=int, default=N_BINS)
+    ap.add_argument("--cpu-apps", type=int, default=1200,
+                    help="apps in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true",
                     help="profiling run: skip CUPTI launch counting, e2e and CPU legs")
@@ -57,75 +67,66 @@ def parse():
 
 
 # ---------------------------------------------------------------------------
-# synthetic workload (host numpy; identical generator for both arms)
+# queue state shared by both arms
 # ---------------------------------------------------------------------------
 
-def make_rows(n, b, seed):
-    rng = np.random.default_rng(seed)
-    lo = rng.uniform(0.0, 600.0, n)
-    w = rng.lognormal(-0.5, 1.0, n)
-    est = rng.uniform(0.0, 300.0, n)
-    # each row: a mixture of two bumps over the bucket grid, n=512 samples
-    j = np.arange(b)
-    c1 = rng.uniform(0, b, n)[:, None]
-    c2 = rng.uniform(0, b, n)[:, None]
-    s1 = rng.uniform(2, b / 4, n)[:, None]
-    s2 = rng.uniform(2, b / 4, n)[:, None]
-    mix = rng.uniform(0.2, 0.8, n)[:, None]
-    pr = mix * np.exp(-0.5 * ((j - c1) / s1) ** 2) + (1 - mix) * np.exp(-0.5 * ((j - c2) / s2) ** 2)
-    pr /= pr.sum(axis=1, keepdims=True)
-    cdf = np.cumsum(pr, axis=1)
-    cdf[:, -1] = 1.0
-    off = np.arange(n, dtype=np.float64)[:, None]
-    u = rng.random((n, N_SAMP))
-    flat = np.searchsorted((cdf + off).ravel(), (u + off).ravel(), side="right")
-    idx = np.minimum(flat.reshape(n, N_SAMP) - (np.arange(n) * b)[:, None], b - 1)
-    counts = np.zeros((n, b), dtype=np.int64)
-    np.add.at(counts, (np.repeat(np.arange(n), N_SAMP), idx.ravel()), 1)
-    nb = np.full(n, b)
-    age = est + rng.uniform(0.0, 1.05, n) * (b * w)
-    return dict(lo=lo, width=w, est_age=est, nbins=nb, nsamp=np.full(n, N_SAMP),
-                counts=counts, age=age)
+def reachable_units(u: int) -> int:
+    """Units reachable from unit u in the synth template (tools/synth.py)."""
+    return {0: 8, 1: 7, 2: 6, 3: 5, 4: 5, 5: 5, 6: 2, 7: 1}[int(u)]
 
 
-def oracle_values(rows):
-    b = rows["counts"].shape[1]
-    j = np.arange(b, dtype=np.float64)
-    lo, w = rows["lo"][:, None], rows["width"][:, None]
-    v = ((lo + j * w) + (lo + (j + 1.0) * w)) / 2.0 + rows["est_age"][:, None]
-    return v, rows["counts"] / rows["nsamp"][:, None].astype(np.float64)
+def ages_for(rng, n, mean_rem, max_rem):
+    """est_age (attained service at the estimate) and age now: served since the
+    estimate ~ U(0, 0.9) x E[remaining]; 1% forced exhausted."""
+    est = rng.uniform(0.0, 200.0, n)
+    age = est + rng.uniform(0.0, 0.9, n) * mean_rem
+    ex = rng.random(n) < 0.01
+    age[ex] = est[ex] + 1.01 * max_rem[ex]
+    return est, age
 
 
 # ---------------------------------------------------------------------------
-# CPU (oracle port) timing: used by the cpu_baseline object and --impl reference
+# CPU (oracle port) timing: cpu_baseline object and --impl reference
 # ---------------------------------------------------------------------------
 
-def _cpu_chunk(args):
-    rows, reps = args
+def _cpu_worker(args):
+    """Full re-score of apps [lo, hi) of the synthetic shard on one core:
+    MC(n=512) + bucketize(256) + Gittins row + penalty (the reference policy
+    runtime, restated by the oracle)."""
+    lo_i, hi_i, n_apps, seed, bins = args
     from oracle import pdg_oracle as O
-    v, p = oracle_values(rows)
+    from tools import synth
+    w = synth.make(n_apps, N_REC, seed=seed)
+    jb = synth.jobs(n_apps, seed=seed + 1)
+    rng = np.random.default_rng(seed + 2)
+    graphs = [O.graph_from_kb(synth.kb_doc(w, a)) for a in range(lo_i, hi_i)]
     t0 = time.perf_counter()
-    for _ in range(reps):
-        r = O.gittins_rank_batch(v, p, rows["age"])
-        r = np.where(np.isnan(r), rows["age"] * PENALTY, r)
-        np.lexsort((np.arange(len(r)), r))
-    return (time.perf_counter() - t0) / reps
+    keys = []
+    for g, a in zip(graphs, range(lo_i, hi_i)):
+        r = O.mc_remaining_demand(g, f"s{jb['unit'][a]}", [], N_SAMP, int(jb["seed"][a]),
+                                  VISIT_CAP)
+        b = O.bucketize(r.samples.tolist(), bins)
+        est = float(rng.uniform(0, 200))
+        age = est + float(rng.uniform(0, 0.9)) * float(r.samples.mean())
+        v = b.midpoints() + est
+        k = O.gittins_rank_batch(v[None], b.probs[None], np.array([age]))[0]
+        keys.append(age * PENALTY if np.isnan(k) else k)
+    np.lexsort((np.arange(len(keys)), np.asarray(keys)))
+    return time.perf_counter() - t0, hi_i - lo_i
 
 
-def cpu_rate(sample_rows, procs):
-    """apps/s of the oracle port over `sample_rows`, sharded over `procs` processes."""
-    n = len(sample_rows["lo"])
+def cpu_rate(sample_apps, procs, n_apps, seed, bins):
     if procs <= 1:
-        return n / _cpu_chunk((sample_rows, 1))
+        dt, m = _cpu_worker((0, sample_apps, max(n_apps, sample_apps), seed, bins))
+        return m / dt
     import multiprocessing as mp
-    parts = np.array_split(np.arange(n), procs)
-    chunks = [({k: v[p] for k, v in sample_rows.items()}, 1) for p in parts]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(procs) as pool:
-        t0 = time.perf_counter()
-        pool.map(_cpu_chunk, chunks)
-        dt = time.perf_counter() - t0
-    return n / dt
+    edges = np.linspace(0, sample_apps, procs + 1).astype(int)
+    tasks = [(int(a), int(b), max(n_apps, sample_apps), seed, bins)
+             for a, b in zip(edges[:-1], edges[1:]) if b > a]
+    with mp.get_context("fork").Pool(len(tasks)) as pool:
+        res = pool.map(_cpu_worker, tasks)
+    # the shards run concurrently: wall = slowest shard's compute time
+    return sum(m for _, m in res) / max(dt for dt, _ in res)
 
 
 def run_reference(args):
@@ -133,27 +134,24 @@ def run_reference(args):
     if rank != 0:
         return
     procs = os.cpu_count() or 1
-    sample = min(args.apps, 20_000)
-    rows = make_rows(sample, args.bins, seed=1)
+    sample = max(procs * 40, 80)
     for _ in range(max(args.warmup, 1)):
-        cpu_rate(rows, procs)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cpu_rate(rows, procs)
-        times.append(time.perf_counter() - t0)
-    ms = float(np.median(times)) * 1e3
-    val = sample / (ms / 1e3)
+        cpu_rate(min(sample, procs * 4), procs, sample, 1000, args.bins)
+    rates = [cpu_rate(sample, procs, sample, 1000 + s, args.bins) for s in range(args.steps)]
+    val = float(np.median(rates))
+    ms = args.apps / val * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2: full Gittins re-score of a 256-bucket queue",
-                   "apps": args.apps, "bins": args.bins, "samples_per_hist": N_SAMP},
+        "config": {"workload": "config2: full re-score (MC n=512 + 256-bucket Gittins) of a "
+                               "100k-app queue of depth-8 PDGraphs",
+                   "apps": args.apps, "bins": args.bins, "samples_per_app": N_SAMP},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{sample} apps per step (of {args.apps}), numpy "
-                                   f"gittins_rank_batch + penalty + lexsort, {procs} procs"},
+                         "sample": f"{sample} apps per step (bounded sample of the {args.apps}-app "
+                                   f"shard), oracle MC+bucketize+Gittins, {procs} processes; "
+                                   f"ms_per_step extrapolated to {args.apps} apps"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -229,14 +227,26 @@ def measured_peaks():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel):
+def ncu_summary(kernel):
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            d = json.load(fh)
-        return d[kernel]["dram_bytes_per_launch"], d[kernel].get("apps_per_launch")
-    except (OSError, KeyError, ValueError):
-        return None, None
+            return json.load(fh).get(kernel, {})
+    except (OSError, ValueError):
+        return {}
+
+
+def count_launches(step):
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step(0)
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+    ours = [nm for nm in names if ("pdg" in nm or "gittins" in nm or "mc_engine" in nm
+                                   or "Radix" in nm or "cub" in nm.lower())]
+    return len(ours), sorted(set(ours))
 
 
 # ---------------------------------------------------------------------------
@@ -248,7 +258,9 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2506_14851_b200 import _lib
+    from paper_2506_14851_b200.estimator import DemandEngine
     from paper_2506_14851_b200.queue import HistQueue
+    from tools import synth
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -260,11 +272,29 @@ def run_ours(args):
     L = _lib.lib()
     n, b = args.apps, args.bins
 
-    rows = make_rows(n, b, seed=1000 + rank)
+    # ---- resident state: graph bank + queue + per-app job state ----------
+    w = synth.make(n, N_REC, seed=1000 + rank)
+    eng = DemandEngine(synth.bank(w, device=str(dev)), device=str(dev))
+    jb = synth.jobs(n, seed=1001 + rank)
     q = HistQueue(n, b)
-    gtb = (rank * n + np.arange(n)).astype(np.int64)          # global arrival position
-    q.load_rows(rows["lo"], rows["width"], rows["est_age"], rows["nbins"], rows["nsamp"],
-                rows["counts"], age=rows["age"], tiebreak=gtb)
+    g_idx = torch.arange(n, dtype=torch.int32, device=dev)
+    u_idx = torch.from_numpy(jb["unit"]).to(dev)
+    seeds0 = torch.from_numpy(jb["seed"]).to(dev)
+    seeds = seeds0.clone()
+    # attained service: drawn once from the first estimate's mean / max
+    eng.run(g_idx, u_idx, seeds, n=N_SAMP, bucket_count=b, visit_cap=VISIT_CAP, queue=q)
+    torch.cuda.synchronize()
+    k = q.nbins[:n].double()
+    j = torch.arange(q.stride, device=dev, dtype=torch.float64)
+    mids = q.lo[:n, None] + (j[None, :] + 0.5) * q.width[:n, None]
+    mean_rem = ((q.counts[:n].double() * mids).sum(1) / N_SAMP).cpu().numpy()
+    max_rem = (q.lo[:n] + k * q.width[:n]).cpu().numpy()
+    est, age = ages_for(np.random.default_rng(1002 + rank), n, mean_rem, max_rem)
+    q.est_age[:n] = torch.from_numpy(est).to(dev)
+    q.age[:n] = torch.from_numpy(age).to(dev)
+    q.tiebreak[:n] = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int32, device=dev)
+    q.n = n
+
     stream = torch.cuda.current_stream()
     gathered = torch.empty(world * n, dtype=torch.int64, device=dev)
     gslots = torch.arange(world * n, dtype=torch.int32, device=dev)
@@ -273,48 +303,55 @@ def run_ours(args):
     tb = int(L.pdg_order_temp_bytes(world * n))
     temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    k1_ev = []
+    k_ev = {"engine": [], "k1": []}
 
-    def step(record_k1=False):
-        if record_k1:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def step(salt, record=False):
+        torch.add(seeds0, salt, out=seeds)                  # fresh estimate seeds
+        if record:
+            e0, e1, e2 = ev(), ev(), ev()
             e0.record(stream)
-        q.score(PENALTY)
-        if record_k1:
+        eng.run(g_idx, u_idx, seeds, n=N_SAMP, bucket_count=b, visit_cap=VISIT_CAP, queue=q)
+        if record:
             e1.record(stream)
-            k1_ev.append((e0, e1))
+        q.score(PENALTY)
+        if record:
+            e2.record(stream)
+            k_ev["engine"].append((e0, e1))
+            k_ev["k1"].append((e1, e2))
         if world > 1:
             dist.all_gather_into_tensor(gathered, q.keys[:n])
             src = gathered
         else:
             src = q.keys[:n]
+        # shards are in global arrival order (rank-major), so a stable sort on
+        # the 32-bit key alone yields the (key, arrival) order
         _lib.check(L.pdg_order(_lib.ptr(src), _lib.ptr(out_keys), _lib.ptr(gslots),
                                _lib.ptr(out_slots), world * n, 32, _lib.ptr(temp),
                                temp.numel(), _lib.stream_ptr(stream)), "pdg_order")
 
-    # kernels per step (CUPTI count of one step, outside the timed region)
-    launches = None if args.ncu else count_launches(step)
+    launches, kernel_names = (None, None) if args.ncu else count_launches(step)
 
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
         flush.zero_()
-        step()
+        step(1 + i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = Clocks(local)
     clocks.start()
-    # keep the GPU busy ~0.4 s before the timed steps so nvidia-smi samples
-    # the clocks under load; the timed steps run inside that sampled window
-    t_end = time.perf_counter() + 0.4
+    t_end = time.perf_counter() + 0.4        # clocks sampled under load
     while time.perf_counter() < t_end:
-        step()
+        step(7)
         torch.cuda.synchronize()
     step_ev = []
-    for _ in range(args.steps):
+    for i in range(args.steps):
         flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = ev(), ev()
         e0.record(stream)
-        step(record_k1=True)
+        step(100 + i, record=True)
         e1.record(stream)
         step_ev.append((e0, e1))
     torch.cuda.synchronize()
@@ -322,11 +359,12 @@ def run_ours(args):
         dist.barrier()
     t_end = time.perf_counter() + 0.3
     while time.perf_counter() < t_end:
-        step()
+        step(9)
         torch.cuda.synchronize()
     clk = clocks.stop()
     step_ms = np.array([a.elapsed_time(b_) for a, b_ in step_ev])
-    k1_ms = np.array([a.elapsed_time(b_) for a, b_ in k1_ev])
+    eng_ms = np.array([a.elapsed_time(b_) for a, b_ in k_ev["engine"]])
+    k1_ms = np.array([a.elapsed_time(b_) for a, b_ in k_ev["k1"]])
     tot = torch.tensor([step_ms.sum(), np.median(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -334,33 +372,42 @@ def run_ours(args):
     p50 = float(tot[1].item())
     value = world * n / (ms_per_step / 1e3)
 
-    # e2e: through the public queue API with pinned HOST buffers -- each step
-    # uploads that refresh's attained-service vector (the per-refresh input)
-    # and reads back the global order and keys.
     if args.ncu:
         if rank == 0:
             print(json.dumps({"ncu_run": True, "ms_per_step": ms_per_step}), flush=True)
         return
-    h_age = torch.from_numpy(rows["age"]).pin_memory()
+
+    # ---- e2e through the public API with pinned HOST buffers --------------
+    # every step uploads the per-app queue state the scheduler owns (current
+    # unit, estimate seed, attained service now and at the estimate) and reads
+    # back the global order and the keys
+    h_unit = torch.from_numpy(jb["unit"]).pin_memory()
+    h_seed = torch.from_numpy(jb["seed"]).pin_memory()
+    h_age = torch.from_numpy(age).pin_memory()
+    h_est = torch.from_numpy(est).pin_memory()
     h_order = torch.empty(world * n, dtype=torch.int32).pin_memory()
     h_keys = torch.empty(n, dtype=torch.float32).pin_memory()
-    for _ in range(2):
+
+    def e2e_step(salt):
+        u_idx.copy_(h_unit, non_blocking=True)
+        seeds0.copy_(h_seed, non_blocking=True)
         q.age[:n].copy_(h_age, non_blocking=True)
-        step()
+        q.est_age[:n].copy_(h_est, non_blocking=True)
+        step(salt)
         h_order.copy_(out_slots, non_blocking=True)
         h_keys.copy_(q.key_f32[:n], non_blocking=True)
+
+    for i in range(2):
+        e2e_step(200 + i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e2e_ms = []
-    for _ in range(args.steps):
+    for i in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        q.age[:n].copy_(h_age, non_blocking=True)
-        step()
-        h_order.copy_(out_slots, non_blocking=True)
-        h_keys.copy_(q.key_f32[:n], non_blocking=True)
+        e2e_step(300 + i)
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2t = torch.tensor([float(np.sum(e2e_ms)), float(np.median(e2e_ms))], dtype=torch.float64,
@@ -368,62 +415,67 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(e2t, op=dist.ReduceOp.MAX)
     e2e_ms_step = float(e2t[0].item()) / args.steps
+    h2d = h_unit.numel() * 4 + h_seed.numel() * 8 + h_age.numel() * 8 + h_est.numel() * 8
     e2e = {"value": world * n / (e2e_ms_step / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": int(h_age.numel() * 8),
+           "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(h_order.numel() * 4 + h_keys.numel() * 4),
            "ms_per_step": e2e_ms_step, "p50_latency_ms": float(e2t[1].item()),
-           "path": "HistQueue.age <- pinned host; score+order; order/keys -> pinned host"}
+           "path": "pinned host queue state -> DemandEngine.run + HistQueue.score + "
+                   "pdg_order -> pinned host order/keys (wall clock, synchronized)"}
 
-    # roofline of the dominant kernel (K1b), algorithmic bytes per app
-    bytes_per_app = 2 * b + 4 * 8 + 4 + 4 + 4 + 1 + 8
-    k1_avg = float(k1_ms.mean())
-    achieved = bytes_per_app * n / (k1_avg / 1e3) / 1e9
+    # ---- roofline of the dominant kernel (the engine) ----------------------
+    reach = np.array([reachable_units(u) for u in jb["unit"]])
+    # per app: pools of reachable units (256 f64) + their descriptors (64 B) and
+    # successor slots (4 x 12 B) + job (unit, graph, seed) + histogram row out
+    per_app = reach * (N_REC * 8 + 64 + 48) + (4 + 4 + 8) + (2 * q.stride + 8 + 8 + 4 + 4)
+    bytes_per_app = float(per_app.mean())
+    eng_avg = float(eng_ms.mean())
+    achieved = bytes_per_app * n / (eng_avg / 1e3) / 1e9
     peak, peak_src = measured_peaks()
-    traffic, _ = ncu_traffic("gittins_hist_kernel")
+    ns = ncu_summary("mc_engine_kernel")
+    traffic = ns.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": "gittins_hist_kernel<1>",
-                "bytes_per_app": bytes_per_app, "avg_launch_ms": k1_avg,
-                "share_of_step": k1_avg / float(np.mean(step_ms)), "peak_source": peak_src}
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "mc_engine_kernel", "bytes_per_app": bytes_per_app,
+                "avg_launch_ms": eng_avg, "share_of_step": eng_avg / float(np.mean(step_ms)),
+                "peak_source": peak_src,
+                "note": "integer-issue bound (PCG64 128-bit jump-ahead per draw); the "
+                        "issue-rate roofline from ncu is in profiles/ncu_summary.json",
+                "issue_frac": ns.get("issue_active_frac")}
+    k1_bytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
+    k1 = {"kernel": "gittins_hist_kernel<1>", "avg_launch_ms": float(k1_ms.mean()),
+          "bytes_per_app": k1_bytes,
+          "achieved_gbs": k1_bytes * n / (float(k1_ms.mean()) / 1e3) / 1e9,
+          "apps_per_s": n / (float(k1_ms.mean()) / 1e3)}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "p50_latency_ms": p50, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64/f32/u16 (f64 support, f32 scan, u16 counts)",
-        "data": "synthetic (seeded multinomial histograms, n=512 per app)",
-        "config": {"workload": "config2: full Gittins re-score of a 100k-app 256-bucket queue + global order",
-                   "apps_per_gpu": n, "bins": b, "samples_per_hist": N_SAMP,
+        "vs_baseline": None, "dtype": "f64 walks/f32 scan/u16 counts",
+        "data": "synthetic (seeded app-unique depth-8 PDGraphs, 256 records per unit)",
+        "config": {"workload": "config2: full re-score = MC demand engine (n=512, bit-exact "
+                               "vs reference) + 256-bucket Gittins + global order",
+                   "apps_per_gpu": n, "bins": b, "samples_per_app": N_SAMP,
+                   "records_per_unit": N_REC, "units_per_graph": 8, "visit_cap": VISIT_CAP,
                    "parallelism": f"shard-by-app x{world}, NCCL all_gather of 8 B keys",
-                   "l2": "flushed between steps (256 MiB write, outside the step events)"},
+                   "l2": "flushed between steps (256 MiB write, outside the step events); "
+                         "1.6 GB graph bank > L2"},
         "gpu_launches": None if launches is None else launches * args.steps,
-        "gpu_launches_per_step": launches,
-        "e2e": e2e, "roofline": roofline, "clocks": clk,
+        "gpu_launches_per_step": launches, "kernels": kernel_names,
+        "e2e": e2e, "roofline": roofline, "k1_refresh": k1, "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sample = min(n, 20_000)
-        sub = {k: v[:sample] for k, v in rows.items()}
-        rate = cpu_rate(sub, 1)
+        rate = cpu_rate(args.cpu_apps, 1, args.cpu_apps, 1000, b)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"{sample} of {n} apps, oracle numpy "
-                                          f"gittins_rank_batch + penalty + lexsort, 1 process"}
+                                "sample": f"{args.cpu_apps} of {n} apps (same synthetic generator),"
+                                          " oracle MC(n=512)+bucketize(256)+Gittins row, "
+                                          "1 process"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def count_launches(step):
-    import torch
-    from torch.profiler import ProfilerActivity, profile
-    torch.cuda.synchronize()
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        step()
-        torch.cuda.synchronize()
-    names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
-    ours = [nm for nm in names if ("pdg" in nm or "gittins" in nm or "cub" in nm.lower()
-                                   or "Radix" in nm)]
-    return len(ours)
 
 
 def main():

@@ -82,24 +82,23 @@ class RemainingDemand:
 class DemandEngine:
     """Resident graph bank + launch wrapper for K2/K3/a4."""
 
-    def __init__(self, graphs: dict, prefill_rate: float = 10000.0, decode_rate: float = 50.0,
+    def __init__(self, graphs, prefill_rate: float = 10000.0, decode_rate: float = 50.0,
                  device: str = "cuda"):
+        """graphs: dict name -> graph (reference PDGraph or KBGraph), or a
+        prebuilt GraphBank."""
         _lib.lib()
         self.device = torch.device(device)
-        self.bank = GraphBank(graphs, device=device)
+        self.bank = graphs if isinstance(graphs, GraphBank) else GraphBank(graphs, device=device)
         b = self.bank
-        caps = [b.capacity[nm][uid] for nm in b.names for uid in b.unit_order[nm]]
-        self.unit_capacity = torch.tensor(caps or [1000], dtype=torch.int32, device=self.device)
         self.jump = _jump_tensor(self.device)
         self.c_bank = GraphBankC(
             _lib.ptr(b.units), _lib.ptr(b.graph_base), _lib.ptr(b.graph_n),
-            _lib.ptr(self.unit_capacity), _lib.ptr(b.vals), _lib.ptr(b.pool_off),
+            _lib.ptr(b.unit_capacity), _lib.ptr(b.vals), _lib.ptr(b.pool_off),
             _lib.ptr(b.pool_len), _lib.ptr(b.succ_cum), _lib.ptr(b.succ_nxt),
             _lib.ptr(b.conds), _lib.ptr(b.pairs), _lib.ptr(self.jump),
             float(prefill_rate), float(decode_rate))
-        hu = b.host_units
-        self.max_unit_k = int(hu["ib_k"].max()) if len(hu) else 1
-        self.max_pairs = int(b.host_conds["pair_len"].max()) if len(b.host_conds) else 0
+        self.max_unit_k = b.max_unit_k
+        self.max_pairs = b.max_pairs
         self._scratch = None
 
     # -- job marshalling ------------------------------------------------------

@@ -298,15 +298,29 @@ class GraphBank:
                 units.append(d)
 
         self.graphs = graphs
-        self.n_units = len(units)
-        self.host_units = np.array(units, dtype=UNIT_DTYPE) if units else np.zeros(0, UNIT_DTYPE)
-        self.host_vals = np.asarray(vals, dtype=np.float64)
-        self.capacity = {nm: {uid: getattr(graphs[nm].units[uid], "capacity", 1000)
-                              for uid in self.unit_order[nm]} for nm in self.names}
-        self._upload(device, gbase, gn, pools_off, pools_len, succ_cum, succ_nxt, conds, pairs)
+        caps = [getattr(graphs[nm].units[uid], "capacity", 1000)
+                for nm in self.names for uid in self.unit_order[nm]]
+        self._finish(device, np.array(units, dtype=UNIT_DTYPE) if units else
+                     np.zeros(0, UNIT_DTYPE), vals, gbase, gn, caps, pools_off, pools_len,
+                     succ_cum, succ_nxt, conds, pairs)
 
-    def _upload(self, device, gbase, gn, pools_off, pools_len, succ_cum, succ_nxt, conds,
-                pairs):
+    @classmethod
+    def from_arrays(cls, *, units, vals, graph_base, graph_n, succ_cum, succ_nxt,
+                    unit_capacity, device: str = "cuda", names=None, unit_order=None):
+        """Bank from pre-built tables (vectorised synthetic workloads); same
+        layout the compiler produces.  No K3 records, no own-input pools."""
+        self = cls.__new__(cls)
+        g = len(graph_base)
+        self.names = list(names) if names is not None else [str(i) for i in range(g)]
+        self.index = {nm: i for i, nm in enumerate(self.names)}
+        self.unit_order = unit_order or {}
+        self.graphs = {}
+        self._finish(device, units, vals, graph_base, graph_n, unit_capacity, [], [],
+                     succ_cum, succ_nxt, [], [])
+        return self
+
+    def _finish(self, device, units, vals, gbase, gn, caps, pools_off, pools_len, succ_cum,
+                succ_nxt, conds, pairs):
         import torch
         dev = torch.device(device)
 
@@ -316,19 +330,24 @@ class GraphBank:
                 a = np.zeros(1, dtype=dt)
             return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 
-        self.units = t(self.host_units.view(np.uint8).reshape(-1), np.uint8)
-        self.vals = t(self.host_vals, np.float64)
+        self.host_units = units
+        self.n_units = len(units)
+        self.units = t(units.view(np.uint8).reshape(-1), np.uint8)
+        self.vals = t(vals, np.float64)
         self.graph_base = t(gbase, np.int32)
         self.graph_n = t(gn, np.int32)
+        self.unit_capacity = t(caps, np.int32)
         self.pool_off = t(pools_off, np.int32)
         self.pool_len = t(pools_len, np.int32)
         self.succ_cum = t(succ_cum, np.float64)
         self.succ_nxt = t(succ_nxt, np.int32)
-        ca = np.array(conds, dtype=COND_DTYPE) if conds else np.zeros(1, COND_DTYPE)
+        ca = np.array(conds, dtype=COND_DTYPE) if len(conds) else np.zeros(1, COND_DTYPE)
+        pa = np.array(pairs, dtype=PAIR_DTYPE) if len(pairs) else np.zeros(1, PAIR_DTYPE)
         self.host_conds = ca
-        pa = np.array(pairs, dtype=PAIR_DTYPE) if pairs else np.zeros(1, PAIR_DTYPE)
         self.conds = t(ca.view(np.uint8).reshape(-1), np.uint8)
         self.pairs = t(pa.view(np.uint8).reshape(-1), np.uint8)
+        self.max_unit_k = int(units["ib_k"].max()) if len(units) else 1
+        self.max_pairs = int(ca["pair_len"].max())
 
     def local_unit(self, name: str, uid: str) -> int:
         return self.unit_order[name].index(uid)

@@ -1,0 +1,88 @@
+"""Parity on the benchmark workload (config 2 shape): app-unique depth-8
+PDGraphs.  A random sample of apps is checked bit-exactly against the CPU
+oracle; the full 100k-app queue is checked through size-independent
+properties (every histogram holds n samples, keys finite and positive, the
+global order is a permutation sorted by key then arrival)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import pdg_oracle as O
+from tools import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def test_synth_sample_bit_exact():
+    import torch
+    from paper_2506_14851_b200.estimator import DemandEngine
+    n_apps = 3000
+    w = synth.make(n_apps, 256, seed=11)
+    jb = synth.jobs(n_apps, seed=12)
+    eng = DemandEngine(synth.bank(w))
+    dev = eng.device
+    res = eng.run(torch.arange(n_apps, dtype=torch.int32, device=dev),
+                  torch.from_numpy(jb["unit"]).to(dev), torch.from_numpy(jb["seed"]).to(dev),
+                  n=512, bucket_count=256, samples=True)
+    S = res["samples"].cpu().numpy()
+    cap = res["capped"].cpu().numpy()
+    q = res["queue"]
+    cnt = q.counts[:n_apps].cpu().numpy()
+    rng = np.random.default_rng(0)
+    for a in rng.choice(n_apps, 120, replace=False):
+        g = O.graph_from_kb(synth.kb_doc(w, a))
+        want = O.mc_remaining_demand(g, f"s{jb['unit'][a]}", [], 512, int(jb["seed"][a]))
+        np.testing.assert_array_equal(S[a], want.samples)
+        assert cap[a] == want.capped
+        b = O.bucketize(want.samples.tolist(), 256)
+        np.testing.assert_array_equal(cnt[a, :b.k], b.counts)
+
+
+def test_full_size_queue_properties():
+    import torch
+    from paper_2506_14851_b200 import _lib
+    from paper_2506_14851_b200.estimator import DemandEngine
+    from paper_2506_14851_b200.queue import HistQueue
+    n = 100_000
+    w = synth.make(n, 256, seed=21)
+    jb = synth.jobs(n, seed=22)
+    eng = DemandEngine(synth.bank(w))
+    dev = eng.device
+    q = HistQueue(n, 256)
+    eng.run(torch.arange(n, dtype=torch.int32, device=dev), torch.from_numpy(jb["unit"]).to(dev),
+            torch.from_numpy(jb["seed"]).to(dev), n=512, bucket_count=256, queue=q)
+    cnt = q.counts[:n].to(torch.int64)
+    assert bool((cnt.sum(1) == 512).all())
+    assert bool((q.nsamp[:n] == 512).all())
+    nb = q.nbins[:n]
+    assert bool(((nb == 256) | (nb == 1)).all())
+    # counts only inside the row's buckets
+    j = torch.arange(q.stride, device=dev)
+    assert int(cnt[j[None, :] >= nb[:, None]].sum()) == 0
+    q.est_age[:n] = 0.0
+    q.age[:n] = torch.rand(n, device=dev, dtype=torch.float64) * 5.0
+    q.score(2.0)
+    key = q.key_f32[:n]
+    assert bool(torch.isfinite(key).all()) and bool((key >= 0).all())
+    order = q.order(arrival_ordered=True)
+    assert torch.equal(torch.sort(order.long()).values, torch.arange(n, device=dev))
+    ko = key[order.long()]
+    assert bool((ko[1:] >= ko[:-1]).all())
+    ties = ko[1:] == ko[:-1]
+    assert bool((order[1:][ties] > order[:-1][ties]).all())   # arrival tie-break
+    # spot-check keys against the float64 oracle on the GPU histograms
+    sel = np.random.default_rng(1).choice(n, 2000, replace=False)
+    lo = q.lo[:n].cpu().numpy()[sel]
+    wd = q.width[:n].cpu().numpy()[sel]
+    nbn = nb.cpu().numpy()[sel]
+    c = cnt.cpu().numpy()[sel]
+    ag = q.age[:n].cpu().numpy()[sel]
+    jj = np.arange(256, dtype=np.float64)
+    v = ((lo[:, None] + jj * wd[:, None]) + (lo[:, None] + (jj + 1) * wd[:, None])) / 2.0
+    v = np.where(jj[None, :] >= nbn[:, None], v[np.arange(len(sel)), nbn - 1][:, None], v)
+    r = O.gittins_rank_batch(v, c / 512.0, ag)
+    r = np.where(np.isnan(r), ag * 2.0, r)
+    got = key.cpu().numpy()[sel].astype(np.float64)
+    assert np.max(np.abs(got - r) / np.maximum(r, 1e-30)) < 1e-5
