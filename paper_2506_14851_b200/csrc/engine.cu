@@ -7,18 +7,21 @@
 // reference for the same (graph, current unit, observations, n, seed): the
 // kernel evaluates the reference's numpy PCG64 stream *by position*.
 //
-// Mapping: one warp per application; walk w lives on lane w % 32 (round
-// w / 32).  The reference walk is vectorised per (step, unit): at each outer
-// step the occupied-unit set is frozen, units are visited in ascending index
-// order, and every walk sitting on the unit *at that moment* draws
+// Mapping: one warp per application.  The reference walk is vectorised per
+// (step, unit): at each outer step the occupied-unit set is frozen, units are
+// visited in ascending index order, and every walk sitting on the unit *at
+// that moment* draws
 //   choice(A, m) [, choice(B, m) | per-input-bucket choice(pool_b, m_b)],
 //   then random(m)                                 (estimator.py:343-353)
 // so each draw's position in the stream is (group base) + (rank of the walk
-// among the unit's members), computed with ballots; each lane jumps the
-// PCG64 state straight to its position (pcg64.cuh).  numpy's Lemire rejection
-// (probability < P/2^32 per draw) is detected by a warp vote and the affected
-// unit visit is then replayed sequentially by lane 0 with the exact
-// sequential generator.
+// among the unit's members).  Per step the warp compacts the still-active
+// walks (index order kept); per unit visit it compacts that unit's members
+// into a list whose position IS the rank, and lane l takes a contiguous block
+// of members, so its stream positions are consecutive: one PCG64 jump to the
+// block start (pcg64.cuh), then single LCG steps (a 64-bit word serves two
+// 32-bit bounded draws).  numpy's Lemire rejection (probability < P/2^32 per
+// draw) is detected by a warp vote and the visit is then replayed
+// sequentially by lane 0 with the exact sequential generator.
 #include "common.cuh"
 #include "pcg64.cuh"
 
@@ -59,6 +62,7 @@ struct EngineArgs {
   int cap;           // visit cap
   int k_out;         // bucket_count of the output histogram
   int counters;      // u32 counters per warp in smem
+  int max_unit_k;    // largest unit input-bucket count (own-input sampling)
   int max_pairs;     // K3 scratch per warp
   char* scratch;     // global scratch base
   size_t scratch_per_warp;
@@ -116,11 +120,49 @@ __device__ __forceinline__ void close_u32(const uint64_t* jt, Stream& g, uint32_
   g.s = pcg_jump(jt, g.s, g.inc, (F + 1) >> 1);
 }
 
+// Reads fresh words of the stream forward from a base state: word q is the
+// output after q+1 steps.  Short gaps step, long gaps jump.
+struct Cursor {
+  U128 st;
+  uint32_t q;      // index of the word held in w (0xffffffff: st is the base)
+  uint64_t w;
+};
+
+__device__ __forceinline__ uint64_t cursor_word(Cursor& c, const uint64_t* jt, const U128& inc,
+                                                uint32_t q) {
+  if (q != c.q) {
+    uint32_t d = q - c.q;
+    if (d <= 4) {
+      do { c.st = pcg_step(c.st, inc); } while (--d);
+    } else {
+      c.st = pcg_jump(jt, c.st, inc, d);
+    }
+    c.q = q;
+    c.w = pcg_out(c.st);
+  }
+  return c.w;
+}
+
+// R-th 32-bit half of the bounded-draw stream (R = 0 is the buffered half).
+__device__ __forceinline__ uint32_t cursor_half(Cursor& c, const uint64_t* jt, const Stream& g,
+                                                uint32_t R) {
+  if (g.pend) {
+    if (R == 0) return g.pv;
+    --R;
+  }
+  const uint64_t w = cursor_word(c, jt, g.inc, R >> 1);
+  return (R & 1) ? uint32_t(w >> 32) : uint32_t(w);
+}
+
+template <typename Idx>
 struct WarpState {
   double* tot;      // [n] accumulated remaining demand per walk
-  double* tmp;      // [n] this visit's stage time per walk
+  double* tmp;      // [n] stage time of this visit, per member rank
+  Idx* act;         // [n] active walks, ascending
+  Idx* mem;         // [n] members of the visited unit, ascending (= rank order)
+  Idx* osrt;        // [n] member ranks sorted by input bucket (own-input)
+  uint16_t* bkt;    // [n] input bucket per member rank (own-input)
   int8_t* cur;      // [n] current unit per walk (-1 = terminated)
-  uint16_t* bkt;    // [n] input bucket per walk (own-input sampling)
   uint32_t* cnt;    // [counters]
   double* kin;      // [max_pairs] K3 kept inputs
   double* kout;     // [max_pairs] K3 kept outputs
@@ -129,31 +171,28 @@ struct WarpState {
 // ---------------------------------------------------------------------------
 // Sequential replay of one unit visit (lane 0) -- exact on Lemire rejections.
 // ---------------------------------------------------------------------------
+template <typename Idx>
 __device__ void serial_visit(const EngineArgs& a, const UnitDesc& d, const Pools& pl,
-                             bool own, int u, const WarpState& ws, Stream& g) {
+                             bool own, uint32_t m, const WarpState<Idx>& ws, Stream& g) {
   SeqGen sg{g.s, g.inc, g.pend, g.pv};
-  const int n = a.n;
-  const double* V = a.b.vals;
   const bool llm = d.flags & F_LLM;
-  for (int w = 0; w < n; ++w)
-    if (ws.cur[w] == u) ws.tmp[w] = pl.A[sg.bounded(uint32_t(pl.pa))];
+  for (uint32_t k = 0; k < m; ++k) ws.tmp[k] = pl.A[sg.bounded(uint32_t(pl.pa))];
   if (llm) {
     if (!own) {
-      for (int w = 0; w < n; ++w)
-        if (ws.cur[w] == u)
-          ws.tmp[w] = dadd(__ddiv_rn(ws.tmp[w], a.b.prefill_rate),
-                           __ddiv_rn(pl.B[sg.bounded(uint32_t(pl.pb))], a.b.decode_rate));
+      for (uint32_t k = 0; k < m; ++k)
+        ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], a.b.prefill_rate),
+                         __ddiv_rn(pl.B[sg.bounded(uint32_t(pl.pb))], a.b.decode_rate));
     } else {
-      const int k = d.ib_k;
-      for (int w = 0; w < n; ++w)
-        if (ws.cur[w] == u) ws.bkt[w] = uint16_t(bucket_of(ws.tmp[w], d.ib_lo, d.ib_hi, k));
-      for (int bb = 0; bb < k; ++bb) {
+      const int K = d.ib_k;
+      for (uint32_t k = 0; k < m; ++k)
+        ws.bkt[k] = uint16_t(bucket_of(ws.tmp[k], d.ib_lo, d.ib_hi, K));
+      for (int bb = 0; bb < K; ++bb) {
         const int pln = a.b.pool_len[d.pool_off + bb];
-        const double* pool = pln > 0 ? V + a.b.pool_off[d.pool_off + bb] : pl.B;
+        const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
         const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
-        for (int w = 0; w < n; ++w)
-          if (ws.cur[w] == u && ws.bkt[w] == bb)
-            ws.tmp[w] = dadd(__ddiv_rn(ws.tmp[w], a.b.prefill_rate),
+        for (uint32_t k = 0; k < m; ++k)
+          if (ws.bkt[k] == bb)
+            ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], a.b.prefill_rate),
                              __ddiv_rn(pool[sg.bounded(P)], a.b.decode_rate));
       }
     }
@@ -164,14 +203,14 @@ __device__ void serial_visit(const EngineArgs& a, const UnitDesc& d, const Pools
 }
 
 // ---------------------------------------------------------------------------
-// one (step, unit) visit of the vectorised walk
+// one (step, unit) visit of the vectorised walk; returns true if the visit
+// was replayed serially (a Lemire rejection occurred)
 // ---------------------------------------------------------------------------
-__device__ void visit_unit(const EngineArgs& a, int gbase, int u, const Pools& ovp,
-                           bool has_ov, int cur_unit, const WarpState& ws, Stream& g,
-                           int lane) {
+template <typename Idx>
+__device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& ovp,
+                           bool has_ov, int cur_unit, const WarpState<Idx>& ws, uint32_t na,
+                           Stream& g, int lane) {
   const uint64_t* jt = a.b.jump;
-  const int n = a.n;
-  const int W = (n + 31) >> 5;
   const unsigned lt = lanemask_lt();
   const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u];
   const bool llm = d.flags & F_LLM;
@@ -186,108 +225,119 @@ __device__ void visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
     pl.pb = d.b_len;
   }
   const bool own = llm && (d.flags & F_OWN) && !ov;
-  // members
+  // members of this visit, in walk order: list position == rank
   uint32_t m = 0;
-  for (int i = 0; i < W; ++i) {
-    const int w = i * 32 + lane;
-    m += __popc(__ballot_sync(kFull, w < n && ws.cur[w] == u));
+  for (uint32_t base = 0; base < na; base += 32) {
+    const uint32_t idx = base + lane;
+    bool is = false;
+    Idx w = 0;
+    if (idx < na) {
+      w = ws.act[idx];
+      is = ws.cur[w] == u;
+    }
+    const unsigned bal = __ballot_sync(kFull, is);
+    if (is) ws.mem[m + __popc(bal & lt)] = w;
+    m += __popc(bal);
   }
+  __syncwarp();
+  const uint32_t per = (m + 31) >> 5;
+  const uint32_t k0 = min(lane * per, m), k1 = min(k0 + per, m);
   const uint32_t c1 = pl.pa > 1 ? m : 0u;
   bool rej = false;
   uint32_t C = 0;
+  Cursor cs{g.s, 0xffffffffu, 0};
   if (!own) {
-    uint32_t R = 0;
-    for (int i = 0; i < W; ++i) {
-      const int w = i * 32 + lane;
-      const bool mem = w < n && ws.cur[w] == u;
-      const unsigned bal = __ballot_sync(kFull, mem);
-      if (mem) {
-        const uint32_t r = R + __popc(bal & lt);
-        const uint32_t ia = pl.pa > 1 ? lemire(half_at(jt, g, r), uint32_t(pl.pa), rej) : 0u;
-        double t = pl.A[ia];
-        if (llm) {
-          const uint32_t ib = pl.pb > 1 ? lemire(half_at(jt, g, c1 + r), uint32_t(pl.pb), rej) : 0u;
-          t = dadd(__ddiv_rn(t, a.b.prefill_rate), __ddiv_rn(pl.B[ib], a.b.decode_rate));
-        }
-        ws.tmp[w] = t;
+    for (uint32_t k = k0; k < k1; ++k) {
+      const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(cs, jt, g, k), uint32_t(pl.pa), rej) : 0u;
+      ws.tmp[k] = pl.A[ia];
+    }
+    if (llm) {
+      for (uint32_t k = k0; k < k1; ++k) {
+        const uint32_t ib =
+            pl.pb > 1 ? lemire(cursor_half(cs, jt, g, c1 + k), uint32_t(pl.pb), rej) : 0u;
+        ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], a.b.prefill_rate),
+                         __ddiv_rn(pl.B[ib], a.b.decode_rate));
       }
-      R += __popc(bal);
     }
     C = c1 + ((llm && pl.pb > 1) ? m : 0u);
   } else {
     // own-input sampling: outputs drawn per input bucket, buckets ascending,
     // walks in order within a bucket (estimator.py:275-283)
-    const int k = d.ib_k;
-    for (int b = lane; b < k; b += 32) ws.cnt[b] = 0;
+    const int K = d.ib_k;
+    uint32_t* cnt = ws.cnt;
+    uint32_t* start = ws.cnt + a.max_unit_k;
+    uint32_t* effo = ws.cnt + 2 * a.max_unit_k;
+    for (int b = lane; b < K; b += 32) cnt[b] = 0;
     __syncwarp();
-    uint32_t R = 0;
-    for (int i = 0; i < W; ++i) {
-      const int w = i * 32 + lane;
-      const bool mem = w < n && ws.cur[w] == u;
-      const unsigned bal = __ballot_sync(kFull, mem);
-      if (mem) {
-        const uint32_t r = R + __popc(bal & lt);
-        const uint32_t ia = pl.pa > 1 ? lemire(half_at(jt, g, r), uint32_t(pl.pa), rej) : 0u;
-        const double iv = pl.A[ia];
-        ws.tmp[w] = iv;
-        const int bb = bucket_of(iv, d.ib_lo, d.ib_hi, k);
-        ws.bkt[w] = uint16_t(bb);
-        atomicAdd(&ws.cnt[bb], 1u);
-      }
-      R += __popc(bal);
+    for (uint32_t k = k0; k < k1; ++k) {
+      const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(cs, jt, g, k), uint32_t(pl.pa), rej) : 0u;
+      const double iv = pl.A[ia];
+      ws.tmp[k] = iv;
+      const int bb = bucket_of(iv, d.ib_lo, d.ib_hi, K);
+      ws.bkt[k] = uint16_t(bb);
+      atomicAdd(&cnt[bb], 1u);
     }
     __syncwarp();
-    // exclusive offsets over buckets that consume stream halves (pool > 1)
-    const int per = (k + 31) >> 5;
-    uint32_t loc = 0;
-    for (int q = 0; q < per; ++q) {
-      const int bb = lane * per + q;
-      if (bb < k) {
+    const int perb = (K + 31) >> 5;
+    uint32_t la = 0, le = 0;
+    for (int q = 0; q < perb; ++q) {
+      const int bb = lane * perb + q;
+      if (bb < K) {
         const int pln = a.b.pool_len[d.pool_off + bb];
         const int P = pln > 0 ? pln : pl.pb;
-        loc += P > 1 ? ws.cnt[bb] : 0u;
+        la += cnt[bb];
+        le += P > 1 ? cnt[bb] : 0u;
       }
     }
-    const uint32_t incl = warp_incl_scan(loc, lane);
-    const uint32_t eff_total = __shfl_sync(kFull, incl, 31);
-    uint32_t run = incl - loc;
+    const uint32_t ia_incl = warp_incl_scan(la, lane), ie_incl = warp_incl_scan(le, lane);
+    const uint32_t eff_total = __shfl_sync(kFull, ie_incl, 31);
+    uint32_t ra = ia_incl - la, re = ie_incl - le;
     __syncwarp();
-    for (int q = 0; q < per; ++q) {
-      const int bb = lane * per + q;
-      if (bb < k) {
+    for (int q = 0; q < perb; ++q) {
+      const int bb = lane * perb + q;
+      if (bb < K) {
         const int pln = a.b.pool_len[d.pool_off + bb];
         const int P = pln > 0 ? pln : pl.pb;
-        const uint32_t c = ws.cnt[bb];
-        ws.cnt[bb] = run;                 // becomes the running position cursor
-        run += P > 1 ? c : 0u;
+        const uint32_t c = cnt[bb];
+        start[bb] = ra;
+        effo[bb] = re;
+        cnt[bb] = ra;                        // cursor of the counting sort
+        ra += c;
+        re += P > 1 ? c : 0u;
       }
     }
     __syncwarp();
-    for (int i = 0; i < W; ++i) {
-      const int w = i * 32 + lane;
-      const bool mem = w < n && ws.cur[w] == u;
-      const int bb = mem ? int(ws.bkt[w]) : (0x10000 + lane);
+    // stable counting sort of member ranks by bucket (rank order = round order)
+    for (uint32_t base = 0; base < m; base += 32) {
+      const uint32_t k = base + lane;
+      const bool valid = k < m;
+      const int bb = valid ? int(ws.bkt[k]) : (0x10000 + lane);
       const unsigned peers = __match_any_sync(kFull, bb);
-      uint32_t base = 0;
-      if (mem) base = ws.cnt[bb];
+      uint32_t dest = 0;
+      if (valid) dest = cnt[bb];
       __syncwarp();
-      if (mem && (__ffs(peers) - 1) == lane) ws.cnt[bb] = base + __popc(peers);
+      if (valid && (__ffs(peers) - 1) == lane) cnt[bb] = dest + __popc(peers);
       __syncwarp();
-      if (mem) {
-        const int pln = a.b.pool_len[d.pool_off + bb];
-        const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
-        const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
-        const uint32_t pos = c1 + base + __popc(peers & lt);
-        const uint32_t ob = P > 1 ? lemire(half_at(jt, g, pos), P, rej) : 0u;
-        ws.tmp[w] = dadd(__ddiv_rn(ws.tmp[w], a.b.prefill_rate),
-                         __ddiv_rn(pool[ob], a.b.decode_rate));
-      }
+      if (valid) ws.osrt[dest + __popc(peers & lt)] = Idx(k);
+    }
+    __syncwarp();
+    for (uint32_t j = k0; j < k1; ++j) {
+      const uint32_t k = ws.osrt[j];
+      const int bb = ws.bkt[k];
+      const int pln = a.b.pool_len[d.pool_off + bb];
+      const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
+      const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
+      const uint32_t pos = c1 + effo[bb] + (j - start[bb]);
+      const uint32_t ob = P > 1 ? lemire(cursor_half(cs, jt, g, pos), P, rej) : 0u;
+      ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], a.b.prefill_rate),
+                       __ddiv_rn(pool[ob], a.b.decode_rate));
     }
     C = c1 + eff_total;
   }
-  if (__any_sync(kFull, rej)) {
-    __syncwarp();
-    if (lane == 0) serial_visit(a, d, pl, own, u, ws, g);
+  const bool replay = __any_sync(kFull, rej);
+  __syncwarp();
+  if (replay) {
+    if (lane == 0) serial_visit(a, d, pl, own, m, ws, g);
     __syncwarp();
     g.s.lo = __shfl_sync(kFull, g.s.lo, 0);
     g.s.hi = __shfl_sync(kFull, g.s.hi, 0);
@@ -300,30 +350,26 @@ __device__ void visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
   const double* cum = a.b.succ_cum + d.succ_off;
   const int32_t* nxt = a.b.succ_nxt + d.succ_off;
   const int ns = d.succ_len;
-  uint32_t R = 0;
-  for (int i = 0; i < W; ++i) {
-    const int w = i * 32 + lane;
-    const bool mem = w < n && ws.cur[w] == u;
-    const unsigned bal = __ballot_sync(kFull, mem);
-    if (mem) {
-      const uint32_t r = R + __popc(bal & lt);
-      const double uu = u53_double(pcg_out(pcg_jump(jt, g.s, g.inc, r + 1)));
-      int idx = 0;
-      while (idx < ns && __ldg(cum + idx) <= uu) ++idx;   // searchsorted(side="right")
-      ws.cur[w] = int8_t(__ldg(nxt + idx));
-      ws.tot[w] = dadd(ws.tot[w], ws.tmp[w]);
-    }
-    R += __popc(bal);
+  Cursor cdb{g.s, 0xffffffffu, 0};
+  for (uint32_t k = k0; k < k1; ++k) {
+    const double uu = u53_double(cursor_word(cdb, jt, g.inc, k));
+    int idx = 0;
+    while (idx < ns && __ldg(cum + idx) <= uu) ++idx;    // searchsorted(side="right")
+    const Idx w = ws.mem[k];
+    ws.cur[w] = int8_t(__ldg(nxt + idx));
+    ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
   }
   g.s = pcg_jump(jt, g.s, g.inc, m);
   __syncwarp();
+  return replay;
 }
 
 // ---------------------------------------------------------------------------
 // K3: conditioned draw pools for the current unit (estimator.py:155-233)
 // ---------------------------------------------------------------------------
+template <typename Idx>
 __device__ bool condition(const EngineArgs& a, int gbase, int cur_unit, int obs_up,
-                          const double* obs, const WarpState& ws, Pools& ovp,
+                          const double* obs, const WarpState<Idx>& ws, Pools& ovp,
                           bool& conditioned, int lane) {
   const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + cur_unit];
   if (obs_up < 0 || !(d.flags & F_ANYMASK)) return false;   // no override
@@ -386,32 +432,45 @@ __device__ bool condition(const EngineArgs& a, int gbase, int cur_unit, int obs_
 }
 
 // ---------------------------------------------------------------------------
+// per-warp walk-state footprint (bytes per walk slot) for index type Idx
+template <typename Idx>
+__host__ __device__ constexpr size_t walk_bytes() { return 16 + 3 * sizeof(Idx) + 2 + 1; }
+
+template <typename Idx>
+__device__ WarpState<Idx> carve(unsigned char* base, int nw, uint32_t* cnt, double* k3,
+                                int max_pairs) {
+  WarpState<Idx> ws;
+  ws.tot = reinterpret_cast<double*>(base);
+  ws.tmp = ws.tot + nw;
+  ws.act = reinterpret_cast<Idx*>(ws.tmp + nw);
+  ws.mem = ws.act + nw;
+  ws.osrt = ws.mem + nw;
+  ws.bkt = reinterpret_cast<uint16_t*>(ws.osrt + nw);
+  ws.cur = reinterpret_cast<int8_t*>(ws.bkt + nw);
+  ws.cnt = cnt;
+  ws.kin = k3;
+  ws.kout = k3 + max_pairs;
+  return ws;
+}
+
+template <typename Idx>
 __global__ void __launch_bounds__(kWarps * 32) mc_engine_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;
   const bool in_smem = n <= kSmemWalks;
-  // per-warp shared block: counters, then (if small n) walk state
-  const size_t per_warp_smem = size_t(a.counters) * 4 +
-                               (in_smem ? size_t(kSmemWalks) * 19 : 0);
+  const int nw = in_smem ? kSmemWalks : ((n + 15) & ~15);
+  const size_t cnt_bytes = (size_t(a.counters) * 4 + 15) & ~size_t(15);
+  const size_t per_warp_smem = cnt_bytes + (in_smem ? size_t(kSmemWalks) * walk_bytes<Idx>() : 0);
   unsigned char* sb = smem + per_warp_smem * wib;
   const int64_t gwarp = int64_t(blockIdx.x) * kWarps + wib;
-  char* gs = a.scratch + size_t(gwarp) * a.scratch_per_warp;
-  WarpState ws;
-  ws.cnt = reinterpret_cast<uint32_t*>(sb);
-  unsigned char* walk_base = in_smem ? sb + size_t(a.counters) * 4 : reinterpret_cast<unsigned char*>(gs);
-  const int nw = in_smem ? kSmemWalks : n;
-  ws.tot = reinterpret_cast<double*>(walk_base);
-  ws.tmp = ws.tot + nw;
-  ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + nw);
-  ws.cur = reinterpret_cast<int8_t*>(ws.bkt + nw);
-  char* k3 = gs + (in_smem ? 0 : size_t(n) * 19 + 16);
-  k3 = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(k3) + 15) & ~uintptr_t(15));
-  ws.kin = reinterpret_cast<double*>(k3);
-  ws.kout = ws.kin + a.max_pairs;
+  unsigned char* gs = reinterpret_cast<unsigned char*>(a.scratch) + size_t(gwarp) * a.scratch_per_warp;
+  unsigned char* walk_base = in_smem ? sb + cnt_bytes : gs;
+  double* k3 = reinterpret_cast<double*>(gs + (in_smem ? 0 : size_t(nw) * walk_bytes<Idx>()));
+  const WarpState<Idx> ws =
+      carve<Idx>(walk_base, nw, reinterpret_cast<uint32_t*>(sb), k3, a.max_pairs);
 
   const int64_t stride = int64_t(gridDim.x) * kWarps;
-  const int W = (n + 31) >> 5;
   for (int64_t job = gwarp; job < a.n_jobs; job += stride) {
     const int gi = a.j.graph[job];
     const int gbase = a.b.graph_base[gi];
@@ -430,42 +489,55 @@ __global__ void __launch_bounds__(kWarps * 32) mc_engine_kernel(EngineArgs a) {
       obs[1] = a.j.obs_val[3 * job + 1];
       obs[2] = a.j.obs_val[3 * job + 2];
     }
-    const bool has_ov = condition(a, gbase, u0, obs_up, obs, ws, ovp, conditioned, lane);
+    const bool has_ov = condition<Idx>(a, gbase, u0, obs_up, obs, ws, ovp, conditioned, lane);
 
-    for (int i = 0; i < W; ++i) {
-      const int w = i * 32 + lane;
-      if (w < n) {
-        ws.cur[w] = int8_t(u0);
-        ws.tot[w] = 0.0;
-      }
+    for (int w = lane; w < n; w += 32) {
+      ws.cur[w] = int8_t(u0);
+      ws.tot[w] = 0.0;
+      ws.act[w] = Idx(w);
     }
     __syncwarp();
+    uint32_t na = uint32_t(n);
+    bool replayed = false;
+    const unsigned lt = lanemask_lt();
     for (int step = 0; step < a.cap; ++step) {
+      // compact the still-active walks (order kept) and collect occupied units
       unsigned occ = 0;
-      for (int i = 0; i < W; ++i) {
-        const int w = i * 32 + lane;
-        if (w < n && ws.cur[w] >= 0) occ |= 1u << ws.cur[w];
+      uint32_t nn = 0;
+      for (uint32_t base = 0; base < na; base += 32) {
+        const uint32_t idx = base + lane;
+        Idx w = 0;
+        int c = -1;
+        if (idx < na) {
+          w = ws.act[idx];
+          c = ws.cur[w];
+        }
+        const unsigned bal = __ballot_sync(kFull, c >= 0);
+        if (c >= 0) {
+          ws.act[nn + __popc(bal & lt)] = w;
+          occ |= 1u << c;
+        }
+        nn += __popc(bal);
       }
+      na = nn;
       occ = __reduce_or_sync(kFull, occ);
+      __syncwarp();
       if (!occ) break;
       while (occ) {
         const int u = __ffs(occ) - 1;
         occ &= occ - 1;
-        visit_unit(a, gbase, u, ovp, has_ov, u0, ws, g, lane);
+        replayed |= visit_unit<Idx>(a, gbase, u, ovp, has_ov, u0, ws, na, g, lane);
       }
     }
     // capped walks, samples, bucketing (distributions.py:79-105)
     int capped = 0;
     double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
-    for (int i = 0; i < W; ++i) {
-      const int w = i * 32 + lane;
-      if (w < n) {
-        capped += ws.cur[w] >= 0;
-        const double s = ws.tot[w];
-        lo = fmin(lo, s);
-        hi = fmax(hi, s);
-        if (a.o.samples) a.o.samples[job * int64_t(a.o.samples_stride) + w] = s;
-      }
+    for (int w = lane; w < n; w += 32) {
+      capped += ws.cur[w] >= 0;
+      const double sv = ws.tot[w];
+      lo = fmin(lo, sv);
+      hi = fmax(hi, sv);
+      if (a.o.samples) a.o.samples[job * a.o.samples_stride + w] = sv;
     }
     capped = warp_sum(capped);
     for (int o = 16; o > 0; o >>= 1) {
@@ -482,16 +554,13 @@ __global__ void __launch_bounds__(kWarps * 32) mc_engine_kernel(EngineArgs a) {
     }
     for (int b = lane; b < k; b += 32) ws.cnt[b] = 0;
     __syncwarp();
-    for (int i = 0; i < W; ++i) {
-      const int w = i * 32 + lane;
-      if (w < n) {
-        int idx = 0;
-        if (k > 1) {
-          idx = __double2int_rz(__ddiv_rn(dsub(ws.tot[w], lo), width));
-          idx = idx < k - 1 ? idx : k - 1;
-        }
-        atomicAdd(&ws.cnt[idx], 1u);
+    for (int w = lane; w < n; w += 32) {
+      int idx = 0;
+      if (k > 1) {
+        idx = __double2int_rz(__ddiv_rn(dsub(ws.tot[w], lo), width));
+        idx = idx < k - 1 ? idx : k - 1;
       }
+      atomicAdd(&ws.cnt[idx], 1u);
     }
     __syncwarp();
     if (a.o.counts) {
@@ -504,7 +573,8 @@ __global__ void __launch_bounds__(kWarps * 32) mc_engine_kernel(EngineArgs a) {
       if (a.o.nbins) a.o.nbins[row] = k;
       if (a.o.nsamp) a.o.nsamp[row] = n;
       if (a.o.capped) a.o.capped[job] = capped;
-      if (a.o.flags) a.o.flags[job] = (conditioned ? 1 : 0) | (has_ov ? 2 : 0);
+      if (a.o.flags)
+        a.o.flags[job] = (conditioned ? 1 : 0) | (has_ov ? 2 : 0) | (replayed ? 4 : 0);
     }
     __syncwarp();
   }
@@ -514,11 +584,20 @@ __global__ void __launch_bounds__(kWarps * 32) mc_engine_kernel(EngineArgs a) {
 
 using namespace pdg;
 
-static size_t walk_scratch(int n) { return n <= kSmemWalks ? 0 : size_t(n) * 19 + 32; }
+static bool small_idx(int n) { return n <= 65535; }
+
+static size_t walk_scratch(int n) {
+  if (n <= kSmemWalks) return 0;
+  const size_t nw = size_t((n + 15) & ~15);
+  return nw * (small_idx(n) ? walk_bytes<uint16_t>() : walk_bytes<uint32_t>());
+}
+
+static size_t scratch_per_warp(int n, int max_pairs) {
+  return (walk_scratch(n) + size_t(max_pairs) * 16 + 64 + 255) & ~size_t(255);
+}
 
 extern "C" size_t pdg_mc_scratch_bytes(int32_t n_samples, int32_t max_pairs, int32_t grid_warps) {
-  const size_t per = (walk_scratch(n_samples) + size_t(max_pairs) * 16 + 64 + 255) & ~size_t(255);
-  return per * size_t(grid_warps);
+  return scratch_per_warp(n_samples, max_pairs) * size_t(grid_warps);
 }
 
 extern "C" int pdg_mc_grid_warps(void) { return sm_count() * 8 * kWarps; }
@@ -529,8 +608,8 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
                                        int32_t max_pairs, const pdg_mc_out* out,
                                        void* scratch, size_t scratch_bytes, void* stream) {
   if (!bank || !jobs || !out || n_jobs < 0 || n_samples < 1 || n_samples > (1 << 19) ||
-      visit_cap < 0 || bucket_count < 1 || bucket_count > 1024 || max_unit_k > 1024 ||
-      max_pairs < 0) {
+      visit_cap < 0 || bucket_count < 1 || bucket_count > 1024 || max_unit_k < 0 ||
+      max_unit_k > 1024 || max_pairs < 0) {
     set_error("pdg_mc_remaining_demand: invalid arguments");
     return PDG_EINVAL;
   }
@@ -553,19 +632,30 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   a.n = n_samples;
   a.cap = visit_cap;
   a.k_out = bucket_count;
-  int c = bucket_count > max_unit_k ? bucket_count : max_unit_k;
+  a.max_unit_k = max_unit_k;
+  const int c = bucket_count > 3 * max_unit_k ? bucket_count : 3 * max_unit_k;
   a.counters = (c + 3) & ~3;
   a.max_pairs = max_pairs;
   a.scratch = static_cast<char*>(scratch);
-  a.scratch_per_warp = (walk_scratch(n_samples) + size_t(max_pairs) * 16 + 64 + 255) & ~size_t(255);
-  const size_t smem = size_t(kWarps) * (size_t(a.counters) * 4 +
-                                        (n_samples <= kSmemWalks ? size_t(kSmemWalks) * 19 : 0));
-  cudaError_t e = cudaFuncSetAttribute(mc_engine_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(mc_engine_kernel)");
+  a.scratch_per_warp = scratch_per_warp(n_samples, max_pairs);
+  const bool sm = n_samples <= kSmemWalks;
+  const size_t cnt_bytes = (size_t(a.counters) * 4 + 15) & ~size_t(15);
   int64_t blocks = (n_jobs + kWarps - 1) / kWarps;
   const int64_t capb = grid_warps / kWarps;
   if (blocks > capb) blocks = capb;
-  mc_engine_kernel<<<unsigned(blocks), kWarps * 32, smem, (cudaStream_t)stream>>>(a);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (small_idx(n_samples)) {
+    const size_t smem = size_t(kWarps) * (cnt_bytes + (sm ? size_t(kSmemWalks) * walk_bytes<uint16_t>() : 0));
+    cudaError_t e = cudaFuncSetAttribute(mc_engine_kernel<uint16_t>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(mc_engine_kernel)");
+    mc_engine_kernel<uint16_t><<<unsigned(blocks), kWarps * 32, smem, st>>>(a);
+  } else {
+    const size_t smem = size_t(kWarps) * cnt_bytes;
+    cudaError_t e = cudaFuncSetAttribute(mc_engine_kernel<uint32_t>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(mc_engine_kernel)");
+    mc_engine_kernel<uint32_t><<<unsigned(blocks), kWarps * 32, smem, st>>>(a);
+  }
   return launch_status("mc_engine_kernel");
 }

@@ -186,3 +186,4 @@ def test_lemire_rejection_replayed_exactly():
     got = run_cases(eng, case)
     want = O.mc_remaining_demand(og, "a", [], n, seed, steps)
     np.testing.assert_array_equal(got[0][0], want.samples)
+    assert got[0][2] & 4, "the sequential replay path was not exercised"
