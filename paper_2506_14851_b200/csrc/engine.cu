@@ -336,6 +336,7 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
   }
   const bool replay = __any_sync(kFull, rej);
   __syncwarp();
+  uint32_t words;        // fresh words consumed by the bounded draws
   if (replay) {
     if (lane == 0) serial_visit(a, d, pl, own, m, ws, g);
     __syncwarp();
@@ -343,23 +344,59 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
     g.s.hi = __shfl_sync(kFull, g.s.hi, 0);
     g.pend = __shfl_sync(kFull, int(g.pend), 0);
     g.pv = __shfl_sync(kFull, g.pv, 0);
+    words = 0;
+    cs = Cursor{g.s, 0xffffffffu, 0};
   } else {
-    close_u32(jt, g, C);
+    // close the bounded-draw group without re-deriving anything: the word
+    // holding the last fresh half was read by some lane (largest word index)
+    const uint32_t F = C == 0 ? 0u : C - (g.pend ? 1u : 0u);
+    words = (F + 1) >> 1;
+    if (C != 0) {
+      if (F & 1u) {
+        const uint32_t qlast = (F - 1) >> 1;
+        const unsigned owner = __ballot_sync(kFull, cs.q == qlast);
+        g.pv = uint32_t(__shfl_sync(kFull, cs.w, __ffs(owner) - 1) >> 32);
+        g.pend = true;
+      } else {
+        g.pend = false;
+      }
+    }
   }
-  // random(m) + successor jump (estimator.py:350-353)
-  const double* cum = a.b.succ_cum + d.succ_off;
-  const int32_t* nxt = a.b.succ_nxt + d.succ_off;
+  // random(m) + successor jump (estimator.py:350-353); word (words + k) of the
+  // same base serves member k
   const int ns = d.succ_len;
-  Cursor cdb{g.s, 0xffffffffu, 0};
+  double c0 = 2.0, c1s = 2.0, c2 = 2.0;     // first successors cached (cum <= 1)
+  int n0 = -1, n1 = -1, n2 = -1, n3 = -1;
+  {
+    const double* cum = a.b.succ_cum + d.succ_off;
+    const int32_t* nxt = a.b.succ_nxt + d.succ_off;
+    if (ns > 0) c0 = __ldg(cum);
+    if (ns > 1) c1s = __ldg(cum + 1);
+    if (ns > 2) c2 = __ldg(cum + 2);
+    n0 = __ldg(nxt);
+    if (ns > 0) n1 = __ldg(nxt + 1);
+    if (ns > 1) n2 = __ldg(nxt + 2);
+    if (ns > 2) n3 = __ldg(nxt + 3);
+  }
   for (uint32_t k = k0; k < k1; ++k) {
-    const double uu = u53_double(cursor_word(cdb, jt, g.inc, k));
-    int idx = 0;
-    while (idx < ns && __ldg(cum + idx) <= uu) ++idx;    // searchsorted(side="right")
+    const double uu = u53_double(cursor_word(cs, jt, g.inc, words + k));
+    int nx;
+    if (ns <= 3) {                                     // searchsorted(side="right")
+      nx = !(c0 <= uu) ? n0 : !(c1s <= uu) ? n1 : !(c2 <= uu) ? n2 : n3;
+    } else {
+      const double* cum = a.b.succ_cum + d.succ_off;
+      int idx = 0;
+      while (idx < ns && __ldg(cum + idx) <= uu) ++idx;
+      nx = __ldg(a.b.succ_nxt + d.succ_off + idx);
+    }
     const Idx w = ws.mem[k];
-    ws.cur[w] = int8_t(__ldg(nxt + idx));
+    ws.cur[w] = int8_t(nx);
     ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
   }
-  g.s = pcg_jump(jt, g.s, g.inc, m);
+  // the lane that drew the last double holds the advanced base state
+  const unsigned last_lane = (m - 1) / per;
+  g.s.lo = __shfl_sync(kFull, cs.st.lo, last_lane);
+  g.s.hi = __shfl_sync(kFull, cs.st.hi, last_lane);
   __syncwarp();
   return replay;
 }
@@ -454,7 +491,7 @@ __device__ WarpState<Idx> carve(unsigned char* base, int nw, uint32_t* cnt, doub
 }
 
 template <typename Idx>
-__global__ void __launch_bounds__(kWarps * 32) mc_engine_kernel(EngineArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 4) mc_engine_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;
