@@ -154,6 +154,44 @@ int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_jobs* jobs,
                             const pdg_mc_out* out, void* scratch, size_t scratch_bytes,
                             void* stream);
 
+/* ---------------------------------------------------------------------------
+ * K4a  batched plan_prewarm (prewarm.py:42-96), bit-exact: one job per
+ * (application, successor).  Job j's completion samples (absolute times, the
+ * caller's completion_dist.samples) are pool[off[j] .. off[j]+len[j]).
+ * has_plan[j] = 0 when p_s < knob (the reference returns None); otherwise the
+ * PrewarmPlan's (trigger_time, p_e).  Callers validate knob in [0,1], t_p >= 0.
+ * ------------------------------------------------------------------------- */
+int pdg_plan_prewarm(const double* pool, const int32_t* off, const int32_t* len,
+                     const int32_t* bucket_count, const double* p_s, const double* t_p,
+                     const double* knob, const double* now, int64_t n_jobs,
+                     uint8_t* has_plan, double* trigger, double* p_e, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K4b  need probability per backend type and time window (BASELINE config 5).
+ * need[a, t, k] = sum over successors v of a's current unit with type(v) = t
+ * of p_s(v) * P(completion < now + W_k), completion = now + the current
+ * unit's unconditioned service samples (simcore.py:480-487) conditioned on
+ * "> now" as plan_prewarm does (prewarm.py:65-67).  agg[t, k] (optional) is
+ * the sum over applications (expected number of applications needing a warm
+ * type-t backend within W_k).  <= 32 windows, <= 64 types, <= 8 successors.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const double* svc_sorted;   /* service samples per unit, ascending          */
+  const int32_t* svc_off;     /* [U]                                           */
+  const int32_t* svc_len;     /* [U]                                           */
+  const int32_t* graph_base;  /* [G]                                           */
+  const int32_t* succ_off;    /* [U] into succ_nxt / succ_p                    */
+  const int32_t* succ_len;    /* [U]                                           */
+  const int32_t* succ_nxt;    /* local unit index of each successor            */
+  const double* succ_p;       /* branch probability (pdgraph.py:182-194)       */
+  const int32_t* unit_type;   /* [U] warm-content backend type, -1 = none      */
+} pdg_prewarm_tables;
+
+int pdg_prewarm_need(const pdg_prewarm_tables* tables, const int32_t* graph,
+                     const int32_t* unit, const double* now, int64_t n,
+                     const double* windows, int32_t n_windows, int32_t n_types,
+                     float* need, double* agg, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -506,3 +506,24 @@ def exact_mean(g: OGraph, current: str, prefill: float = 10000.0,
         return e
 
     return rec(current)
+
+
+# ---------------------------------------------------------------------------
+# config 5: need probability per backend type and window (derived from
+# plan_prewarm's completion distribution, prewarm.py:65-67, simcore.py:450-487)
+# ---------------------------------------------------------------------------
+
+def need_grid(svc_samples: Sequence[float], successors: Sequence[tuple], now: float,
+              windows: Sequence[float], n_types: int) -> np.ndarray:
+    """need[t, k] = sum_{(p_s, type) in successors, type == t} p_s * P(C < now + W_k),
+    C = now + s conditioned on C > now (all samples if none), P(C < x) =
+    1 - survival(x)."""
+    comp = [now + s for s in svc_samples]
+    live = [c for c in comp if c > now] or comp
+    out = np.zeros((n_types, len(windows)))
+    for k, wk in enumerate(windows):
+        pneed = 1.0 - survival(live, now + wk) if live else 0.0
+        for p_s, t in successors:
+            if t is not None and t >= 0:
+                out[t, k] += p_s * pneed
+    return out

@@ -49,6 +49,8 @@ _SIG = {
     "pdg_mc_scratch_bytes": (C.c_size_t, [_I32, _I32, _I32]),
     "pdg_mc_remaining_demand": (C.c_int, [_P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P,
                                           C.c_size_t, _P]),
+    "pdg_plan_prewarm": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]),
+    "pdg_prewarm_need": (C.c_int, [_P, _P, _P, _P, _I64, _P, _I32, _I32, _P, _P, _P]),
 }
 
 # Every symbol include/pdg_b200.h declares (tests check the .so exports them).

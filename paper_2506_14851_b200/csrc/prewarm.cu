@@ -1,0 +1,260 @@
+// K4: backend-prewarm estimator for sm_100a.
+//
+// K4a prewarm_plan_kernel -- batched, bit-exact pdgsim.prewarm.plan_prewarm
+//     (prewarm.py:42-96): one warp per (application, successor) job.  The
+//     completion samples are conditioned on "still running" (> now, else
+//     all), bucketed (distributions.py:79-105); the candidate triggers are
+//     max(boundary - t_p, now) and now; the plan takes the latest candidate t_s
+//     with p_s * survival(t_s + t_p) >= K, survival(x) = #{s >= x} / n
+//     (distributions.py:73-77).  p_e is monotone in t_s, so "first hit in
+//     descending order" == "largest satisfying candidate": every lane scores
+//     its candidates independently and a warp max picks the trigger.
+//
+// K4b prewarm_need_kernel -- the per-backend-type need probability over a
+//     window grid (BASELINE config 5): for each queued application and window
+//     edge W_k, need[a, type(v), k] = sum over successors v of the current
+//     unit of p_s(v) * P(completion < now + W_k), with the completion time
+//     distribution of the current unit taken exactly as _plan_prewarms builds
+//     it (simcore.py:450-487: now + unconditioned service samples, then the
+//     "> now" conditioning of plan_prewarm).  One warp per application, one
+//     lane per window; the sorted service pools make each survival a binary
+//     search.  Output need[N, T, K] (float32) is the HBM-bound part.
+#include "common.cuh"
+
+namespace pdg {
+
+struct PlanArgs {
+  const double* pool;       // completion samples (absolute times)
+  const int32_t* off;       // [J]
+  const int32_t* len;       // [J]
+  const int32_t* bucket_count;
+  const double* p_s;
+  const double* t_p;
+  const double* knob;
+  const double* now;
+  int64_t n_jobs;
+  uint8_t* has_plan;
+  double* trigger;
+  double* p_e;
+  double* scratch;          // per-warp conditioned samples
+  int scratch_per_warp;
+};
+
+// count of cond samples >= x (cond = samples > now, or all if none)
+__device__ __forceinline__ int count_ge(const double* s, int n, double now, bool all, double x,
+                                       int lane) {
+  int c = 0;
+  for (int i = lane; i < n; i += 32) {
+    const double v = s[i];
+    c += ((all || v > now) && v >= x) ? 1 : 0;
+  }
+  return warp_sum(c);
+}
+
+__global__ void __launch_bounds__(128) prewarm_plan_kernel(PlanArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = gw; j < a.n_jobs; j += nw) {
+    const double* s = a.pool + a.off[j];
+    const int n = a.len[j];
+    const double now = a.now[j], p_s = a.p_s[j], t_p = a.t_p[j], knob = a.knob[j];
+    if (p_s < knob || n <= 0) {                      // prewarm.py:63-64
+      if (lane == 0) { a.has_plan[j] = 0; a.trigger[j] = 0.0; a.p_e[j] = 0.0; }
+      continue;
+    }
+    // conditioning on "still running" (prewarm.py:65-67)
+    int live = 0;
+    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+    for (int i = lane; i < n; i += 32) live += s[i] > now ? 1 : 0;
+    live = warp_sum(live);
+    const bool all = live == 0;
+    const int m = all ? n : live;
+    for (int i = lane; i < n; i += 32) {
+      const double v = s[i];
+      if (all || v > now) { lo = fmin(lo, v); hi = fmax(hi, v); }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
+    }
+    // bucket boundaries (distributions.py:120-126): [lo] if degenerate, else
+    // lo + j*w for j = 0..k with w = (hi - lo)/k
+    const int k = a.bucket_count[j];
+    const bool degen = lo == hi;
+    const double w = degen ? 0.0 : __ddiv_rn(dsub(hi, lo), small_int_to_double(k));
+    const int nb = degen ? 1 : k + 1;
+    // candidates: max(b - t_p, now) for each boundary, plus now
+    double best_ts = -__longlong_as_double(0x7ff0000000000000ll), best_pe = 0.0;
+    bool any = false;
+    for (int c = lane; c <= nb; c += 32) {
+      double ts;
+      if (c == nb) {
+        ts = now;
+      } else {
+        const double b = c == 0 ? lo : dadd(lo, dmul(small_int_to_double(c), w));
+        const double t = dsub(b, t_p);
+        ts = t > now ? t : now;
+      }
+      const double x = dadd(ts, t_p);
+      int cnt = 0;
+      for (int i = 0; i < n; ++i) {
+        const double v = s[i];
+        cnt += ((all || v > now) && v >= x) ? 1 : 0;
+      }
+      const double pe = dmul(p_s, __ddiv_rn(small_int_to_double(cnt), small_int_to_double(m)));
+      if (pe >= knob && ts > best_ts) { best_ts = ts; best_pe = pe; any = true; }
+    }
+    const bool anyw = __any_sync(kFull, any);
+    // warp arg-max of the satisfying trigger
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ots = __shfl_xor_sync(kFull, best_ts, o);
+      const double ope = __shfl_xor_sync(kFull, best_pe, o);
+      if (ots > best_ts) { best_ts = ots; best_pe = ope; }
+    }
+    if (!anyw) {                                     // prewarm.py:87-96
+      const double x = dadd(now, t_p);
+      const int cnt = count_ge(s, n, now, all, x, lane);
+      best_ts = now;
+      best_pe = dmul(p_s, __ddiv_rn(small_int_to_double(cnt), small_int_to_double(m)));
+    }
+    if (lane == 0) { a.has_plan[j] = 1; a.trigger[j] = best_ts; a.p_e[j] = best_pe; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+struct NeedArgs {
+  const double* svc_sorted;     // unconditioned service samples, ascending, per unit
+  const int32_t* svc_off;       // [U] per global unit
+  const int32_t* svc_len;
+  const int32_t* graph_base;    // [G]
+  const int32_t* succ_off;      // [U]
+  const int32_t* succ_len;      // [U]
+  const int32_t* succ_nxt;      // local unit index
+  const double* succ_p;         // branch probability (pdgraph.py:182-194)
+  const int32_t* unit_type;     // [U] backend type (warm content), -1 none
+  const int32_t* graph;         // [N] job graph
+  const int32_t* unit;          // [N] current unit (local)
+  const double* now;            // [N]
+  const double* windows;        // [K] window edges W_k (relative)
+  int n_types, n_windows;
+  int64_t n;
+  float* need;                  // [N, T, K] optional
+  double* agg;                  // [T, K] optional, sum over applications
+};
+
+// first index i in the ascending array with now + s[i] >= x  (exact f64)
+__device__ __forceinline__ int lower_bound_abs(const double* s, int n, double now, double x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (dadd(now, s[mid]) >= x) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) prewarm_need_kernel(NeedArgs a) {
+  extern __shared__ double sagg[];                  // [T*K] block partial aggregate
+  const int lane = threadIdx.x & 31;
+  const int TK = a.n_types * a.n_windows;
+  if (a.agg) {
+    for (int i = threadIdx.x; i < TK; i += blockDim.x) sagg[i] = 0.0;
+    __syncthreads();
+  }
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int kwin = lane < a.n_windows ? lane : -1;
+  const double wk = kwin >= 0 ? a.windows[kwin] : 0.0;
+  for (int64_t app = gw; app < a.n; app += nw) {
+    const int gbase = a.graph_base[a.graph[app]];
+    const int u = gbase + a.unit[app];
+    const double now = a.now[app];
+    const double* s = a.svc_sorted + a.svc_off[u];
+    const int n = a.svc_len[u];
+    // completion = now + s; conditioned on > now (all if none)
+    const int first_live = lower_bound_abs(s, n, now, __longlong_as_double(
+        __double_as_longlong(now) + 1));             // smallest value > now
+    const int live = n - first_live;
+    const int base = live > 0 ? first_live : 0;
+    const int m = live > 0 ? live : n;
+    float out[8];
+    int types[8];
+    const int ns = a.succ_len[u] < 8 ? a.succ_len[u] : 8;
+    double pneed = 0.0;
+    if (kwin >= 0 && m > 0) {
+      const double x = dadd(now, wk);
+      const int ge = n - lower_bound_abs(s + base, n - base, now, x) - base;
+      const int cnt_ge = ge < 0 ? 0 : ge;
+      pneed = 1.0 - __ddiv_rn(small_int_to_double(cnt_ge), small_int_to_double(m));
+    }
+    for (int q = 0; q < ns; ++q) {
+      const int v = gbase + a.succ_nxt[a.succ_off[u] + q];
+      types[q] = a.unit_type[v];
+      out[q] = float(dmul(a.succ_p[a.succ_off[u] + q], pneed));
+    }
+    if (a.need && kwin >= 0) {
+      float* row = a.need + app * int64_t(TK);
+      for (int t = 0; t < a.n_types; ++t) {
+        float acc = 0.f;
+        for (int q = 0; q < ns; ++q) acc += types[q] == t ? out[q] : 0.f;
+        __stcs(row + t * a.n_windows + kwin, acc);
+      }
+    }
+    if (a.agg && kwin >= 0) {
+      for (int q = 0; q < ns; ++q)
+        if (types[q] >= 0)
+          atomicAdd(&sagg[types[q] * a.n_windows + kwin],
+                    dmul(a.succ_p[a.succ_off[u] + q], pneed));
+    }
+  }
+  if (a.agg) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < TK; i += blockDim.x)
+      if (sagg[i] != 0.0) atomicAdd(a.agg + i, sagg[i]);
+  }
+}
+
+}  // namespace pdg
+
+using namespace pdg;
+
+extern "C" int pdg_plan_prewarm(const double* pool, const int32_t* off, const int32_t* len,
+                                const int32_t* bucket_count, const double* p_s,
+                                const double* t_p, const double* knob, const double* now,
+                                int64_t n_jobs, uint8_t* has_plan, double* trigger,
+                                double* p_e, void* stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && (!pool || !off || !len || !bucket_count || !p_s || !t_p ||
+                                    !knob || !now || !has_plan || !trigger || !p_e))) {
+    set_error("pdg_plan_prewarm: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (n_jobs == 0) return PDG_OK;
+  PlanArgs a{pool, off, len, bucket_count, p_s, t_p, knob, now, n_jobs, has_plan, trigger, p_e,
+             nullptr, 0};
+  int64_t blocks = (n_jobs * 32 + 127) / 128;
+  const int64_t cap = int64_t(sm_count()) * 16;
+  if (blocks > cap) blocks = cap;
+  prewarm_plan_kernel<<<unsigned(blocks), 128, 0, (cudaStream_t)stream>>>(a);
+  return launch_status("prewarm_plan_kernel");
+}
+
+extern "C" int pdg_prewarm_need(const pdg_prewarm_tables* t, const int32_t* graph,
+                                const int32_t* unit, const double* now, int64_t n,
+                                const double* windows, int32_t n_windows, int32_t n_types,
+                                float* need, double* agg, void* stream) {
+  if (!t || n < 0 || n_windows < 1 || n_windows > 32 || n_types < 1 || n_types > 64 ||
+      (n > 0 && (!graph || !unit || !now || !windows))) {
+    set_error("pdg_prewarm_need: invalid arguments (1 <= windows <= 32, 1 <= types <= 64)");
+    return PDG_EINVAL;
+  }
+  if (n == 0) return PDG_OK;
+  NeedArgs a{t->svc_sorted, t->svc_off, t->svc_len, t->graph_base, t->succ_off, t->succ_len,
+             t->succ_nxt, t->succ_p, t->unit_type, graph, unit, now, windows, n_types,
+             n_windows, n, need, agg};
+  int64_t blocks = (n * 32 + 255) / 256;
+  const int64_t cap = int64_t(sm_count()) * 8;
+  if (blocks > cap) blocks = cap;
+  const size_t smem = agg ? size_t(n_types) * n_windows * sizeof(double) : 0;
+  prewarm_need_kernel<<<unsigned(blocks), 256, smem, (cudaStream_t)stream>>>(a);
+  return launch_status("prewarm_need_kernel");
+}

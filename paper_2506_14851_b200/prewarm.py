@@ -1,0 +1,179 @@
+"""GPU backend-prewarm estimator (K4): drop-in ``plan_prewarm`` and the
+per-backend-type need-probability grid.
+
+* ``plan_prewarm`` / ``plan_prewarm_batch`` -- the reference's latest-safe
+  trigger rule (prewarm.py:42-96), bit-exact, one warp per (app, successor).
+* ``PrewarmTables.need`` -- need[a, type, window] for a whole queue (BASELINE
+  config 5), from the same completion-time samples ``_plan_prewarms`` uses
+  (simcore.py:450-487).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+
+DEFAULT_KNOB = 0.5          # prewarm.py:21
+
+
+@dataclass
+class PrewarmPlan:
+    """Mirror of the reference decision record (prewarm.py:24-39)."""
+    target_backend: object
+    p_s: float
+    t_p: float
+    trigger_time: float
+    p_e: float
+    knob: float
+
+    def __post_init__(self):
+        if not (0.0 <= self.knob <= 1.0):
+            raise ValueError(f"knob must be in [0, 1], got {self.knob}")
+        if self.p_s < self.knob:
+            raise ValueError("plan must not exist when p_s < K")
+
+
+def plan_prewarm_batch(samples: Sequence[Sequence[float]], bucket_count, p_s, t_p, knob, now):
+    """Vectorised plan_prewarm over J jobs (lists of absolute completion
+    samples).  Returns (has_plan bool[J], trigger f64[J], p_e f64[J])."""
+    J = len(samples)
+    L = _lib.lib()
+    dev = torch.device("cuda")
+    lens = np.array([len(s) for s in samples], dtype=np.int32)
+    offs = np.zeros(J, dtype=np.int32)
+    if J > 1:
+        offs[1:] = np.cumsum(lens)[:-1]
+    pool = np.concatenate([np.asarray(s, dtype=np.float64) for s in samples]) if J else np.zeros(0)
+
+    def col(x, dt):
+        a = np.broadcast_to(np.asarray(x, dtype=dt), (J,)).copy()
+        return torch.from_numpy(a).to(dev)
+
+    knob_a = np.broadcast_to(np.asarray(knob, dtype=np.float64), (J,))
+    tp_a = np.broadcast_to(np.asarray(t_p, dtype=np.float64), (J,))
+    if ((knob_a < 0) | (knob_a > 1)).any():
+        raise ValueError("knob must be in [0, 1]")
+    if (tp_a < 0).any():
+        raise ValueError("warm-up duration must be >= 0")
+    if J == 0:
+        return np.zeros(0, bool), np.zeros(0), np.zeros(0)
+    tpool = torch.from_numpy(pool if pool.size else np.zeros(1)).to(dev)
+    has = torch.empty(J, dtype=torch.uint8, device=dev)
+    trig = torch.empty(J, dtype=torch.float64, device=dev)
+    pe = torch.empty(J, dtype=torch.float64, device=dev)
+    args = [col(offs, np.int32), col(lens, np.int32), col(bucket_count, np.int32),
+            col(p_s, np.float64), col(t_p, np.float64), col(knob, np.float64),
+            col(now, np.float64)]
+    _lib.check(L.pdg_plan_prewarm(_lib.ptr(tpool), *[_lib.ptr(t) for t in args], J,
+                                  _lib.ptr(has), _lib.ptr(trig), _lib.ptr(pe),
+                                  _lib.stream_ptr()), "pdg_plan_prewarm")
+    return has.cpu().numpy().astype(bool), trig.cpu().numpy(), pe.cpu().numpy()
+
+
+def plan_prewarm(completion_dist, p_s: float, t_p: float, knob: float, now: float,
+                 target_backend=None) -> Optional[PrewarmPlan]:
+    """Same contract as the reference; `completion_dist` needs `.samples` and
+    `.bucket_count` (an EmpiricalDistribution)."""
+    if not (0.0 <= knob <= 1.0):
+        raise ValueError(f"knob must be in [0, 1], got {knob}")
+    if t_p < 0:
+        raise ValueError(f"warm-up duration must be >= 0, got {t_p}")
+    if p_s < knob:
+        return None
+    has, trig, pe = plan_prewarm_batch([list(completion_dist.samples)],
+                                       completion_dist.bucket_count, p_s, t_p, knob, now)
+    if not has[0]:
+        return None
+    return PrewarmPlan(target_backend=target_backend, p_s=p_s, t_p=t_p,
+                       trigger_time=float(trig[0]), p_e=float(pe[0]), knob=knob)
+
+
+# ---------------------------------------------------------------------------
+# need-probability grid (config 5)
+# ---------------------------------------------------------------------------
+
+class PrewarmTablesC(C.Structure):
+    _fields_ = [(nm, C.c_void_p) for nm in ("svc_sorted", "svc_off", "svc_len", "graph_base",
+                                            "succ_off", "succ_len", "succ_nxt", "succ_p",
+                                            "unit_type")]
+
+
+class PrewarmTables:
+    """Sorted service-time pools, successor probabilities and backend types
+    per unit, resident on the device."""
+
+    def __init__(self, *, svc_sorted, svc_off, svc_len, graph_base, succ_off, succ_len,
+                 succ_nxt, succ_p, unit_type, n_types, device="cuda"):
+        _lib.lib()
+        dev = torch.device(device)
+
+        def t(a, dt):
+            a = np.ascontiguousarray(np.asarray(a, dtype=dt))
+            return torch.from_numpy(a if a.size else np.zeros(1, dtype=dt)).to(dev)
+
+        self.device = dev
+        self.n_types = int(n_types)
+        self.t = dict(svc_sorted=t(svc_sorted, np.float64), svc_off=t(svc_off, np.int32),
+                      svc_len=t(svc_len, np.int32), graph_base=t(graph_base, np.int32),
+                      succ_off=t(succ_off, np.int32), succ_len=t(succ_len, np.int32),
+                      succ_nxt=t(succ_nxt, np.int32), succ_p=t(succ_p, np.float64),
+                      unit_type=t(unit_type, np.int32))
+        self.c = PrewarmTablesC(*[_lib.ptr(self.t[nm]) for nm, _ in PrewarmTablesC._fields_])
+
+    @classmethod
+    def from_graphs(cls, graphs: dict, prefill_rate=10000.0, decode_rate=50.0, device="cuda"):
+        """Tables for named graphs (reference PDGraph or KBGraph); graph and
+        unit order match GraphBank (graph insertion order, sorted unit ids)."""
+        svc, soff, slen, gbase = [], [], [], []
+        s_off, s_len, s_nxt, s_p, utype = [], [], [], [], []
+        types: dict = {}
+        for nm, g in graphs.items():
+            order = sorted(g.units)
+            pos = {u: i for i, u in enumerate(order)}
+            gbase.append(len(slen))
+            for uid in order:
+                u = g.units[uid]
+                if u.is_llm:       # simcore.py:480-487 (records' joint i, o)
+                    xs = [r.input_len / prefill_rate + r.output_len / decode_rate
+                          for r in u.records]
+                else:
+                    xs = list(u.duration_dist.samples)
+                soff.append(len(svc))
+                slen.append(len(xs))
+                svc.extend(sorted(xs))
+                succ = sorted(u.successors.items())
+                s_off.append(len(s_nxt))
+                s_len.append(len(succ))
+                s_nxt.extend(pos[v] for v, _ in succ)
+                s_p.extend(p for _, p in succ)
+                backend = getattr(u, "backend", None)
+                wc = backend.warm_content_id() if backend is not None else getattr(
+                    u, "warm_content", None)
+                utype.append(types.setdefault(wc, len(types)) if wc is not None else -1)
+        tb = cls(svc_sorted=svc, svc_off=soff, svc_len=slen, graph_base=gbase, succ_off=s_off,
+                 succ_len=s_len, succ_nxt=s_nxt, succ_p=s_p, unit_type=utype,
+                 n_types=max(len(types), 1), device=device)
+        tb.type_ids = types
+        return tb
+
+    def need(self, graph_idx, unit_idx, now, windows, *, dense=True, aggregate=True,
+             out=None, stream=None):
+        """need[N, T, K] float32 (dense) and/or agg[T, K] float64 over the queue."""
+        n = int(graph_idx.numel())
+        K = int(windows.numel())
+        dev = self.device
+        need = out if out is not None else (
+            torch.empty((n, self.n_types, K), dtype=torch.float32, device=dev) if dense else None)
+        agg = torch.zeros((self.n_types, K), dtype=torch.float64, device=dev) if aggregate else None
+        L = _lib.lib()
+        _lib.check(L.pdg_prewarm_need(C.byref(self.c), _lib.ptr(graph_idx), _lib.ptr(unit_idx),
+                                      _lib.ptr(now), n, _lib.ptr(windows), K, self.n_types,
+                                      _lib.ptr(need), _lib.ptr(agg), _lib.stream_ptr(stream)),
+                   "pdg_prewarm_need")
+        return need, agg
