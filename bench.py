@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--cpu-apps", type=int, default=1200,
                     help="apps in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the config-4 stream and config-5 prewarm sections")
     ap.add_argument("--ncu", action="store_true",
                     help="profiling run: skip CUPTI launch counting, e2e and CPU legs")
     return ap.parse_args()
@@ -465,6 +467,12 @@ def run_ours(args):
         "gpu_launches_per_step": launches, "kernels": kernel_names,
         "e2e": e2e, "roofline": roofline, "k1_refresh": k1, "clocks": clk,
     }
+    if world == 1 and not args.no_extra:
+        del eng, q, w
+        torch.cuda.empty_cache()
+        line["config4_stream"] = bench_stream(dev)
+        torch.cuda.empty_cache()
+        line["config5_prewarm"] = bench_need(dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate = cpu_rate(args.cpu_apps, 1, args.cpu_apps, 1000, b)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
@@ -476,6 +484,141 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# BASELINE config 4 (refinement stream) and config 5 (prewarm need grid)
+# ---------------------------------------------------------------------------
+
+STREAM_TEMPLATES = ["code-gen", "fact-verify", "verify-chain-bimodal", "bimodal",
+                    "plan-execute", "react-loop", "fanout-reduce", "cond"]
+
+
+def bench_stream(dev, n_apps=1_000_000, n_events=100_000, batch=1000):
+    """Config 4: 1M-app queue of template PDGraphs (the reference's own
+    archetypes, with correlation masks); 100k unit-completion events with
+    observations, applied in micro-batches: K3+K2 re-estimate, K1 re-score of
+    the touched rows, K5 re-sort of the whole queue.  Device-timed."""
+    import gzip
+    import torch
+    from paper_2506_14851_b200.estimator import DemandEngine
+    from paper_2506_14851_b200.graphs import graph_from_kb
+    from paper_2506_14851_b200.queue import HistQueue
+    from paper_2506_14851_b200.stream import RefinementStream
+    from tools import synth
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "graphs.json.gz"), "rt") as fh:
+        docs = json.load(fh)
+    graphs = {k: graph_from_kb(docs[k]) for k in STREAM_TEMPLATES}
+    q = synth.template_queue(graphs, n_apps, seed=41)
+    ev = synth.events(graphs, q, n_events, seed=42)
+    eng = DemandEngine(graphs, device=str(dev))
+    hq = HistQueue(n_apps, N_BINS)
+    gi = torch.from_numpy(q["graph"]).to(dev)
+    ui = torch.from_numpy(q["unit"].copy()).to(dev)
+    seeds = torch.arange(n_apps, dtype=torch.int64, device=dev) * 1000003
+    eng.run(gi, ui, seeds, n=N_SAMP, bucket_count=N_BINS, queue=hq)
+    hq.est_age[:n_apps] = 0.0
+    hq.age[:n_apps] = 0.0
+    hq.n = n_apps
+    hq.score()
+    st = RefinementStream(eng, hq, gi, ui, bucket_count=N_BINS)
+    st.order()
+    # pinned host event buffers; each batch is uploaded inside its timed span
+    h = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+         for k, v in (("app", ev["app"]), ("next", ev["next"]), ("comp", ev["completed"]),
+                      ("obs", ev["obs"]), ("seed", ev["seed"]))}
+    h["att"] = torch.full((n_events,), 5.0, dtype=torch.float64).pin_memory()
+    d = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in h.items()}
+    stream = torch.cuda.current_stream()
+    nb = n_events // batch
+
+    def run_batch(i, evs=None):
+        sl = slice(i * batch, (i + 1) * batch)
+        for k in h:
+            d[k][sl].copy_(h[k][sl], non_blocking=True)
+        if evs:
+            evs[0].record(stream)
+        st.process(d["app"][sl], d["next"][sl], d["seed"][sl], d["comp"][sl], d["obs"][sl],
+                   d["att"][sl], resort=True)
+
+    run_batch(0)                                       # warm-up (re-applies batch 0)
+    torch.cuda.synchronize()
+    marks = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(nb)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(nb):
+        sub = torch.cuda.Event(enable_timing=True)
+        run_batch(i, [sub])
+        marks[i] = (sub, torch.cuda.Event(enable_timing=True))
+        marks[i][1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    lat = np.array([a.elapsed_time(b) for a, b in marks])
+    return {"workload": f"config4: {n_apps} queued template apps ({len(STREAM_TEMPLATES)} "
+                        f"reference archetypes), {n_events} refinement events in batches of "
+                        f"{batch}; per batch K3+K2+a4 re-estimate, K1 re-score, K5 full re-sort",
+            "events_per_s": n_events / (total_ms / 1e3), "batch": batch,
+            "batch_latency_ms_p50": float(np.median(lat)),
+            "batch_latency_ms_p99": float(np.percentile(lat, 99)),
+            "note": "latency = batch upload issued -> global order visible (device events); "
+                    "at 100k events/s a 1000-event batch is 10 ms of arrivals"}
+
+
+def bench_need(dev, n_apps=1_000_000, n_templates=1024, steps=10):
+    """Config 5: need probability for 16 backend types x 32 windows over 1M
+    apps (templates: depth-8 synth graphs, unit types random in [0,16))."""
+    import torch
+    from paper_2506_14851_b200.prewarm import PrewarmTables
+    from tools import synth
+    w = synth.make(n_templates, N_REC, seed=77)
+    rng = np.random.default_rng(78)
+    A, U, R = n_templates, synth.U, N_REC
+    svc = np.sort(w["dur"], axis=2).reshape(-1)
+    counts = np.zeros((A, U, U))
+    for v in range(U):
+        counts[:, :, v] = (w["nxt"] == v).sum(axis=2)
+    s_off = np.arange(A * U) * synth.SLOT
+    s_len = w["succ_len"].reshape(-1)
+    s_nxt = w["succ_nxt"].reshape(-1)
+    s_p = np.zeros(A * U * synth.SLOT)
+    for a_u in range(A * U):
+        a, u = divmod(a_u, U)
+        for q in range(s_len[a_u]):
+            s_p[a_u * synth.SLOT + q] = counts[a, u, s_nxt[a_u * synth.SLOT + q]] / R
+    tb = PrewarmTables(svc_sorted=svc, svc_off=np.arange(A * U) * R, svc_len=np.full(A * U, R),
+                       graph_base=np.arange(A) * U, succ_off=s_off, succ_len=s_len,
+                       succ_nxt=s_nxt, succ_p=s_p, unit_type=rng.integers(0, 16, A * U),
+                       n_types=16, device=str(dev))
+    g = torch.from_numpy(rng.integers(0, A, n_apps).astype(np.int32)).to(dev)
+    u = torch.from_numpy(rng.integers(0, U, n_apps).astype(np.int32)).to(dev)
+    now = torch.from_numpy(rng.uniform(0, 100, n_apps)).to(dev)
+    win = torch.linspace(2.0, 64.0, 32, dtype=torch.float64, device=dev)
+    need = torch.empty((n_apps, 16, 32), dtype=torch.float32, device=dev)
+    for _ in range(3):
+        tb.need(g, u, now, win, out=need)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    for e0, e1 in ev:
+        e0.record()
+        tb.need(g, u, now, win, out=need)
+        e1.record()
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    # algorithmic bytes per app: dense need row out + job (graph, unit, now)
+    # + the binary-searched service samples (<= 32 lanes x log2(256) probes)
+    bytes_app = 16 * 32 * 4 + 4 + 4 + 8
+    peak, _ = measured_peaks()
+    return {"workload": f"config5: need[{n_apps},16,32] float32 + [16,32] aggregate over "
+                        f"{n_apps} apps ({n_templates} depth-8 templates)",
+            "apps_per_s": n_apps / (ms / 1e3), "ms_per_launch": ms,
+            "roofline": {"bound": "hbm", "bytes_per_app": bytes_app,
+                         "achieved": bytes_app * n_apps / (ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s",
+                         "frac": bytes_app * n_apps / (ms / 1e3) / 1e9 / peak}}
 
 
 def main():

@@ -71,13 +71,16 @@ typedef struct {
   int64_t stride;          /* counts row stride in elements, multiple of 8        */
 } pdg_hist_rows;
 
-/* age: [N] attained service now.  penalty: overrun_penalty_factor.
- * out_key (optional): (float32 key bits << 32) | tiebreak[i]; tiebreak is the
- * position of (arrival_time, app_instance_id) in arrival order (sched.py:168). */
+/* age: [rows] attained service now.  penalty: overrun_penalty_factor.
+ * out_key (optional): (float32 key bits << 32) | tiebreak[row]; tiebreak is
+ * the position of (arrival_time, app_instance_id) in arrival order
+ * (sched.py:168).  row_idx (optional): score only rows row_idx[0..n) (the
+ * incremental re-score after refinement events); otherwise rows 0..n-1.
+ * All per-row inputs and outputs are indexed by row. */
 int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* age,
                            int64_t n, double penalty, float* out_key_f32,
                            uint8_t* out_flags, const uint32_t* tiebreak,
-                           uint64_t* out_key, void* stream);
+                           uint64_t* out_key, const int32_t* row_idx, void* stream);
 
 /* ---------------------------------------------------------------------------
  * K5  global order: stable radix sort of packed 64-bit keys ascending,

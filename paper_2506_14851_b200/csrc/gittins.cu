@@ -87,6 +87,7 @@ struct HistArgs {
   uint8_t* __restrict__ out_flags;
   const uint32_t* __restrict__ tiebreak;
   uint64_t* __restrict__ out_key;
+  const int32_t* __restrict__ row_idx;   // optional: score only these rows
 };
 
 // Exact d = fl(fl(mid_j + est) - age), as sched.py:179 then sched.py:114.
@@ -193,7 +194,9 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
   // row is scored
   uint4 nxt[CH];
   int knxt;
-  auto load = [&](int64_t r, uint4 (&dst)[CH], int& kk) {
+  auto row_of = [&](int64_t i) -> int64_t { return a.row_idx ? int64_t(__ldg(a.row_idx + i)) : i; };
+  auto load = [&](int64_t i, uint4 (&dst)[CH], int& kk) {
+    const int64_t r = row_of(i);
     const uint4* row = reinterpret_cast<const uint4*>(a.counts + r * a.stride);
     kk = __ldg(a.nbins + r);
 #pragma unroll
@@ -203,14 +206,15 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
     }
   };
   load(gw, nxt, knxt);
-  for (int64_t r = gw; r < a.n; r += nw) {
+  for (int64_t i = gw; i < a.n; i += nw) {
+    const int64_t r = row_of(i);
     uint4 cur[CH];
 #pragma unroll
     for (int c = 0; c < CH; ++c) cur[c] = nxt[c];
     const int k = knxt;
     const double lo = __ldg(a.lo + r), w = __ldg(a.width + r);
     const double est = __ldg(a.est + r), age = __ldg(a.age + r);
-    if (r + nw < a.n) load(r + nw, nxt, knxt);
+    if (i + nw < a.n) load(i + nw, nxt, knxt);
 
     float m[CH][8], d[CH][8];
 #pragma unroll
@@ -261,7 +265,8 @@ extern "C" int pdg_gittins_rank_f64(const double* values, const double* probs,
 extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* age,
                                       int64_t n, double penalty, float* out_key_f32,
                                       uint8_t* out_flags, const uint32_t* tiebreak,
-                                      uint64_t* out_key, void* stream) {
+                                      uint64_t* out_key, const int32_t* row_idx,
+                                      void* stream) {
   if (!rows || n < 0 || (n > 0 && (!age || !rows->lo || !rows->width || !rows->est_age ||
                                    !rows->nbins || !rows->counts))) {
     set_error("pdg_gittins_score_hist: invalid arguments");
@@ -273,7 +278,8 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
   }
   if (n == 0) return PDG_OK;
   HistArgs a{rows->lo, rows->width, rows->est_age, rows->nbins, rows->counts,
-             rows->stride, age, n, penalty, out_key_f32, out_flags, tiebreak, out_key};
+             rows->stride, age, n, penalty, out_key_f32, out_flags, tiebreak, out_key,
+             row_idx};
   const int threads = 256;
   int64_t blocks = (n * 32 + threads - 1) / threads;
   const int64_t cap = int64_t(sm_count()) * 4;

@@ -96,14 +96,15 @@ class HistQueue:
 
     # -- scoring ---------------------------------------------------------------
     def score(self, penalty: float = 2.0, n: Optional[int] = None, stream=None,
-              keys: bool = True) -> None:
-        """K1b over the first n rows: key_f32, flags and packed sort keys."""
-        n = self.n if n is None else int(n)
+              keys: bool = True, rows: Optional[torch.Tensor] = None) -> None:
+        """K1b over the first n rows (or only `rows`, an int32 device tensor):
+        key_f32, flags and packed sort keys, indexed by row."""
+        n = (self.n if n is None else int(n)) if rows is None else int(rows.numel())
         L = _lib.lib()
         _lib.check(L.pdg_gittins_score_hist(
             C.byref(self._rows), _lib.ptr(self.age), n, float(penalty),
             _lib.ptr(self.key_f32), _lib.ptr(self.flags), _lib.ptr(self.tiebreak),
-            _lib.ptr(self.keys) if keys else None, _lib.stream_ptr(stream)),
+            _lib.ptr(self.keys) if keys else None, _lib.ptr(rows), _lib.stream_ptr(stream)),
             "pdg_gittins_score_hist")
 
     def order(self, n: Optional[int] = None, stream=None,

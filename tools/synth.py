@@ -104,3 +104,45 @@ def jobs(n_apps: int, seed: int = 7):
     rng = np.random.default_rng(seed)
     return {"unit": rng.integers(0, U, n_apps).astype(np.int32),
             "seed": rng.integers(0, 2**62, n_apps).astype(np.int64)}
+
+
+# ---------------------------------------------------------------------------
+# config 4: refinement events over a queue of template apps
+# ---------------------------------------------------------------------------
+
+def template_queue(graphs: dict, n_apps: int, seed: int = 7):
+    """Queue of n_apps instances of the template graphs (name -> KBGraph),
+    each at a random unit that has at least one successor."""
+    rng = np.random.default_rng(seed)
+    names = list(graphs)
+    orders = {nm: sorted(graphs[nm].units) for nm in names}
+    gi = rng.integers(0, len(names), n_apps).astype(np.int32)
+    ui = np.zeros(n_apps, dtype=np.int32)
+    for g, nm in enumerate(names):
+        cand = [i for i, u in enumerate(orders[nm]) if graphs[nm].units[u].successors]
+        sel = gi == g
+        ui[sel] = rng.choice(cand, int(sel.sum()))
+    return {"names": names, "orders": orders, "graph": gi, "unit": ui}
+
+
+def events(graphs: dict, q: dict, n_events: int, seed: int = 7):
+    """n_events unit completions on distinct apps: the app's current unit
+    completes with an observation drawn from that unit's records; the next
+    unit is drawn by branch probability (pdgraph.py:182-194)."""
+    rng = np.random.default_rng(seed)
+    apps = rng.choice(len(q["graph"]), n_events, replace=False).astype(np.int32)
+    nxt = np.zeros(n_events, dtype=np.int32)
+    obs = np.zeros((n_events, 3))
+    for e, a in enumerate(apps):
+        nm = q["names"][q["graph"][a]]
+        g = graphs[nm]
+        uid = q["orders"][nm][q["unit"][a]]
+        unit = g.units[uid]
+        succ = sorted(unit.successors.items())
+        p = np.array([x for _, x in succ])
+        k = rng.choice(len(succ), p=p / p.sum())
+        nxt[e] = q["orders"][nm].index(succ[k][0])
+        r = unit.records[rng.integers(0, len(unit.records))]
+        obs[e] = (r.input_len, r.output_len, float(r.parallelism))
+    return {"app": apps, "completed": q["unit"][apps].copy(), "next": nxt, "obs": obs,
+            "seed": rng.integers(0, 2**62, n_events).astype(np.int64)}
