@@ -83,6 +83,16 @@ int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* age,
                            uint64_t* out_key, const int32_t* row_idx, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * a4  ApplicationInstance.set_remaining's bucketing as a standalone call
+ * (sched.py:170-181, distributions.py:79-105): rows of n float64 samples ->
+ * (lo, width, nbins, u16 counts[stride]) in the pdg_hist_rows layout.  The
+ * demand engine fuses the same epilogue.  n <= 65535.
+ * ------------------------------------------------------------------------- */
+int pdg_bucketize(const double* samples, int64_t rows, int32_t n, int32_t k, double* lo,
+                  double* width, int32_t* nbins, uint16_t* counts, int64_t stride,
+                  void* stream);
+
+/* ---------------------------------------------------------------------------
  * K5  global order: stable radix sort of packed 64-bit keys ascending,
  * carrying a u32 payload (the queue slot).  Replaces the Python min()/sort
  * over _task_sort_key (simcore.py:339-344, 512-516).

@@ -44,6 +44,7 @@ _SIG = {
     "pdg_gittins_rank_f64": (C.c_int, [_P, _P, _P, _I64, _I32, _P, _P]),
     "pdg_gittins_score_hist": (C.c_int, [C.POINTER(HistRows), _P, _I64, _D, _P, _P, _P, _P, _P,
                                                   _P]),
+    "pdg_bucketize": (C.c_int, [_P, _I64, _I32, _I32, _P, _P, _P, _P, _I64, _P]),
     "pdg_order_temp_bytes": (C.c_size_t, [_I64]),
     "pdg_order": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, C.c_size_t, _P]),
     "pdg_mc_grid_warps": (C.c_int, []),

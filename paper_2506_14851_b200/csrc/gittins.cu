@@ -327,3 +327,64 @@ extern "C" int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
                                                   (cudaStream_t)stream);
   return cuda_status(e, "pdg_order");
 }
+
+// ---------------------------------------------------------------------------
+// a4 standalone: equal-width bucketing of sample rows (distributions.py:79-105)
+// one warp per row; the engine fuses the same epilogue.
+// ---------------------------------------------------------------------------
+namespace pdg {
+__global__ void __launch_bounds__(128) bucketize_kernel(const double* __restrict__ samples,
+                                                        int64_t rows, int n, int k,
+                                                        double* lo_out, double* w_out,
+                                                        int32_t* nb_out, uint16_t* counts,
+                                                        int64_t stride) {
+  extern __shared__ uint32_t bcnt[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint32_t* cnt = bcnt + size_t(wib) * k;
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = gw; r < rows; r += nw) {
+    const double* s = samples + r * int64_t(n);
+    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+    for (int i = lane; i < n; i += 32) { lo = fmin(lo, s[i]); hi = fmax(hi, s[i]); }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
+    }
+    const int kk = lo == hi ? 1 : k;
+    const double w = lo == hi ? 0.0 : __ddiv_rn(dsub(hi, lo), small_int_to_double(k));
+    for (int b = lane; b < kk; b += 32) cnt[b] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      int idx = 0;
+      if (kk > 1) {
+        idx = __double2int_rz(__ddiv_rn(dsub(s[i], lo), w));
+        idx = idx < kk - 1 ? idx : kk - 1;
+      }
+      atomicAdd(&cnt[idx], 1u);
+    }
+    __syncwarp();
+    for (int b = lane; b < stride; b += 32)
+      counts[r * stride + b] = b < kk ? uint16_t(cnt[b]) : uint16_t(0);
+    if (lane == 0) { lo_out[r] = lo; w_out[r] = w; nb_out[r] = kk; }
+    __syncwarp();
+  }
+}
+}  // namespace pdg
+
+extern "C" int pdg_bucketize(const double* samples, int64_t rows, int32_t n, int32_t k,
+                             double* lo, double* width, int32_t* nbins, uint16_t* counts,
+                             int64_t stride, void* stream) {
+  if (rows < 0 || n < 1 || n > 65535 || k < 1 || k > 1024 || stride < k ||
+      (rows > 0 && (!samples || !lo || !width || !nbins || !counts))) {
+    set_error("pdg_bucketize: invalid arguments (n <= 65535, 1 <= k <= stride, k <= 1024)");
+    return PDG_EINVAL;
+  }
+  if (rows == 0) return PDG_OK;
+  int64_t blocks = (rows * 32 + 127) / 128;
+  const int64_t cap = int64_t(sm_count()) * 16;
+  if (blocks > cap) blocks = cap;
+  bucketize_kernel<<<unsigned(blocks), 128, 4 * k * sizeof(uint32_t), (cudaStream_t)stream>>>(
+      samples, rows, n, k, lo, width, nbins, counts, stride);
+  return launch_status("bucketize_kernel");
+}

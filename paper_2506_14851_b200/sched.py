@@ -130,6 +130,54 @@ def lstf_slack(dist, age: float, deadline: float, now: float) -> float:
 
 
 # ---------------------------------------------------------------------------
+# a4: set_remaining's bucket view (sched.py:170-181, distributions.py:79-133)
+# ---------------------------------------------------------------------------
+
+def bucketize_rows(samples, bucket_count: int):
+    """GPU bucketing of sample rows [R, n] -> (lo, width, nbins, counts u16)."""
+    x = np.ascontiguousarray(np.asarray(samples, dtype=np.float64))
+    if x.ndim == 1:
+        x = x[None, :]
+    R, n = x.shape
+    stride = (int(bucket_count) + 7) // 8 * 8
+    L = _lib.lib()
+    dev = torch.device("cuda")
+    t = torch.from_numpy(x).to(dev)
+    lo = torch.empty(R, dtype=torch.float64, device=dev)
+    w = torch.empty(R, dtype=torch.float64, device=dev)
+    nb = torch.empty(R, dtype=torch.int32, device=dev)
+    cnt = torch.empty((R, stride), dtype=torch.uint16, device=dev)
+    _lib.check(L.pdg_bucketize(_lib.ptr(t), R, n, int(bucket_count), _lib.ptr(lo), _lib.ptr(w),
+                               _lib.ptr(nb), _lib.ptr(cnt), stride, _lib.stream_ptr()),
+               "pdg_bucketize")
+    return lo.cpu().numpy(), w.cpu().numpy(), nb.cpu().numpy(), cnt.cpu().numpy()
+
+
+def bucket_points_from(lo: float, width: float, k: int, counts, n: int):
+    """(values, probs) exactly as EmpiricalDistribution.bucket_points builds
+    them from the bucket grid (distributions.py:102-104, 128-133)."""
+    if k == 1 and width == 0.0:
+        return [lo], [1.0]
+    vals = [((lo + i * width) + (lo + (i + 1) * width)) / 2.0 for i in range(k)]
+    return vals, [int(c) / n for c in counts[:k]]
+
+
+def set_remaining(app, remaining, bucket_count: int) -> None:
+    """ApplicationInstance.set_remaining with the bucketing on the GPU."""
+    samples = list(remaining.samples)
+    app.remaining = remaining
+    app.estimate_age = app.attained_service
+    lo, w, nb, cnt = bucketize_rows(np.asarray(samples)[None, :], bucket_count)
+    values, probs = bucket_points_from(float(lo[0]), float(w[0]), int(nb[0]), cnt[0],
+                                       len(samples))
+    app.bucket_values = np.asarray(values)
+    app.bucket_probs = np.asarray(probs)
+    app.shifted_values = app.bucket_values + app.estimate_age
+    app.bucket_width = len(values)
+    app.worst_case = max(samples)
+
+
+# ---------------------------------------------------------------------------
 # a3: single-instance priority (sched.py:195-234)
 # ---------------------------------------------------------------------------
 
