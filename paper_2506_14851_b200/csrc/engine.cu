@@ -17,11 +17,15 @@
 // among the unit's members).  Per step the warp compacts the still-active
 // walks (index order kept); per unit visit it compacts that unit's members
 // into a list whose position IS the rank, and lane l takes a contiguous block
-// of members, so its stream positions are consecutive: one PCG64 jump to the
-// block start (pcg64.cuh), then single LCG steps (a 64-bit word serves two
-// 32-bit bounded draws).  numpy's Lemire rejection (probability < P/2^32 per
-// draw) is detected by a warp vote and the visit is then replayed
-// sequentially by lane 0 with the exact sequential generator.
+// of ranks.  Its stream positions are then consecutive inside each draw
+// group: one PCG64 jump per group to the block start (pcg64.cuh), then single
+// LCG steps (a 64-bit word serves two 32-bit bounded draws).  A member's
+// bounded draws, its uniform and its commit happen in one loop iteration.
+//
+// numpy's Lemire rejection (probability < P/2^32 per draw) shifts every later
+// position.  A warp vote detects it; the application is then abandoned by the
+// fast kernel and recomputed from scratch by mc_serial_kernel, which runs the
+// reference algorithm with the sequential generator (one lane per app).
 #include "common.cuh"
 #include "pcg64.cuh"
 
@@ -46,7 +50,6 @@ struct __align__(16) CondDesc {      // graphs.COND_DTYPE
   double lo[3], hi[3];
   int32_t k[3], ok[3], pad2[2];
 };
-static_assert(sizeof(CondDesc) == 88 || sizeof(CondDesc) == 96, "cond descriptor layout");
 
 struct __align__(8) PairRec {        // graphs.PAIR_DTYPE
   int32_t bk[3], pad;
@@ -66,6 +69,8 @@ struct EngineArgs {
   int max_pairs;     // K3 scratch per warp
   char* scratch;     // global scratch base
   size_t scratch_per_warp;
+  int32_t* serial_list;   // [n_jobs] apps left to mc_serial_kernel
+  int32_t* serial_count;  // [1]
 };
 
 // distributions.py:107-118 with (lo, hi = last bucket edge, k)
@@ -90,38 +95,15 @@ struct Pools {            // the draw pools of one unit visit
   int pb;
 };
 
-// Per-warp stream state (warp-uniform).
+// Per-warp stream state (warp-uniform): base state after the consumed words,
+// plus the buffered high half of numpy's next_uint32.
 struct Stream {
   U128 s, inc;
   bool pend;
   uint32_t pv;
 };
 
-__device__ __forceinline__ uint32_t half_at(const uint64_t* jt, const Stream& g, uint32_t R) {
-  if (g.pend) {
-    if (R == 0) return g.pv;
-    R -= 1;
-  }
-  const uint64_t w = pcg_out(pcg_jump(jt, g.s, g.inc, (R >> 1) + 1));
-  return (R & 1) ? uint32_t(w >> 32) : uint32_t(w);
-}
-
-// C halves (positions 0..C-1) of the u32 stream were consumed.
-__device__ __forceinline__ void close_u32(const uint64_t* jt, Stream& g, uint32_t C) {
-  if (C == 0) return;
-  const uint32_t F = C - (g.pend ? 1u : 0u);
-  if (F & 1u) {
-    const uint64_t w = pcg_out(pcg_jump(jt, g.s, g.inc, ((F - 1) >> 1) + 1));
-    g.pv = uint32_t(w >> 32);
-    g.pend = true;
-  } else {
-    g.pend = false;
-  }
-  g.s = pcg_jump(jt, g.s, g.inc, (F + 1) >> 1);
-}
-
-// Reads fresh words of the stream forward from a base state: word q is the
-// output after q+1 steps.  Short gaps step, long gaps jump.
+// Reads words forward from a base state: word q is the output after q+1 steps.
 struct Cursor {
   U128 st;
   uint32_t q;      // index of the word held in w (0xffffffff: st is the base)
@@ -131,12 +113,9 @@ struct Cursor {
 __device__ __forceinline__ uint64_t cursor_word(Cursor& c, const uint64_t* jt, const U128& inc,
                                                 uint32_t q) {
   if (q != c.q) {
-    uint32_t d = q - c.q;
-    if (d <= 4) {
-      do { c.st = pcg_step(c.st, inc); } while (--d);
-    } else {
-      c.st = pcg_jump(jt, c.st, inc, d);
-    }
+    const uint32_t d = q - c.q;
+    if (d == 1) c.st = pcg_step(c.st, inc);
+    else c.st = pcg_jump(jt, c.st, inc, d);
     c.q = q;
     c.w = pcg_out(c.st);
   }
@@ -157,54 +136,130 @@ __device__ __forceinline__ uint32_t cursor_half(Cursor& c, const uint64_t* jt, c
 template <typename Idx>
 struct WarpState {
   double* tot;      // [n] accumulated remaining demand per walk
-  double* tmp;      // [n] stage time of this visit, per member rank
   Idx* act;         // [n] active walks, ascending
   Idx* mem;         // [n] members of the visited unit, ascending (= rank order)
-  Idx* osrt;        // [n] member ranks sorted by input bucket (own-input)
-  uint16_t* bkt;    // [n] input bucket per member rank (own-input)
   int8_t* cur;      // [n] current unit per walk (-1 = terminated)
   uint32_t* cnt;    // [counters]
+  double* tmp;      // [n] own-input path: input draw / stage time per rank (global)
+  uint16_t* bkt;    // [n] own-input path: input bucket per rank (global)
+  Idx* osrt;        // [n] own-input path: ranks sorted by bucket (global)
   double* kin;      // [max_pairs] K3 kept inputs
   double* kout;     // [max_pairs] K3 kept outputs
 };
 
 // ---------------------------------------------------------------------------
-// Sequential replay of one unit visit (lane 0) -- exact on Lemire rejections.
+// K3: conditioned draw pools for the current unit (estimator.py:155-233)
 // ---------------------------------------------------------------------------
-template <typename Idx>
-__device__ void serial_visit(const EngineArgs& a, const UnitDesc& d, const Pools& pl,
-                             bool own, uint32_t m, const WarpState<Idx>& ws, Stream& g) {
-  SeqGen sg{g.s, g.inc, g.pend, g.pv};
-  const bool llm = d.flags & F_LLM;
-  for (uint32_t k = 0; k < m; ++k) ws.tmp[k] = pl.A[sg.bounded(uint32_t(pl.pa))];
-  if (llm) {
-    if (!own) {
-      for (uint32_t k = 0; k < m; ++k)
-        ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], a.b.prefill_rate),
-                         __ddiv_rn(pl.B[sg.bounded(uint32_t(pl.pb))], a.b.decode_rate));
-    } else {
-      const int K = d.ib_k;
-      for (uint32_t k = 0; k < m; ++k)
-        ws.bkt[k] = uint16_t(bucket_of(ws.tmp[k], d.ib_lo, d.ib_hi, K));
-      for (int bb = 0; bb < K; ++bb) {
-        const int pln = a.b.pool_len[d.pool_off + bb];
-        const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
-        const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
-        for (uint32_t k = 0; k < m; ++k)
-          if (ws.bkt[k] == bb)
-            ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], a.b.prefill_rate),
-                             __ddiv_rn(pool[sg.bounded(P)], a.b.decode_rate));
-      }
+__device__ bool condition(const EngineArgs& a, int gbase, int cur_unit, int obs_up,
+                          const double* obs, double* kin_buf, double* kout_buf, Pools& ovp,
+                          bool& conditioned, int lane) {
+  const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + cur_unit];
+  if (obs_up < 0 || !(d.flags & F_ANYMASK)) return false;   // no override
+  const CondDesc* cd = reinterpret_cast<const CondDesc*>(a.b.conds) + d.cond_off;
+  int ci = -1;
+  for (int q = 0; q < d.cond_len; ++q)
+    if (cd[q].up_local == obs_up) ci = q;
+  ovp.A = a.b.vals + d.a_off;
+  ovp.pa = d.a_len;
+  ovp.B = a.b.vals + d.b_off;
+  ovp.pb = d.b_len;
+  conditioned = false;
+  if (ci < 0) return true;            // override exists, nothing joins: priors
+  const CondDesc& c = cd[ci];
+  int ob[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+    ob[t] = c.ok[t] ? bucket_of(obs[t], c.lo[t], c.hi[t], c.k[t]) : -2;
+  // which upstream variables condition which target (estimator.py:209-221)
+  const bool iui = d.flags & F_IUI, iuo = d.flags & F_IUO;
+  const bool ouo = d.flags & F_OUO, pup = d.flags & F_PUP;
+  const PairRec* pr = reinterpret_cast<const PairRec*>(a.b.pairs) + c.pair_off;
+  const unsigned lt = lanemask_lt();
+  uint32_t nin = 0, nout = 0, npar = 0;
+  const int plen = c.pair_len;
+  for (int base = 0; base < plen; base += 32) {
+    const int p = base + lane;
+    bool kn = false, ko = false, kp = false;
+    double rin = 0.0, rout = 0.0;
+    if (p < plen) {
+      const PairRec rec = pr[p];
+      rin = rec.in;
+      rout = rec.out;
+      // a condition on an empty upstream distribution never matches
+      kn = (iui || iuo) && (!iui || (ob[0] >= 0 && rec.bk[0] == ob[0])) &&
+           (!iuo || (ob[1] >= 0 && rec.bk[1] == ob[1]));
+      ko = ouo && ob[1] >= 0 && rec.bk[1] == ob[1];
+      kp = pup && ob[2] >= 0 && rec.bk[2] == ob[2];
     }
+    const unsigned bi = __ballot_sync(kFull, kn), bo = __ballot_sync(kFull, ko);
+    if (kn) kin_buf[nin + __popc(bi & lt)] = rin;
+    if (ko) kout_buf[nout + __popc(bo & lt)] = rout;
+    nin += __popc(bi);
+    nout += __popc(bo);
+    npar += __popc(__ballot_sync(kFull, kp));
   }
-  g.s = sg.s;
-  g.pend = sg.pend;
-  g.pv = sg.pv;
+  __syncwarp();
+  const int capu = a.b.unit_capacity ? a.b.unit_capacity[gbase + cur_unit] : 1000;
+  constexpr uint32_t kMin = 5;          // MIN_CONDITIONAL_SAMPLES (estimator.py:25)
+  if ((iui || iuo) && nin >= kMin) {    // FIFO cap keeps the last `capacity` kept values
+    const uint32_t keep = nin > uint32_t(capu) ? uint32_t(capu) : nin;
+    ovp.A = kin_buf + (nin - keep);
+    ovp.pa = int(keep);
+    conditioned = true;
+  }
+  if (ouo && nout >= kMin) {
+    const uint32_t keep = nout > uint32_t(capu) ? uint32_t(capu) : nout;
+    ovp.B = kout_buf + (nout - keep);
+    ovp.pb = int(keep);
+    conditioned = true;
+  }
+  if (pup && npar >= kMin) conditioned = true;
+  return true;
+}
+
+__device__ __forceinline__ Pools pools_for(const EngineArgs& a, const UnitDesc& d, bool ov,
+                                           const Pools& ovp) {
+  Pools pl;
+  if ((d.flags & F_LLM) && ov) {
+    pl = ovp;
+  } else {
+    pl.A = a.b.vals + d.a_off;
+    pl.pa = d.a_len;
+    pl.B = a.b.vals + d.b_off;
+    pl.pb = d.b_len;
+  }
+  return pl;
+}
+
+// successor index of a uniform draw: searchsorted(cum, u, side="right")
+__device__ __forceinline__ int next_unit(const EngineArgs& a, const UnitDesc& d, double uu) {
+  const double* cum = a.b.succ_cum + d.succ_off;
+  int idx = 0;
+  while (idx < d.succ_len && __ldg(cum + idx) <= uu) ++idx;
+  return __ldg(a.b.succ_nxt + d.succ_off + idx);
+}
+
+// close a bounded-draw group of C halves: the word holding the last fresh half
+// was read by some lane (the largest word index a cursor holds)
+__device__ __forceinline__ void close_group(Stream& g, uint32_t C, const Cursor& ca,
+                                            const Cursor& cb) {
+  if (C == 0) return;
+  const uint32_t F = C - (g.pend ? 1u : 0u);
+  if (F & 1u) {
+    const uint32_t qlast = (F - 1) >> 1;
+    const bool own_a = ca.q == qlast, own_b = cb.q == qlast;
+    const unsigned who = __ballot_sync(kFull, own_a || own_b);
+    const uint64_t wv = own_a ? ca.w : cb.w;
+    g.pv = uint32_t(__shfl_sync(kFull, wv, __ffs(who) - 1) >> 32);
+    g.pend = true;
+  } else {
+    g.pend = false;
+  }
 }
 
 // ---------------------------------------------------------------------------
-// one (step, unit) visit of the vectorised walk; returns true if the visit
-// was replayed serially (a Lemire rejection occurred)
+// one (step, unit) visit; returns false if a Lemire rejection was seen (the
+// application must then be recomputed by mc_serial_kernel)
 // ---------------------------------------------------------------------------
 template <typename Idx>
 __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& ovp,
@@ -214,17 +269,8 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
   const unsigned lt = lanemask_lt();
   const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u];
   const bool llm = d.flags & F_LLM;
-  const bool ov = has_ov && u == cur_unit;
-  Pools pl;
-  if (llm && ov) {
-    pl = ovp;
-  } else {
-    pl.A = a.b.vals + d.a_off;
-    pl.pa = d.a_len;
-    pl.B = a.b.vals + d.b_off;
-    pl.pb = d.b_len;
-  }
-  const bool own = llm && (d.flags & F_OWN) && !ov;
+  const Pools pl = pools_for(a, d, has_ov && u == cur_unit, ovp);
+  const bool own = llm && (d.flags & F_OWN) && !(has_ov && u == cur_unit);
   // members of this visit, in walk order: list position == rank
   uint32_t m = 0;
   for (uint32_t base = 0; base < na; base += 32) {
@@ -243,291 +289,253 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
   const uint32_t per = (m + 31) >> 5;
   const uint32_t k0 = min(lane * per, m), k1 = min(k0 + per, m);
   const uint32_t c1 = pl.pa > 1 ? m : 0u;
+  const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
   bool rej = false;
-  uint32_t C = 0;
-  Cursor cs{g.s, 0xffffffffu, 0};
+  Cursor ca{g.s, 0xffffffffu, 0}, cb{g.s, 0xffffffffu, 0};
+  uint32_t words;
   if (!own) {
-    for (uint32_t k = k0; k < k1; ++k) {
-      const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(cs, jt, g, k), uint32_t(pl.pa), rej) : 0u;
-      ws.tmp[k] = pl.A[ia];
-    }
-    if (llm) {
-      for (uint32_t k = k0; k < k1; ++k) {
-        const uint32_t ib =
-            pl.pb > 1 ? lemire(cursor_half(cs, jt, g, c1 + k), uint32_t(pl.pb), rej) : 0u;
-        ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], a.b.prefill_rate),
-                         __ddiv_rn(pl.B[ib], a.b.decode_rate));
-      }
-    }
-    C = c1 + ((llm && pl.pb > 1) ? m : 0u);
-  } else {
-    // own-input sampling: outputs drawn per input bucket, buckets ascending,
-    // walks in order within a bucket (estimator.py:275-283)
-    const int K = d.ib_k;
-    uint32_t* cnt = ws.cnt;
-    uint32_t* start = ws.cnt + a.max_unit_k;
-    uint32_t* effo = ws.cnt + 2 * a.max_unit_k;
-    for (int b = lane; b < K; b += 32) cnt[b] = 0;
-    __syncwarp();
-    for (uint32_t k = k0; k < k1; ++k) {
-      const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(cs, jt, g, k), uint32_t(pl.pa), rej) : 0u;
-      const double iv = pl.A[ia];
-      ws.tmp[k] = iv;
-      const int bb = bucket_of(iv, d.ib_lo, d.ib_hi, K);
-      ws.bkt[k] = uint16_t(bb);
-      atomicAdd(&cnt[bb], 1u);
-    }
-    __syncwarp();
-    const int perb = (K + 31) >> 5;
-    uint32_t la = 0, le = 0;
-    for (int q = 0; q < perb; ++q) {
-      const int bb = lane * perb + q;
-      if (bb < K) {
-        const int pln = a.b.pool_len[d.pool_off + bb];
-        const int P = pln > 0 ? pln : pl.pb;
-        la += cnt[bb];
-        le += P > 1 ? cnt[bb] : 0u;
-      }
-    }
-    const uint32_t ia_incl = warp_incl_scan(la, lane), ie_incl = warp_incl_scan(le, lane);
-    const uint32_t eff_total = __shfl_sync(kFull, ie_incl, 31);
-    uint32_t ra = ia_incl - la, re = ie_incl - le;
-    __syncwarp();
-    for (int q = 0; q < perb; ++q) {
-      const int bb = lane * perb + q;
-      if (bb < K) {
-        const int pln = a.b.pool_len[d.pool_off + bb];
-        const int P = pln > 0 ? pln : pl.pb;
-        const uint32_t c = cnt[bb];
-        start[bb] = ra;
-        effo[bb] = re;
-        cnt[bb] = ra;                        // cursor of the counting sort
-        ra += c;
-        re += P > 1 ? c : 0u;
-      }
-    }
-    __syncwarp();
-    // stable counting sort of member ranks by bucket (rank order = round order)
-    for (uint32_t base = 0; base < m; base += 32) {
-      const uint32_t k = base + lane;
-      const bool valid = k < m;
-      const int bb = valid ? int(ws.bkt[k]) : (0x10000 + lane);
-      const unsigned peers = __match_any_sync(kFull, bb);
-      uint32_t dest = 0;
-      if (valid) dest = cnt[bb];
-      __syncwarp();
-      if (valid && (__ffs(peers) - 1) == lane) cnt[bb] = dest + __popc(peers);
-      __syncwarp();
-      if (valid) ws.osrt[dest + __popc(peers & lt)] = Idx(k);
-    }
-    __syncwarp();
-    for (uint32_t j = k0; j < k1; ++j) {
-      const uint32_t k = ws.osrt[j];
-      const int bb = ws.bkt[k];
-      const int pln = a.b.pool_len[d.pool_off + bb];
-      const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
-      const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
-      const uint32_t pos = c1 + effo[bb] + (j - start[bb]);
-      const uint32_t ob = P > 1 ? lemire(cursor_half(cs, jt, g, pos), P, rej) : 0u;
-      ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], a.b.prefill_rate),
-                       __ddiv_rn(pool[ob], a.b.decode_rate));
-    }
-    C = c1 + eff_total;
-  }
-  const bool replay = __any_sync(kFull, rej);
-  __syncwarp();
-  uint32_t words;        // fresh words consumed by the bounded draws
-  if (replay) {
-    if (lane == 0) serial_visit(a, d, pl, own, m, ws, g);
-    __syncwarp();
-    g.s.lo = __shfl_sync(kFull, g.s.lo, 0);
-    g.s.hi = __shfl_sync(kFull, g.s.hi, 0);
-    g.pend = __shfl_sync(kFull, int(g.pend), 0);
-    g.pv = __shfl_sync(kFull, g.pv, 0);
-    words = 0;
-    cs = Cursor{g.s, 0xffffffffu, 0};
-  } else {
-    // close the bounded-draw group without re-deriving anything: the word
-    // holding the last fresh half was read by some lane (largest word index)
+    const uint32_t C = c1 + ((llm && pl.pb > 1) ? m : 0u);
     const uint32_t F = C == 0 ? 0u : C - (g.pend ? 1u : 0u);
     words = (F + 1) >> 1;
-    if (C != 0) {
-      if (F & 1u) {
-        const uint32_t qlast = (F - 1) >> 1;
-        const unsigned owner = __ballot_sync(kFull, cs.q == qlast);
-        g.pv = uint32_t(__shfl_sync(kFull, cs.w, __ffs(owner) - 1) >> 32);
-        g.pend = true;
-      } else {
-        g.pend = false;
+    Cursor cd{g.s, 0xffffffffu, 0};
+    for (uint32_t k = k0; k < k1; ++k) {
+      const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(ca, jt, g, k), uint32_t(pl.pa), rej) : 0u;
+      double t = pl.A[ia];
+      if (llm) {
+        const uint32_t ib =
+            pl.pb > 1 ? lemire(cursor_half(cb, jt, g, c1 + k), uint32_t(pl.pb), rej) : 0u;
+        t = dadd(__ddiv_rn(t, pre), __ddiv_rn(pl.B[ib], dec));
       }
+      // random(m) word of member k, then the successor jump (estimator.py:350-353)
+      const double uu = u53_double(cursor_word(cd, jt, g.inc, words + k));
+      const Idx w = ws.mem[k];
+      ws.cur[w] = int8_t(next_unit(a, d, uu));
+      ws.tot[w] = dadd(ws.tot[w], t);
     }
+    if (__any_sync(kFull, rej)) return false;
+    close_group(g, C, ca, cb);
+    const unsigned last_lane = (m - 1) / per;   // it drew the last uniform
+    g.s.lo = __shfl_sync(kFull, cd.st.lo, last_lane);
+    g.s.hi = __shfl_sync(kFull, cd.st.hi, last_lane);
+    __syncwarp();
+    return true;
   }
-  // random(m) + successor jump (estimator.py:350-353); word (words + k) of the
-  // same base serves member k
-  const int ns = d.succ_len;
-  double c0 = 2.0, c1s = 2.0, c2 = 2.0;     // first successors cached (cum <= 1)
-  int n0 = -1, n1 = -1, n2 = -1, n3 = -1;
-  {
-    const double* cum = a.b.succ_cum + d.succ_off;
-    const int32_t* nxt = a.b.succ_nxt + d.succ_off;
-    if (ns > 0) c0 = __ldg(cum);
-    if (ns > 1) c1s = __ldg(cum + 1);
-    if (ns > 2) c2 = __ldg(cum + 2);
-    n0 = __ldg(nxt);
-    if (ns > 0) n1 = __ldg(nxt + 1);
-    if (ns > 1) n2 = __ldg(nxt + 2);
-    if (ns > 2) n3 = __ldg(nxt + 3);
-  }
+  // ---- own-input sampling: outputs drawn per input bucket, buckets
+  // ascending, walks in order within a bucket (estimator.py:275-283)
+  const int K = d.ib_k;
+  uint32_t* cnt = ws.cnt;
+  uint32_t* start = ws.cnt + a.max_unit_k;
+  uint32_t* effo = ws.cnt + 2 * a.max_unit_k;
+  for (int b = lane; b < K; b += 32) cnt[b] = 0;
+  __syncwarp();
   for (uint32_t k = k0; k < k1; ++k) {
-    const double uu = u53_double(cursor_word(cs, jt, g.inc, words + k));
-    int nx;
-    if (ns <= 3) {                                     // searchsorted(side="right")
-      nx = !(c0 <= uu) ? n0 : !(c1s <= uu) ? n1 : !(c2 <= uu) ? n2 : n3;
-    } else {
-      const double* cum = a.b.succ_cum + d.succ_off;
-      int idx = 0;
-      while (idx < ns && __ldg(cum + idx) <= uu) ++idx;
-      nx = __ldg(a.b.succ_nxt + d.succ_off + idx);
+    const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(ca, jt, g, k), uint32_t(pl.pa), rej) : 0u;
+    const double iv = pl.A[ia];
+    ws.tmp[k] = iv;
+    const int bb = bucket_of(iv, d.ib_lo, d.ib_hi, K);
+    ws.bkt[k] = uint16_t(bb);
+    atomicAdd(&cnt[bb], 1u);
+  }
+  __syncwarp();
+  const int perb = (K + 31) >> 5;
+  uint32_t la = 0, le = 0;
+  for (int q = 0; q < perb; ++q) {
+    const int bb = lane * perb + q;
+    if (bb < K) {
+      const int pln = a.b.pool_len[d.pool_off + bb];
+      const int P = pln > 0 ? pln : pl.pb;
+      la += cnt[bb];
+      le += P > 1 ? cnt[bb] : 0u;
     }
+  }
+  const uint32_t ia_incl = warp_incl_scan(la, lane), ie_incl = warp_incl_scan(le, lane);
+  const uint32_t eff_total = __shfl_sync(kFull, ie_incl, 31);
+  uint32_t ra = ia_incl - la, re = ie_incl - le;
+  __syncwarp();
+  for (int q = 0; q < perb; ++q) {
+    const int bb = lane * perb + q;
+    if (bb < K) {
+      const int pln = a.b.pool_len[d.pool_off + bb];
+      const int P = pln > 0 ? pln : pl.pb;
+      const uint32_t c = cnt[bb];
+      start[bb] = ra;
+      effo[bb] = re;
+      cnt[bb] = ra;                        // cursor of the counting sort
+      ra += c;
+      re += P > 1 ? c : 0u;
+    }
+  }
+  __syncwarp();
+  // stable counting sort of member ranks by bucket (rank order = round order)
+  for (uint32_t base = 0; base < m; base += 32) {
+    const uint32_t k = base + lane;
+    const bool valid = k < m;
+    const int bb = valid ? int(ws.bkt[k]) : (0x10000 + lane);
+    const unsigned peers = __match_any_sync(kFull, bb);
+    uint32_t dest = 0;
+    if (valid) dest = cnt[bb];
+    __syncwarp();
+    if (valid && (__ffs(peers) - 1) == lane) cnt[bb] = dest + __popc(peers);
+    __syncwarp();
+    if (valid) ws.osrt[dest + __popc(peers & lt)] = Idx(k);
+  }
+  __syncwarp();
+  for (uint32_t j = k0; j < k1; ++j) {
+    const uint32_t k = ws.osrt[j];
+    const int bb = ws.bkt[k];
+    const int pln = a.b.pool_len[d.pool_off + bb];
+    const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
+    const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
+    const uint32_t pos = c1 + effo[bb] + (j - start[bb]);
+    const uint32_t ob = P > 1 ? lemire(cursor_half(cb, jt, g, pos), P, rej) : 0u;
+    ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], pre), __ddiv_rn(pool[ob], dec));
+  }
+  if (__any_sync(kFull, rej)) return false;
+  const uint32_t C = c1 + eff_total;
+  const uint32_t F = C == 0 ? 0u : C - (g.pend ? 1u : 0u);
+  words = (F + 1) >> 1;
+  close_group(g, C, ca, cb);
+  __syncwarp();
+  Cursor cd{g.s, 0xffffffffu, 0};
+  for (uint32_t k = k0; k < k1; ++k) {
+    const double uu = u53_double(cursor_word(cd, jt, g.inc, words + k));
     const Idx w = ws.mem[k];
-    ws.cur[w] = int8_t(nx);
+    ws.cur[w] = int8_t(next_unit(a, d, uu));
     ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
   }
-  // the lane that drew the last double holds the advanced base state
   const unsigned last_lane = (m - 1) / per;
-  g.s.lo = __shfl_sync(kFull, cs.st.lo, last_lane);
-  g.s.hi = __shfl_sync(kFull, cs.st.hi, last_lane);
+  g.s.lo = __shfl_sync(kFull, cd.st.lo, last_lane);
+  g.s.hi = __shfl_sync(kFull, cd.st.hi, last_lane);
   __syncwarp();
-  return replay;
-}
-
-// ---------------------------------------------------------------------------
-// K3: conditioned draw pools for the current unit (estimator.py:155-233)
-// ---------------------------------------------------------------------------
-template <typename Idx>
-__device__ bool condition(const EngineArgs& a, int gbase, int cur_unit, int obs_up,
-                          const double* obs, const WarpState<Idx>& ws, Pools& ovp,
-                          bool& conditioned, int lane) {
-  const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + cur_unit];
-  if (obs_up < 0 || !(d.flags & F_ANYMASK)) return false;   // no override
-  const CondDesc* cd = reinterpret_cast<const CondDesc*>(a.b.conds) + d.cond_off;
-  int ci = -1;
-  for (int q = 0; q < d.cond_len; ++q)
-    if (cd[q].up_local == obs_up) ci = q;
-  ovp.A = a.b.vals + d.a_off;
-  ovp.pa = d.a_len;
-  ovp.B = a.b.vals + d.b_off;
-  ovp.pb = d.b_len;
-  conditioned = false;
-  if (ci < 0) return true;            // override exists, nothing joins: priors
-  const CondDesc c = cd[ci];
-  int ob[3];
-  for (int t = 0; t < 3; ++t)
-    ob[t] = c.ok[t] ? bucket_of(obs[t], c.lo[t], c.hi[t], c.k[t]) : -2;
-  // which upstream variables condition which target (estimator.py:209-221)
-  const bool iui = d.flags & F_IUI, iuo = d.flags & F_IUO;
-  const bool ouo = d.flags & F_OUO, pup = d.flags & F_PUP;
-  const PairRec* pr = reinterpret_cast<const PairRec*>(a.b.pairs) + c.pair_off;
-  const unsigned lt = lanemask_lt();
-  uint32_t nin = 0, nout = 0, npar = 0;
-  for (int base = 0; base < c.pair_len; base += 32) {
-    const int p = base + lane;
-    bool kin = false, kout = false, kpar = false;
-    PairRec rec;
-    if (p < c.pair_len) {
-      rec = pr[p];
-      // a condition on an empty upstream distribution never matches
-      kin = (iui || iuo) && (!iui || (ob[0] >= 0 && rec.bk[0] == ob[0])) &&
-            (!iuo || (ob[1] >= 0 && rec.bk[1] == ob[1]));
-      kout = ouo && ob[1] >= 0 && rec.bk[1] == ob[1];
-      kpar = pup && ob[2] >= 0 && rec.bk[2] == ob[2];
-    }
-    const unsigned bi = __ballot_sync(kFull, kin), bo = __ballot_sync(kFull, kout);
-    if (kin) ws.kin[nin + __popc(bi & lt)] = rec.in;
-    if (kout) ws.kout[nout + __popc(bo & lt)] = rec.out;
-    nin += __popc(bi);
-    nout += __popc(bo);
-    npar += __popc(__ballot_sync(kFull, kpar));
-  }
-  __syncwarp();
-  const int capu = a.b.unit_capacity ? a.b.unit_capacity[gbase + cur_unit] : 1000;
-  constexpr uint32_t kMin = 5;          // MIN_CONDITIONAL_SAMPLES (estimator.py:25)
-  if ((iui || iuo) && nin >= kMin) {    // FIFO cap keeps the last `capacity` kept values
-    const uint32_t keep = nin > uint32_t(capu) ? uint32_t(capu) : nin;
-    ovp.A = ws.kin + (nin - keep);
-    ovp.pa = int(keep);
-    conditioned = true;
-  }
-  if (ouo && nout >= kMin) {
-    const uint32_t keep = nout > uint32_t(capu) ? uint32_t(capu) : nout;
-    ovp.B = ws.kout + (nout - keep);
-    ovp.pb = int(keep);
-    conditioned = true;
-  }
-  if (pup && npar >= kMin) conditioned = true;
   return true;
 }
 
 // ---------------------------------------------------------------------------
-// per-warp walk-state footprint (bytes per walk slot) for index type Idx
+// shared epilogue: samples out, capped count, bucketing (distributions.py:79-105)
+// ---------------------------------------------------------------------------
+__device__ void write_result(const EngineArgs& a, int64_t job, const double* tot,
+                             const int8_t* cur, uint32_t* cnt, bool conditioned, bool has_ov,
+                             bool replayed, int lane) {
+  const int n = a.n;
+  int capped = 0;
+  double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+  for (int w = lane; w < n; w += 32) {
+    capped += cur[w] >= 0;
+    const double sv = tot[w];
+    lo = fmin(lo, sv);
+    hi = fmax(hi, sv);
+    if (a.o.samples) a.o.samples[job * a.o.samples_stride + w] = sv;
+  }
+  capped = warp_sum(capped);
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
+  }
+  const int64_t row = a.o.slot ? a.o.slot[job] : job;
+  int k = a.k_out;
+  double width = 0.0;
+  if (lo == hi) k = 1;
+  else width = __ddiv_rn(dsub(hi, lo), small_int_to_double(k));
+  for (int b = lane; b < k; b += 32) cnt[b] = 0;
+  __syncwarp();
+  for (int w = lane; w < n; w += 32) {
+    int idx = 0;
+    if (k > 1) {
+      idx = __double2int_rz(__ddiv_rn(dsub(tot[w], lo), width));
+      idx = idx < k - 1 ? idx : k - 1;
+    }
+    atomicAdd(&cnt[idx], 1u);
+  }
+  __syncwarp();
+  if (a.o.counts) {
+    uint16_t* crow = a.o.counts + row * a.o.stride;
+    for (int b = lane; b < a.o.stride; b += 32) crow[b] = b < k ? uint16_t(cnt[b]) : 0;
+  }
+  if (lane == 0) {
+    if (a.o.lo) a.o.lo[row] = lo;
+    if (a.o.width) a.o.width[row] = width;
+    if (a.o.nbins) a.o.nbins[row] = k;
+    if (a.o.nsamp) a.o.nsamp[row] = n;
+    if (a.o.capped) a.o.capped[job] = capped;
+    if (a.o.flags)
+      a.o.flags[job] = (conditioned ? 1 : 0) | (has_ov ? 2 : 0) | (replayed ? 4 : 0);
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// per-warp footprints
+// ---------------------------------------------------------------------------
 template <typename Idx>
-__host__ __device__ constexpr size_t walk_bytes() { return 16 + 3 * sizeof(Idx) + 2 + 1; }
+__host__ __device__ constexpr size_t smem_walk_bytes() { return 8 + 2 * sizeof(Idx) + 1; }
+template <typename Idx>
+__host__ __device__ constexpr size_t gmem_walk_bytes() {   // own-input arrays
+  return 8 + 2 + sizeof(Idx);
+}
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 template <typename Idx>
-__device__ WarpState<Idx> carve(unsigned char* base, int nw, uint32_t* cnt, double* k3,
-                                int max_pairs) {
+__device__ WarpState<Idx> carve(unsigned char* walk_base, unsigned char* gbase, int nw,
+                                uint32_t* cnt, int max_pairs) {
   WarpState<Idx> ws;
-  ws.tot = reinterpret_cast<double*>(base);
-  ws.tmp = ws.tot + nw;
-  ws.act = reinterpret_cast<Idx*>(ws.tmp + nw);
+  ws.tot = reinterpret_cast<double*>(walk_base);
+  ws.act = reinterpret_cast<Idx*>(ws.tot + nw);
   ws.mem = ws.act + nw;
-  ws.osrt = ws.mem + nw;
-  ws.bkt = reinterpret_cast<uint16_t*>(ws.osrt + nw);
-  ws.cur = reinterpret_cast<int8_t*>(ws.bkt + nw);
+  ws.cur = reinterpret_cast<int8_t*>(ws.mem + nw);
   ws.cnt = cnt;
-  ws.kin = k3;
-  ws.kout = k3 + max_pairs;
+  ws.tmp = reinterpret_cast<double*>(gbase);
+  ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + nw);
+  ws.osrt = reinterpret_cast<Idx*>(ws.bkt + nw);
+  ws.kin = reinterpret_cast<double*>(gbase + align16(size_t(nw) * gmem_walk_bytes<Idx>()));
+  ws.kout = ws.kin + max_pairs;
   return ws;
 }
 
+__device__ __forceinline__ void job_obs(const EngineArgs& a, int64_t job, int& obs_up,
+                                        double (&obs)[3]) {
+  obs_up = a.j.obs_unit ? a.j.obs_unit[job] : -1;
+  obs[0] = obs[1] = obs[2] = 0.0;
+  if (obs_up >= 0) {
+    obs[0] = a.j.obs_val[3 * job];
+    obs[1] = a.j.obs_val[3 * job + 1];
+    obs[2] = a.j.obs_val[3 * job + 2];
+  }
+}
+
 template <typename Idx>
-__global__ void __launch_bounds__(kWarps * 32, 4) mc_engine_kernel(EngineArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 5) mc_engine_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;
   const bool in_smem = n <= kSmemWalks;
   const int nw = in_smem ? kSmemWalks : ((n + 15) & ~15);
-  const size_t cnt_bytes = (size_t(a.counters) * 4 + 15) & ~size_t(15);
-  const size_t per_warp_smem = cnt_bytes + (in_smem ? size_t(kSmemWalks) * walk_bytes<Idx>() : 0);
+  const size_t cnt_bytes = align16(size_t(a.counters) * 4);
+  const size_t per_warp_smem =
+      cnt_bytes + (in_smem ? size_t(kSmemWalks) * smem_walk_bytes<Idx>() : 0);
   unsigned char* sb = smem + per_warp_smem * wib;
   const int64_t gwarp = int64_t(blockIdx.x) * kWarps + wib;
-  unsigned char* gs = reinterpret_cast<unsigned char*>(a.scratch) + size_t(gwarp) * a.scratch_per_warp;
-  unsigned char* walk_base = in_smem ? sb + cnt_bytes : gs;
-  double* k3 = reinterpret_cast<double*>(gs + (in_smem ? 0 : size_t(nw) * walk_bytes<Idx>()));
-  const WarpState<Idx> ws =
-      carve<Idx>(walk_base, nw, reinterpret_cast<uint32_t*>(sb), k3, a.max_pairs);
-
+  unsigned char* gs =
+      reinterpret_cast<unsigned char*>(a.scratch) + size_t(gwarp) * a.scratch_per_warp;
+  unsigned char* gown = gs + (in_smem ? 0 : align16(size_t(nw) * smem_walk_bytes<Idx>()));
+  const WarpState<Idx> ws = carve<Idx>(in_smem ? sb + cnt_bytes : gs, gown, nw,
+                                       reinterpret_cast<uint32_t*>(sb), a.max_pairs);
+  const unsigned lt = lanemask_lt();
   const int64_t stride = int64_t(gridDim.x) * kWarps;
   for (int64_t job = gwarp; job < a.n_jobs; job += stride) {
-    const int gi = a.j.graph[job];
-    const int gbase = a.b.graph_base[gi];
+    const int gbase = a.b.graph_base[a.j.graph[job]];
     const int u0 = a.j.unit[job];
     Stream g;
     pcg_seed(a.j.seed[job], g.s, g.inc);
     g.pend = false;
     g.pv = 0;
-    // K3 conditioning of the current unit
     Pools ovp{nullptr, 0, nullptr, 0};
     bool conditioned = false;
-    const int obs_up = a.j.obs_unit ? a.j.obs_unit[job] : -1;
-    double obs[3] = {0.0, 0.0, 0.0};
-    if (obs_up >= 0) {
-      obs[0] = a.j.obs_val[3 * job];
-      obs[1] = a.j.obs_val[3 * job + 1];
-      obs[2] = a.j.obs_val[3 * job + 2];
-    }
-    const bool has_ov = condition<Idx>(a, gbase, u0, obs_up, obs, ws, ovp, conditioned, lane);
-
+    int obs_up;
+    double obs[3];
+    job_obs(a, job, obs_up, obs);
+    const bool has_ov =
+        condition(a, gbase, u0, obs_up, obs, ws.kin, ws.kout, ovp, conditioned, lane);
     for (int w = lane; w < n; w += 32) {
       ws.cur[w] = int8_t(u0);
       ws.tot[w] = 0.0;
@@ -535,9 +543,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) mc_engine_kernel(EngineArgs a)
     }
     __syncwarp();
     uint32_t na = uint32_t(n);
-    bool replayed = false;
-    const unsigned lt = lanemask_lt();
-    for (int step = 0; step < a.cap; ++step) {
+    bool ok = true;
+    for (int step = 0; step < a.cap && ok; ++step) {
       // compact the still-active walks (order kept) and collect occupied units
       unsigned occ = 0;
       uint32_t nn = 0;
@@ -560,60 +567,104 @@ __global__ void __launch_bounds__(kWarps * 32, 4) mc_engine_kernel(EngineArgs a)
       occ = __reduce_or_sync(kFull, occ);
       __syncwarp();
       if (!occ) break;
-      while (occ) {
+      while (occ && ok) {
         const int u = __ffs(occ) - 1;
         occ &= occ - 1;
-        replayed |= visit_unit<Idx>(a, gbase, u, ovp, has_ov, u0, ws, na, g, lane);
+        ok = visit_unit<Idx>(a, gbase, u, ovp, has_ov, u0, ws, na, g, lane);
       }
     }
-    // capped walks, samples, bucketing (distributions.py:79-105)
-    int capped = 0;
-    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
-    for (int w = lane; w < n; w += 32) {
-      capped += ws.cur[w] >= 0;
-      const double sv = ws.tot[w];
-      lo = fmin(lo, sv);
-      hi = fmax(hi, sv);
-      if (a.o.samples) a.o.samples[job * a.o.samples_stride + w] = sv;
+    if (!ok) {                     // Lemire rejection: leave it to mc_serial_kernel
+      if (lane == 0) a.serial_list[atomicAdd(a.serial_count, 1)] = int32_t(job);
+      __syncwarp();
+      continue;
     }
-    capped = warp_sum(capped);
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
-      hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
-    }
-    const int64_t row = a.o.slot ? a.o.slot[job] : job;
-    int k = a.k_out;
-    double width = 0.0;
-    if (lo == hi) {
-      k = 1;
-    } else {
-      width = __ddiv_rn(dsub(hi, lo), small_int_to_double(k));
-    }
-    for (int b = lane; b < k; b += 32) ws.cnt[b] = 0;
-    __syncwarp();
-    for (int w = lane; w < n; w += 32) {
-      int idx = 0;
-      if (k > 1) {
-        idx = __double2int_rz(__ddiv_rn(dsub(ws.tot[w], lo), width));
-        idx = idx < k - 1 ? idx : k - 1;
-      }
-      atomicAdd(&ws.cnt[idx], 1u);
-    }
-    __syncwarp();
-    if (a.o.counts) {
-      uint16_t* crow = a.o.counts + row * a.o.stride;
-      for (int b = lane; b < a.o.stride; b += 32) crow[b] = b < k ? uint16_t(ws.cnt[b]) : 0;
-    }
+    write_result(a, job, ws.tot, ws.cur, ws.cnt, conditioned, has_ov, false, lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sequential reference walk for the apps the fast kernel gave up on (lane 0
+// computes, the warp helps with conditioning and the epilogue).  Walk state
+// lives in global scratch; numpy's generator is stepped one word at a time.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline size_t serial_bytes(int nw) { return align16(size_t(nw) * 19); }
+
+__global__ void __launch_bounds__(32) mc_serial_kernel(EngineArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int n = a.n;
+  const int nw = (n + 15) & ~15;
+  unsigned char* gs =
+      reinterpret_cast<unsigned char*>(a.scratch) + size_t(blockIdx.x) * a.scratch_per_warp;
+  double* tot = reinterpret_cast<double*>(gs);
+  double* tmp = tot + nw;
+  uint16_t* bkt = reinterpret_cast<uint16_t*>(tmp + nw);
+  int8_t* cur = reinterpret_cast<int8_t*>(bkt + nw);
+  double* kin = reinterpret_cast<double*>(gs + serial_bytes(nw));
+  double* kout = kin + a.max_pairs;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
+  const int total = *a.serial_count;
+  for (int li = blockIdx.x; li < total; li += gridDim.x) {
+    const int64_t job = a.serial_list[li];
+    const int gbase = a.b.graph_base[a.j.graph[job]];
+    const int u0 = a.j.unit[job];
+    Pools ovp{nullptr, 0, nullptr, 0};
+    bool conditioned = false;
+    int obs_up;
+    double obs[3];
+    job_obs(a, job, obs_up, obs);
+    const bool has_ov = condition(a, gbase, u0, obs_up, obs, kin, kout, ovp, conditioned, lane);
     if (lane == 0) {
-      if (a.o.lo) a.o.lo[row] = lo;
-      if (a.o.width) a.o.width[row] = width;
-      if (a.o.nbins) a.o.nbins[row] = k;
-      if (a.o.nsamp) a.o.nsamp[row] = n;
-      if (a.o.capped) a.o.capped[job] = capped;
-      if (a.o.flags)
-        a.o.flags[job] = (conditioned ? 1 : 0) | (has_ov ? 2 : 0) | (replayed ? 4 : 0);
+      SeqGen sg;
+      pcg_seed(a.j.seed[job], sg.s, sg.inc);
+      sg.pend = false;
+      sg.pv = 0;
+      for (int w = 0; w < n; ++w) { cur[w] = int8_t(u0); tot[w] = 0.0; }
+      const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
+      for (int step = 0; step < a.cap; ++step) {
+        unsigned occ = 0;
+        for (int w = 0; w < n; ++w)
+          if (cur[w] >= 0) occ |= 1u << cur[w];
+        if (!occ) break;
+        while (occ) {
+          const int u = __ffs(occ) - 1;
+          occ &= occ - 1;
+          const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u];
+          const bool ov = has_ov && u == u0;
+          const Pools pl = pools_for(a, d, ov, ovp);
+          const bool llm = d.flags & F_LLM;
+          const bool own = llm && (d.flags & F_OWN) && !ov;
+          for (int w = 0; w < n; ++w)
+            if (cur[w] == u) tmp[w] = pl.A[sg.bounded(uint32_t(pl.pa))];
+          if (llm && !own) {
+            for (int w = 0; w < n; ++w)
+              if (cur[w] == u)
+                tmp[w] = dadd(__ddiv_rn(tmp[w], pre),
+                              __ddiv_rn(pl.B[sg.bounded(uint32_t(pl.pb))], dec));
+          } else if (own) {
+            const int K = d.ib_k;
+            for (int w = 0; w < n; ++w)
+              if (cur[w] == u) bkt[w] = uint16_t(bucket_of(tmp[w], d.ib_lo, d.ib_hi, K));
+            for (int bb = 0; bb < K; ++bb) {
+              const int pln = a.b.pool_len[d.pool_off + bb];
+              const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
+              const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
+              for (int w = 0; w < n; ++w)
+                if (cur[w] == u && bkt[w] == bb)
+                  tmp[w] = dadd(__ddiv_rn(tmp[w], pre), __ddiv_rn(pool[sg.bounded(P)], dec));
+            }
+          }
+          for (int w = 0; w < n; ++w) {
+            if (cur[w] != u) continue;
+            const double uu = u53_double(sg.next64());
+            tot[w] = dadd(tot[w], tmp[w]);
+            cur[w] = int8_t(next_unit(a, d, uu));
+          }
+        }
+      }
     }
     __syncwarp();
+    write_result(a, job, tot, cur, cnt, conditioned, has_ov, true, lane);
   }
 }
 
@@ -624,17 +675,23 @@ using namespace pdg;
 static bool small_idx(int n) { return n <= 65535; }
 
 static size_t walk_scratch(int n) {
-  if (n <= kSmemWalks) return 0;
   const size_t nw = size_t((n + 15) & ~15);
-  return nw * (small_idx(n) ? walk_bytes<uint16_t>() : walk_bytes<uint32_t>());
+  const bool si = small_idx(n);
+  const size_t smem_part = n <= kSmemWalks ? 0
+      : align16(nw * (si ? smem_walk_bytes<uint16_t>() : smem_walk_bytes<uint32_t>()));
+  const size_t own = align16(nw * (si ? gmem_walk_bytes<uint16_t>() : gmem_walk_bytes<uint32_t>()));
+  const size_t fast = smem_part + own;
+  const size_t serial = serial_bytes(int(nw));
+  return fast > serial ? fast : serial;
 }
 
 static size_t scratch_per_warp(int n, int max_pairs) {
-  return (walk_scratch(n) + size_t(max_pairs) * 16 + 64 + 255) & ~size_t(255);
+  return (walk_scratch(n) + align16(size_t(max_pairs) * 16) + 64 + 255) & ~size_t(255);
 }
 
+// scratch = per-warp regions + 256 B (serial counter) + one int per job
 extern "C" size_t pdg_mc_scratch_bytes(int32_t n_samples, int32_t max_pairs, int32_t grid_warps) {
-  return scratch_per_warp(n_samples, max_pairs) * size_t(grid_warps);
+  return scratch_per_warp(n_samples, max_pairs) * size_t(grid_warps) + 256;
 }
 
 extern "C" int pdg_mc_grid_warps(void) { return sm_count() * 8 * kWarps; }
@@ -644,9 +701,9 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
                                        int32_t bucket_count, int32_t max_unit_k,
                                        int32_t max_pairs, const pdg_mc_out* out,
                                        void* scratch, size_t scratch_bytes, void* stream) {
-  if (!bank || !jobs || !out || n_jobs < 0 || n_samples < 1 || n_samples > (1 << 19) ||
-      visit_cap < 0 || bucket_count < 1 || bucket_count > 1024 || max_unit_k < 0 ||
-      max_unit_k > 1024 || max_pairs < 0) {
+  if (!bank || !jobs || !out || n_jobs < 0 || n_jobs > INT32_MAX || n_samples < 1 ||
+      n_samples > (1 << 19) || visit_cap < 0 || bucket_count < 1 || bucket_count > 1024 ||
+      max_unit_k < 0 || max_unit_k > 1024 || max_pairs < 0) {
     set_error("pdg_mc_remaining_demand: invalid arguments");
     return PDG_EINVAL;
   }
@@ -656,8 +713,9 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   }
   if (n_jobs == 0) return PDG_OK;
   const int grid_warps = pdg_mc_grid_warps();
-  const size_t need = pdg_mc_scratch_bytes(n_samples, max_pairs, grid_warps);
-  if (scratch_bytes < need || (need > 0 && !scratch)) {
+  const size_t need = pdg_mc_scratch_bytes(n_samples, max_pairs, grid_warps) +
+                      size_t(n_jobs) * sizeof(int32_t);
+  if (scratch_bytes < need || !scratch) {
     set_error("pdg_mc_remaining_demand: scratch %zu < %zu bytes", scratch_bytes, need);
     return PDG_EINVAL;
   }
@@ -675,24 +733,36 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   a.max_pairs = max_pairs;
   a.scratch = static_cast<char*>(scratch);
   a.scratch_per_warp = scratch_per_warp(n_samples, max_pairs);
+  char* tail = static_cast<char*>(scratch) + a.scratch_per_warp * size_t(grid_warps);
+  a.serial_count = reinterpret_cast<int32_t*>(tail);
+  a.serial_list = reinterpret_cast<int32_t*>(tail + 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(a.serial_count, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(serial_count)");
   const bool sm = n_samples <= kSmemWalks;
-  const size_t cnt_bytes = (size_t(a.counters) * 4 + 15) & ~size_t(15);
+  const size_t cnt_bytes = align16(size_t(a.counters) * 4);
   int64_t blocks = (n_jobs + kWarps - 1) / kWarps;
   const int64_t capb = grid_warps / kWarps;
   if (blocks > capb) blocks = capb;
-  cudaStream_t st = (cudaStream_t)stream;
   if (small_idx(n_samples)) {
-    const size_t smem = size_t(kWarps) * (cnt_bytes + (sm ? size_t(kSmemWalks) * walk_bytes<uint16_t>() : 0));
-    cudaError_t e = cudaFuncSetAttribute(mc_engine_kernel<uint16_t>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const size_t smem =
+        size_t(kWarps) * (cnt_bytes + (sm ? size_t(kSmemWalks) * smem_walk_bytes<uint16_t>() : 0));
+    e = cudaFuncSetAttribute(mc_engine_kernel<uint16_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(mc_engine_kernel)");
     mc_engine_kernel<uint16_t><<<unsigned(blocks), kWarps * 32, smem, st>>>(a);
   } else {
     const size_t smem = size_t(kWarps) * cnt_bytes;
-    cudaError_t e = cudaFuncSetAttribute(mc_engine_kernel<uint32_t>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    e = cudaFuncSetAttribute(mc_engine_kernel<uint32_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(mc_engine_kernel)");
     mc_engine_kernel<uint32_t><<<unsigned(blocks), kWarps * 32, smem, st>>>(a);
   }
-  return launch_status("mc_engine_kernel");
+  int rc = launch_status("mc_engine_kernel");
+  if (rc != PDG_OK) return rc;
+  // sequential completion of rejected apps (normally none: every block exits
+  // after reading the counter)
+  const unsigned sblocks = unsigned(grid_warps < n_jobs ? grid_warps : n_jobs);
+  mc_serial_kernel<<<sblocks, 32, cnt_bytes, st>>>(a);
+  return launch_status("mc_serial_kernel");
 }

@@ -114,9 +114,9 @@ class DemandEngine:
                     (float(obs.input_len), float(obs.output_len), float(obs.parallelism)))
         return -1, (0.0, 0.0, 0.0)
 
-    def _scratch_for(self, n: int) -> torch.Tensor:
+    def _scratch_for(self, n: int, n_jobs: int) -> torch.Tensor:
         L = _lib.lib()
-        need = int(L.pdg_mc_scratch_bytes(n, self.max_pairs, L.pdg_mc_grid_warps()))
+        need = int(L.pdg_mc_scratch_bytes(n, self.max_pairs, L.pdg_mc_grid_warps())) + 4 * n_jobs
         if self._scratch is None or self._scratch.numel() < need:
             self._scratch = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._scratch
@@ -148,7 +148,7 @@ class DemandEngine:
         out = OutC(_lib.ptr(out_samples), n, _lib.ptr(queue.lo), _lib.ptr(queue.width),
                    _lib.ptr(queue.nbins), _lib.ptr(queue.nsamp), _lib.ptr(queue.counts),
                    queue.stride, _lib.ptr(slots), _lib.ptr(capped), _lib.ptr(flags))
-        scratch = self._scratch_for(n)
+        scratch = self._scratch_for(n, N)
         L = _lib.lib()
         _lib.check(L.pdg_mc_remaining_demand(
             C.byref(self.c_bank), C.byref(jobs), N, n, visit_cap, bucket_count,
