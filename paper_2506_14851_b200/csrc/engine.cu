@@ -239,6 +239,28 @@ __device__ __forceinline__ int next_unit(const EngineArgs& a, const UnitDesc& d,
   return __ldg(a.b.succ_nxt + d.succ_off + idx);
 }
 
+// the first three successors of a unit held in registers for a whole visit
+struct SuccCache {
+  double c0, c1, c2;
+  int n0, n1, n2, n3, ns;
+  __device__ __forceinline__ void load(const EngineArgs& a, const UnitDesc& d) {
+    const double* cum = a.b.succ_cum + d.succ_off;
+    const int32_t* nxt = a.b.succ_nxt + d.succ_off;
+    ns = d.succ_len;
+    c0 = ns > 0 ? __ldg(cum) : 2.0;                // cumulative probabilities <= 1
+    c1 = ns > 1 ? __ldg(cum + 1) : 2.0;
+    c2 = ns > 2 ? __ldg(cum + 2) : 2.0;
+    n0 = __ldg(nxt);
+    n1 = ns > 0 ? __ldg(nxt + 1) : -1;
+    n2 = ns > 1 ? __ldg(nxt + 2) : -1;
+    n3 = ns > 2 ? __ldg(nxt + 3) : -1;
+  }
+  __device__ __forceinline__ int next(const EngineArgs& a, const UnitDesc& d, double uu) const {
+    if (ns > 3) return next_unit(a, d, uu);
+    return !(c0 <= uu) ? n0 : !(c1 <= uu) ? n1 : !(c2 <= uu) ? n2 : n3;
+  }
+};
+
 // close a bounded-draw group of C halves: the word holding the last fresh half
 // was read by some lane (the largest word index a cursor holds)
 __device__ __forceinline__ void close_group(Stream& g, uint32_t C, const Cursor& ca,
@@ -271,6 +293,8 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
   const bool llm = d.flags & F_LLM;
   const Pools pl = pools_for(a, d, has_ov && u == cur_unit, ovp);
   const bool own = llm && (d.flags & F_OWN) && !(has_ov && u == cur_unit);
+  SuccCache sc;
+  sc.load(a, d);
   // members of this visit, in walk order: list position == rank
   uint32_t m = 0;
   for (uint32_t base = 0; base < na; base += 32) {
@@ -309,7 +333,7 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
       // random(m) word of member k, then the successor jump (estimator.py:350-353)
       const double uu = u53_double(cursor_word(cd, jt, g.inc, words + k));
       const Idx w = ws.mem[k];
-      ws.cur[w] = int8_t(next_unit(a, d, uu));
+      ws.cur[w] = int8_t(sc.next(a, d, uu));
       ws.tot[w] = dadd(ws.tot[w], t);
     }
     if (__any_sync(kFull, rej)) return false;
@@ -400,7 +424,7 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
   for (uint32_t k = k0; k < k1; ++k) {
     const double uu = u53_double(cursor_word(cd, jt, g.inc, words + k));
     const Idx w = ws.mem[k];
-    ws.cur[w] = int8_t(next_unit(a, d, uu));
+    ws.cur[w] = int8_t(sc.next(a, d, uu));
     ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
   }
   const unsigned last_lane = (m - 1) / per;
@@ -744,19 +768,27 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   int64_t blocks = (n_jobs + kWarps - 1) / kWarps;
   const int64_t capb = grid_warps / kWarps;
   if (blocks > capb) blocks = capb;
+  // persistent grid: exactly the resident CTAs (a second partial wave of
+  // grid-stride CTAs would leave SMs idle at the tail)
+  auto launch = [&](auto kern, size_t smem) -> int {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(smem));
+    if (err != cudaSuccess) return cuda_status(err, "cudaFuncSetAttribute(mc_engine_kernel)");
+    int per_sm = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+    if (err != cudaSuccess || per_sm < 1) per_sm = 1;
+    int64_t nb = int64_t(per_sm) * sm_count();
+    if (nb > capb) nb = capb;
+    if (nb > blocks) nb = blocks;
+    kern<<<unsigned(nb), kWarps * 32, smem, st>>>(a);
+    return PDG_OK;
+  };
   if (small_idx(n_samples)) {
     const size_t smem =
         size_t(kWarps) * (cnt_bytes + (sm ? size_t(kSmemWalks) * smem_walk_bytes<uint16_t>() : 0));
-    e = cudaFuncSetAttribute(mc_engine_kernel<uint16_t>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(mc_engine_kernel)");
-    mc_engine_kernel<uint16_t><<<unsigned(blocks), kWarps * 32, smem, st>>>(a);
+    if (int r = launch(mc_engine_kernel<uint16_t>, smem)) return r;
   } else {
-    const size_t smem = size_t(kWarps) * cnt_bytes;
-    e = cudaFuncSetAttribute(mc_engine_kernel<uint32_t>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(mc_engine_kernel)");
-    mc_engine_kernel<uint32_t><<<unsigned(blocks), kWarps * 32, smem, st>>>(a);
+    if (int r = launch(mc_engine_kernel<uint32_t>, size_t(kWarps) * cnt_bytes)) return r;
   }
   int rc = launch_status("mc_engine_kernel");
   if (rc != PDG_OK) return rc;
