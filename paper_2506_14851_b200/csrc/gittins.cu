@@ -239,6 +239,141 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1c: lane-per-row scorer for rows of <= 256 buckets (the queue's layout).
+// Each warp stages 32 rows (16 KB of u16 counts) into shared memory with
+// cp.async (double-buffered: the next tile streams in while this one is
+// scored), then lane l scans row l sequentially: no shuffles, ~11 issue
+// slots per bucket.  The alive boundary j0 is found with bit-exact float64
+// tests (binary search, values ascend), Z = sum of alive counts, and every
+// bucket j >= j0 contributes (P_j + d_j (Z - S_j)) / S_j; zero-mass buckets
+// never beat the previous positive one (and are +inf before any mass), so
+// they need no masking.  Rows must hold zero counts past nbins.
+// ---------------------------------------------------------------------------
+constexpr int kRowWarps = 6;
+constexpr int kRowU4 = 33;          // uint4 per staged row: 32 + 1 pad (bank spread)
+constexpr int kTileU4 = 32 * kRowU4;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gsrc), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ float lo16f(uint32_t x) {      // exact u16 -> float
+  return __int_as_float(__byte_perm(x, 0x4B00u, 0x7410)) - 8388608.f;
+}
+__device__ __forceinline__ float hi16f(uint32_t x) {
+  return __int_as_float(__byte_perm(x, 0x4B00u, 0x7432)) - 8388608.f;
+}
+
+__global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArgs a) {
+  extern __shared__ uint4 stage[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint4* buf0 = stage + size_t(wib) * 2 * kTileU4;
+  const int64_t ntiles = (a.n + 31) >> 5;
+  const int64_t gw = int64_t(blockIdx.x) * kRowWarps + wib;
+  const int64_t nw = int64_t(gridDim.x) * kRowWarps;
+  auto row_of = [&](int64_t i) -> int64_t { return a.row_idx ? int64_t(__ldg(a.row_idx + i)) : i; };
+  auto issue = [&](int64_t t, uint4* dst) {
+    const int64_t i = t * 32 + lane;
+    const int64_t myrow = i < a.n ? row_of(i) : -1;
+    for (int q = 0; q < 32; ++q) {
+      const int64_t r = __shfl_sync(kFull, myrow, q);
+      const uint4* src = reinterpret_cast<const uint4*>(a.counts + (r < 0 ? 0 : r) * a.stride);
+      cp_async16(dst + q * kRowU4 + lane, src + lane, r >= 0);
+    }
+    cp_async_commit();
+  };
+  int cur = 0;
+  if (gw < ntiles) issue(gw, buf0);
+  for (int64_t t = gw; t < ntiles; t += nw) {
+    const int64_t tn = t + nw;
+    if (tn < ntiles) issue(tn, buf0 + (cur ^ 1) * kTileU4);
+    else cp_async_commit();                          // keep the group count uniform
+    cp_async_wait<1>();
+    __syncwarp();
+    const uint4* row = buf0 + cur * kTileU4 + lane * kRowU4;
+    const int64_t i = t * 32 + lane;
+    if (i < a.n) {
+      const int64_t r = row_of(i);
+      const double lo = __ldg(a.lo + r), w = __ldg(a.width + r);
+      const double est = __ldg(a.est + r), age = __ldg(a.age + r);
+      const int k = __ldg(a.nbins + r);
+      // first alive bucket (values ascend): bit-exact float64 tests
+      int j0 = k;
+      double d0 = 0.0;
+      {
+        const double e0 = exact_d(lo, w, est, age, 0);
+        if (e0 > 0.0) {
+          j0 = 0;
+          d0 = e0;
+        } else {
+          int l = 1, h = k;                          // smallest alive j in [l, h)
+          while (l < h) {
+            const int mid = (l + h) >> 1;
+            if (exact_d(lo, w, est, age, mid) > 0.0) h = mid; else l = mid + 1;
+          }
+          j0 = l;
+          if (j0 < k) d0 = exact_d(lo, w, est, age, j0);
+        }
+      }
+      const int c0 = j0 >> 3, cend = (k + 7) >> 3;
+      // alive mass Z
+      float Z = 0.f;
+      for (int c = c0; c < cend; ++c) {
+        const uint4 v = row[c];
+        const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int j = c * 8 + 2 * h;
+          Z += (j >= j0 ? lo16f(wd[h]) : 0.f) + (j + 1 >= j0 ? hi16f(wd[h]) : 0.f);
+        }
+      }
+      float key;
+      uint8_t flags = 0;
+      if (!(Z > 0.f)) {                              // exhausted: sched.py:295-300
+        key = float(dmul(age, a.penalty));
+        flags = PDG_FLAG_OVERRUN;
+      } else {
+        const float df = float(d0), wf = float(w);
+        float S = 0.f, P = 0.f, best = __int_as_float(0x7f800000);
+        float tf = float(c0 * 8 - j0) - 1.f;         // (j - j0) before the first bucket
+        for (int c = c0; c < cend; ++c) {
+          const uint4 v = row[c];
+          const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const float m0 = (h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]);
+            tf += 1.f;
+            const float m = (tf >= 0.f) ? m0 : 0.f;  // j < j0 only in the first chunk
+            const float d = fmaf(tf, wf, df);
+            S += m;
+            P = fmaf(m, d, P);
+            const float num = fmaf(d, Z - S, P);
+            const float rr = tf >= 0.f ? __fdividef(num, S) : __int_as_float(0x7f800000);
+            best = fminf(best, rr);
+          }
+        }
+        key = best;
+      }
+      if (!(key > 0.f)) key = 0.f;
+      if (a.out_f32) a.out_f32[r] = key;
+      if (a.out_flags) a.out_flags[r] = flags;
+      if (a.out_key) {
+        const uint32_t tb = a.tiebreak ? a.tiebreak[r] : uint32_t(r);
+        a.out_key[r] = (uint64_t(__float_as_uint(key)) << 32) | tb;
+      }
+    }
+    __syncwarp();
+    cur ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
 }  // namespace pdg
 
 using namespace pdg;
@@ -286,6 +421,21 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
   if (blocks > cap) blocks = cap;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t maxb = rows->stride;   // buckets per row are bounded by the stride
+  if (maxb == 256) {
+    const size_t smem = size_t(kRowWarps) * 2 * kTileU4 * sizeof(uint4);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(gittins_rows_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gittins_rows_kernel)");
+      attr = true;
+    }
+    int64_t tiles = (n + 31) / 32;
+    int64_t nb = (tiles + kRowWarps - 1) / kRowWarps;
+    if (nb > sm_count()) nb = sm_count();
+    gittins_rows_kernel<<<unsigned(nb), kRowWarps * 32, smem, s>>>(a);
+    return launch_status("gittins_rows_kernel");
+  }
   if (maxb <= 256) gittins_hist_kernel<1><<<unsigned(blocks), threads, 0, s>>>(a);
   else if (maxb <= 512) gittins_hist_kernel<2><<<unsigned(blocks), threads, 0, s>>>(a);
   else if (maxb <= 1024) gittins_hist_kernel<4><<<unsigned(blocks), threads, 0, s>>>(a);
