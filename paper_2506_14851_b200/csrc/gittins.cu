@@ -264,10 +264,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ float lo16f(uint32_t x) {      // exact u16 -> float
-  return __int_as_float(__byte_perm(x, 0x4B00u, 0x7410)) - 8388608.f;
+  return __int_as_float(__byte_perm(x, 0x4B00u, 0x5410)) - 8388608.f;
 }
 __device__ __forceinline__ float hi16f(uint32_t x) {
-  return __int_as_float(__byte_perm(x, 0x4B00u, 0x7432)) - 8388608.f;
+  return __int_as_float(__byte_perm(x, 0x4B00u, 0x5432)) - 8388608.f;
 }
 
 __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArgs a) {
