@@ -242,15 +242,15 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
 // ---------------------------------------------------------------------------
 // K1c: lane-per-row scorer for rows of <= 256 buckets (the queue's layout).
 // Each warp stages 32 rows (16 KB of u16 counts) into shared memory with
-// cp.async (double-buffered: the next tile streams in while this one is
-// scored), then lane l scans row l sequentially: no shuffles, ~11 issue
+// cp.async (12 warps per SM overlap one another's copies and scans), then
+// lane l scans row l sequentially: no shuffles, ~11 issue
 // slots per bucket.  The alive boundary j0 is found with bit-exact float64
 // tests (binary search, values ascend), Z = sum of alive counts, and every
 // bucket j >= j0 contributes (P_j + d_j (Z - S_j)) / S_j; zero-mass buckets
 // never beat the previous positive one (and are +inf before any mass), so
 // they need no masking.  Rows must hold zero counts past nbins.
 // ---------------------------------------------------------------------------
-constexpr int kRowWarps = 6;
+constexpr int kRowWarps = 12;
 constexpr int kRowU4 = 33;          // uint4 per staged row: 32 + 1 pad (bank spread)
 constexpr int kTileU4 = 32 * kRowU4;
 
@@ -273,7 +273,7 @@ __device__ __forceinline__ float hi16f(uint32_t x) {
 __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArgs a) {
   extern __shared__ uint4 stage[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint4* buf0 = stage + size_t(wib) * 2 * kTileU4;
+  uint4* buf0 = stage + size_t(wib) * kTileU4;
   const int64_t ntiles = (a.n + 31) >> 5;
   const int64_t gw = int64_t(blockIdx.x) * kRowWarps + wib;
   const int64_t nw = int64_t(gridDim.x) * kRowWarps;
@@ -288,15 +288,12 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
     }
     cp_async_commit();
   };
-  int cur = 0;
-  if (gw < ntiles) issue(gw, buf0);
+  // single-buffered per warp: 12 warps per SM overlap one another's copies
   for (int64_t t = gw; t < ntiles; t += nw) {
-    const int64_t tn = t + nw;
-    if (tn < ntiles) issue(tn, buf0 + (cur ^ 1) * kTileU4);
-    else cp_async_commit();                          // keep the group count uniform
-    cp_async_wait<1>();
+    issue(t, buf0);
+    cp_async_wait<0>();
     __syncwarp();
-    const uint4* row = buf0 + cur * kTileU4 + lane * kRowU4;
+    const uint4* row = buf0 + lane * kRowU4;
     const int64_t i = t * 32 + lane;
     if (i < a.n) {
       const int64_t r = row_of(i);
@@ -369,9 +366,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
       }
     }
     __syncwarp();
-    cur ^= 1;
   }
-  cp_async_wait<0>();
 }
 
 }  // namespace pdg
@@ -422,7 +417,7 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t maxb = rows->stride;   // buckets per row are bounded by the stride
   if (maxb == 256) {
-    const size_t smem = size_t(kRowWarps) * 2 * kTileU4 * sizeof(uint4);
+    const size_t smem = size_t(kRowWarps) * kTileU4 * sizeof(uint4);
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(gittins_rows_kernel,

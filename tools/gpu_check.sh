@@ -19,7 +19,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mc_engine \
   -s 3 -c 1 -o gpurun_out/engine -f python bench.py --steps 1 --warmup 2 --ncu \
   > gpurun_out/ncu_engine.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gittins_hist \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gittins \
   -s 3 -c 1 -o gpurun_out/k1 -f python bench.py --steps 1 --warmup 2 --ncu \
   > gpurun_out/ncu_k1.log 2>&1
 echo done
