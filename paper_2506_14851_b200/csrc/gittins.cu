@@ -263,6 +263,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+__device__ __forceinline__ float rcp_approx(float x) {    // MUFU.RCP, ~1 ulp; rcp(0) = +inf
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ float lo16f(uint32_t x) {      // exact u16 -> float
   return __int_as_float(__byte_perm(x, 0x4B00u, 0x5410)) - 8388608.f;
 }
@@ -339,21 +345,32 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
         const float df = float(d0), wf = float(w);
         float S = 0.f, P = 0.f, best = __int_as_float(0x7f800000);
         float tf = float(c0 * 8 - j0) - 1.f;         // (j - j0) before the first bucket
-        for (int c = c0; c < cend; ++c) {
-          const uint4 v = row[c];
+        // one bucket: ~10 issue slots (approximate reciprocal: ~1e-7 relative)
+        auto bucket = [&](float m) {
+          tf += 1.f;
+          const float d = fmaf(tf, wf, df);
+          S += m;
+          P = fmaf(m, d, P);
+          const float num = fmaf(d, Z - S, P);
+          best = fminf(best, num * rcp_approx(S));
+        };
+        {                                            // first chunk: skip j < j0
+          const uint4 v = row[c0];
           const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
-            const float m0 = (h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]);
-            tf += 1.f;
-            const float m = (tf >= 0.f) ? m0 : 0.f;  // j < j0 only in the first chunk
-            const float d = fmaf(tf, wf, df);
-            S += m;
-            P = fmaf(m, d, P);
-            const float num = fmaf(d, Z - S, P);
-            const float rr = tf >= 0.f ? __fdividef(num, S) : __int_as_float(0x7f800000);
-            best = fminf(best, rr);
+            if (c0 * 8 + h >= j0) {
+              bucket((h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]));
+            } else {
+              tf += 1.f;
+            }
           }
+        }
+        for (int c = c0 + 1; c < cend; ++c) {
+          const uint4 v = row[c];
+          const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int h = 0; h < 8; ++h) bucket((h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]));
         }
         key = best;
       }
