@@ -190,7 +190,8 @@ int pdg_plan_prewarm(const double* pool, const int32_t* off, const int32_t* len,
  * unit's unconditioned service samples (simcore.py:480-487) conditioned on
  * "> now" as plan_prewarm does (prewarm.py:65-67).  agg[t, k] (optional) is
  * the sum over applications (expected number of applications needing a warm
- * type-t backend within W_k).  <= 32 windows, <= 64 types, <= 8 successors.
+ * type-t backend within W_k).  <= 32 windows, <= 64 types, <= 4 successors
+ * per unit (further successors are ignored).
  * ------------------------------------------------------------------------- */
 typedef struct {
   const double* svc_sorted;   /* service samples per unit, ascending          */

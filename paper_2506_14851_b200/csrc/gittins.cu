@@ -325,17 +325,26 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
         }
       }
       const int c0 = j0 >> 3, cend = (k + 7) >> 3;
-      // alive mass Z
-      float Z = 0.f;
-      for (int c = c0; c < cend; ++c) {
-        const uint4 v = row[c];
+      // alive mass Z: IDP2A sums both u16 counts of a word in one instruction
+      uint32_t zi = 0;
+      {
+        const uint4 v = row[c0];
         const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          const int j = c * 8 + 2 * h;
-          Z += (j >= j0 ? lo16f(wd[h]) : 0.f) + (j + 1 >= j0 ? hi16f(wd[h]) : 0.f);
+          const int j = c0 * 8 + 2 * h;
+          const uint32_t keep = (j >= j0 ? 0x0000ffffu : 0u) | (j + 1 >= j0 ? 0xffff0000u : 0u);
+          zi = __dp2a_lo(wd[h] & keep, 0x0101u, zi);
         }
       }
+      for (int c = c0 + 1; c < cend; ++c) {
+        const uint4 v = row[c];
+        zi = __dp2a_lo(v.x, 0x0101u, zi);
+        zi = __dp2a_lo(v.y, 0x0101u, zi);
+        zi = __dp2a_lo(v.z, 0x0101u, zi);
+        zi = __dp2a_lo(v.w, 0x0101u, zi);
+      }
+      const float Z = float(zi);
       float key;
       uint8_t flags = 0;
       if (!(Z > 0.f)) {                              // exhausted: sched.py:295-300
@@ -344,33 +353,32 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
       } else {
         const float df = float(d0), wf = float(w);
         float S = 0.f, P = 0.f, best = __int_as_float(0x7f800000);
-        float tf = float(c0 * 8 - j0) - 1.f;         // (j - j0) before the first bucket
-        // one bucket: ~10 issue slots (approximate reciprocal: ~1e-7 relative)
-        auto bucket = [&](float m) {
-          tf += 1.f;
-          const float d = fmaf(tf, wf, df);
+        // one bucket at offset h of a chunk whose first bucket sits at
+        // (j - j0) = tb: d = tb*w + h*w + d0 (positive terms), ~10 issue slots
+        auto bucket = [&](float m, float d) {
           S += m;
           P = fmaf(m, d, P);
           const float num = fmaf(d, Z - S, P);
-          best = fminf(best, num * rcp_approx(S));
+          best = fminf(best, num * rcp_approx(S));     // rcp(0) = inf before any mass
         };
         {                                            // first chunk: skip j < j0
           const uint4 v = row[c0];
           const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+          const float tb = float(c0 * 8 - j0);
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
-            if (c0 * 8 + h >= j0) {
-              bucket((h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]));
-            } else {
-              tf += 1.f;
-            }
+            if (c0 * 8 + h >= j0)
+              bucket((h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]),
+                     fmaf(tb + float(h), wf, df));
           }
         }
         for (int c = c0 + 1; c < cend; ++c) {
           const uint4 v = row[c];
           const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+          const float db = fmaf(float(c * 8 - j0), wf, df);
 #pragma unroll
-          for (int h = 0; h < 8; ++h) bucket((h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]));
+          for (int h = 0; h < 8; ++h)
+            bucket((h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]), fmaf(float(h), wf, db));
         }
         key = best;
       }

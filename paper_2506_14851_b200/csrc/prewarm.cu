@@ -171,40 +171,44 @@ __global__ void __launch_bounds__(256) prewarm_need_kernel(NeedArgs a) {
     const double now = a.now[app];
     const double* s = a.svc_sorted + a.svc_off[u];
     const int n = a.svc_len[u];
-    // completion = now + s; conditioned on > now (all if none)
-    const int first_live = lower_bound_abs(s, n, now, __longlong_as_double(
-        __double_as_longlong(now) + 1));             // smallest value > now
+    // completion = now + s; conditioned on > now (all if none).  Samples
+    // ascend; the common case (every sample finishes after now) is one test.
+    int first_live = 0;
+    if (n > 0 && !(dadd(now, s[0]) > now))
+      first_live = lower_bound_abs(s, n, now, __longlong_as_double(
+          __double_as_longlong(now) + 1));           // smallest value > now
     const int live = n - first_live;
     const int base = live > 0 ? first_live : 0;
     const int m = live > 0 ? live : n;
-    float out[8];
-    int types[8];
-    const int ns = a.succ_len[u] < 8 ? a.succ_len[u] : 8;
     double pneed = 0.0;
     if (kwin >= 0 && m > 0) {
       const double x = dadd(now, wk);
-      const int ge = n - lower_bound_abs(s + base, n - base, now, x) - base;
-      const int cnt_ge = ge < 0 ? 0 : ge;
+      const int cnt_ge = (n - base) - lower_bound_abs(s + base, n - base, now, x);
       pneed = 1.0 - __ddiv_rn(small_int_to_double(cnt_ge), small_int_to_double(m));
     }
-    for (int q = 0; q < ns; ++q) {
-      const int v = gbase + a.succ_nxt[a.succ_off[u] + q];
-      types[q] = a.unit_type[v];
-      out[q] = float(dmul(a.succ_p[a.succ_off[u] + q], pneed));
-    }
+    // up to 4 successors in registers; same-type successors add up
+    const int so = a.succ_off[u];
+    const int ns = a.succ_len[u] < 4 ? a.succ_len[u] : 4;
+    int t0 = -1, t1 = -1, t2 = -1, t3 = -1;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    if (ns > 0) { t0 = a.unit_type[gbase + a.succ_nxt[so]];     p0 = dmul(a.succ_p[so], pneed); }
+    if (ns > 1) { t1 = a.unit_type[gbase + a.succ_nxt[so + 1]]; p1 = dmul(a.succ_p[so + 1], pneed); }
+    if (ns > 2) { t2 = a.unit_type[gbase + a.succ_nxt[so + 2]]; p2 = dmul(a.succ_p[so + 2], pneed); }
+    if (ns > 3) { t3 = a.unit_type[gbase + a.succ_nxt[so + 3]]; p3 = dmul(a.succ_p[so + 3], pneed); }
     if (a.need && kwin >= 0) {
-      float* row = a.need + app * int64_t(TK);
+      const float f0 = float(p0), f1 = float(p1), f2 = float(p2), f3 = float(p3);
+      float* row = a.need + app * int64_t(TK) + kwin;
       for (int t = 0; t < a.n_types; ++t) {
-        float acc = 0.f;
-        for (int q = 0; q < ns; ++q) acc += types[q] == t ? out[q] : 0.f;
-        __stcs(row + t * a.n_windows + kwin, acc);
+        const float acc = (t0 == t ? f0 : 0.f) + (t1 == t ? f1 : 0.f) +
+                          (t2 == t ? f2 : 0.f) + (t3 == t ? f3 : 0.f);
+        __stcs(row + t * a.n_windows, acc);
       }
     }
     if (a.agg && kwin >= 0) {
-      for (int q = 0; q < ns; ++q)
-        if (types[q] >= 0)
-          atomicAdd(&sagg[types[q] * a.n_windows + kwin],
-                    dmul(a.succ_p[a.succ_off[u] + q], pneed));
+      if (t0 >= 0) atomicAdd(&sagg[t0 * a.n_windows + kwin], p0);
+      if (t1 >= 0) atomicAdd(&sagg[t1 * a.n_windows + kwin], p1);
+      if (t2 >= 0) atomicAdd(&sagg[t2 * a.n_windows + kwin], p2);
+      if (t3 >= 0) atomicAdd(&sagg[t3 * a.n_windows + kwin], p3);
     }
   }
   if (a.agg) {
