@@ -284,9 +284,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
   const int64_t gw = int64_t(blockIdx.x) * kRowWarps + wib;
   const int64_t nw = int64_t(gridDim.x) * kRowWarps;
   auto row_of = [&](int64_t i) -> int64_t { return a.row_idx ? int64_t(__ldg(a.row_idx + i)) : i; };
-  auto issue = [&](int64_t t, uint4* dst) {
-    const int64_t i = t * 32 + lane;
-    const int64_t myrow = i < a.n ? row_of(i) : -1;
+  auto issue = [&](int64_t myrow, uint4* dst) {
     for (int q = 0; q < 32; ++q) {
       const int64_t r = __shfl_sync(kFull, myrow, q);
       const uint4* src = reinterpret_cast<const uint4*>(a.counts + (r < 0 ? 0 : r) * a.stride);
@@ -296,16 +294,26 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
   };
   // single-buffered per warp: 12 warps per SM overlap one another's copies
   for (int64_t t = gw; t < ntiles; t += nw) {
-    issue(t, buf0);
+    const int64_t i = t * 32 + lane;
+    const bool valid = i < a.n;
+    const int64_t r = valid ? row_of(i) : -1;
+    // row headers are loaded while the counts stream into shared memory
+    double lo = 0.0, w = 0.0, est = 0.0, age = 0.0;
+    int k = 1;
+    uint32_t tb = 0;
+    if (valid) {
+      lo = __ldg(a.lo + r);
+      w = __ldg(a.width + r);
+      est = __ldg(a.est + r);
+      age = __ldg(a.age + r);
+      k = __ldg(a.nbins + r);
+      tb = a.tiebreak ? __ldg(a.tiebreak + r) : uint32_t(r);
+    }
+    issue(valid ? r : -1, buf0);
     cp_async_wait<0>();
     __syncwarp();
     const uint4* row = buf0 + lane * kRowU4;
-    const int64_t i = t * 32 + lane;
-    if (i < a.n) {
-      const int64_t r = row_of(i);
-      const double lo = __ldg(a.lo + r), w = __ldg(a.width + r);
-      const double est = __ldg(a.est + r), age = __ldg(a.age + r);
-      const int k = __ldg(a.nbins + r);
+    if (valid) {
       // first alive bucket (values ascend): bit-exact float64 tests
       int j0 = k;
       double d0 = 0.0;
@@ -327,7 +335,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
       const int c0 = j0 >> 3, cend = (k + 7) >> 3;
       // alive mass Z: IDP2A sums both u16 counts of a word in one instruction
       uint32_t zi = 0;
-      {
+      if (j0 < k) {                                  // else: nothing alive (exhausted)
         const uint4 v = row[c0];
         const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -385,10 +393,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
       if (!(key > 0.f)) key = 0.f;
       if (a.out_f32) a.out_f32[r] = key;
       if (a.out_flags) a.out_flags[r] = flags;
-      if (a.out_key) {
-        const uint32_t tb = a.tiebreak ? a.tiebreak[r] : uint32_t(r);
-        a.out_key[r] = (uint64_t(__float_as_uint(key)) << 32) | tb;
-      }
+      if (a.out_key) a.out_key[r] = (uint64_t(__float_as_uint(key)) << 32) | tb;
     }
     __syncwarp();
   }
