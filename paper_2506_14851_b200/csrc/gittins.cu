@@ -242,15 +242,15 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
 // ---------------------------------------------------------------------------
 // K1c: lane-per-row scorer for rows of <= 256 buckets (the queue's layout).
 // Each warp stages 32 rows (16 KB of u16 counts) into shared memory with
-// cp.async, double-buffered (tile t+1 and its row headers stream in while
-// tile t is scored), then lane l scans row l sequentially: no shuffles, ~11 issue
+// cp.async (12 warps per SM overlap one another's copies and scans), then
+// lane l scans row l sequentially: no shuffles, ~11 issue
 // slots per bucket.  The alive boundary j0 is found with bit-exact float64
 // tests (binary search, values ascend), Z = sum of alive counts, and every
 // bucket j >= j0 contributes (P_j + d_j (Z - S_j)) / S_j; zero-mass buckets
 // never beat the previous positive one (and are +inf before any mass), so
 // they need no masking.  Rows must hold zero counts past nbins.
 // ---------------------------------------------------------------------------
-constexpr int kRowWarps = 6;
+constexpr int kRowWarps = 12;
 constexpr int kRowU4 = 33;          // uint4 per staged row: 32 + 1 pad (bank spread)
 constexpr int kTileU4 = 32 * kRowU4;
 
@@ -279,7 +279,7 @@ __device__ __forceinline__ float hi16f(uint32_t x) {
 __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArgs a) {
   extern __shared__ uint4 stage[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint4* buf0 = stage + size_t(wib) * 2 * kTileU4;
+  uint4* buf0 = stage + size_t(wib) * kTileU4;
   const int64_t ntiles = (a.n + 31) >> 5;
   const int64_t gw = int64_t(blockIdx.x) * kRowWarps + wib;
   const int64_t nw = int64_t(gridDim.x) * kRowWarps;
@@ -292,42 +292,27 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
     }
     cp_async_commit();
   };
-  // per-row header registers, loaded with the tile they belong to
-  struct Hdr {
-    int64_t r;
-    double lo, w, est, age;
-    int k;
-    uint32_t tb;
-  };
-  auto fetch = [&](int64_t t, uint4* dst) -> Hdr {
-    Hdr h{-1, 0.0, 0.0, 0.0, 0.0, 1, 0u};
-    const int64_t i = t * 32 + lane;
-    if (t < ntiles && i < a.n) {
-      h.r = row_of(i);
-      h.lo = __ldg(a.lo + h.r);
-      h.w = __ldg(a.width + h.r);
-      h.est = __ldg(a.est + h.r);
-      h.age = __ldg(a.age + h.r);
-      h.k = __ldg(a.nbins + h.r);
-      h.tb = a.tiebreak ? __ldg(a.tiebreak + h.r) : uint32_t(h.r);
-    }
-    issue(h.r, dst);
-    return h;
-  };
-  // double-buffered per warp: tile t+1 streams in while tile t is scored
-  int cur = 0;
-  Hdr hn = fetch(gw, buf0);
+  // single-buffered per warp: 12 warps per SM overlap one another's copies
   for (int64_t t = gw; t < ntiles; t += nw) {
-    const Hdr hc = hn;
-    hn = fetch(t + nw, buf0 + (cur ^ 1) * kTileU4);
-    cp_async_wait<1>();
+    const int64_t i = t * 32 + lane;
+    const bool valid = i < a.n;
+    const int64_t r = valid ? row_of(i) : -1;
+    // row headers are loaded while the counts stream into shared memory
+    double lo = 0.0, w = 0.0, est = 0.0, age = 0.0;
+    int k = 1;
+    uint32_t tb = 0;
+    if (valid) {
+      lo = __ldg(a.lo + r);
+      w = __ldg(a.width + r);
+      est = __ldg(a.est + r);
+      age = __ldg(a.age + r);
+      k = __ldg(a.nbins + r);
+      tb = a.tiebreak ? __ldg(a.tiebreak + r) : uint32_t(r);
+    }
+    issue(valid ? r : -1, buf0);
+    cp_async_wait<0>();
     __syncwarp();
-    const uint4* row = buf0 + cur * kTileU4 + lane * kRowU4;
-    const bool valid = hc.r >= 0;
-    const int64_t r = hc.r;
-    const double lo = hc.lo, w = hc.w, est = hc.est, age = hc.age;
-    const int k = hc.k;
-    const uint32_t tb = hc.tb;
+    const uint4* row = buf0 + lane * kRowU4;
     if (valid) {
       // first alive bucket (values ascend): bit-exact float64 tests
       int j0 = k;
@@ -411,9 +396,7 @@ __global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArg
       if (a.out_key) a.out_key[r] = (uint64_t(__float_as_uint(key)) << 32) | tb;
     }
     __syncwarp();
-    cur ^= 1;
   }
-  cp_async_wait<0>();
 }
 
 }  // namespace pdg
@@ -464,7 +447,7 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t maxb = rows->stride;   // buckets per row are bounded by the stride
   if (maxb == 256) {
-    const size_t smem = size_t(kRowWarps) * 2 * kTileU4 * sizeof(uint4);
+    const size_t smem = size_t(kRowWarps) * kTileU4 * sizeof(uint4);
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(gittins_rows_kernel,
