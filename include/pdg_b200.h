@@ -125,7 +125,6 @@ typedef struct {
   const void* units;              /* unit descriptors, 64 B each            */
   const int32_t* graph_base;      /* [G] first unit of each graph           */
   const int32_t* graph_n;         /* [G] units per graph (<= 32)            */
-  int32_t max_units;              /* max over graph_n                        */
   const int32_t* unit_capacity;   /* [U] FIFO capacity (kept-list cap, K3)  */
   const double* vals;             /* sample pools (float64)                 */
   const int32_t* pool_off;        /* own-input per-bucket output pools      */

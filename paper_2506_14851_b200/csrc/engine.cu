@@ -136,9 +136,9 @@ __device__ __forceinline__ uint32_t cursor_half(Cursor& c, const uint64_t* jt, c
 template <typename Idx>
 struct WarpState {
   double* tot;      // [n] accumulated remaining demand per walk
+  Idx* act;         // [n] active walks, ascending
   Idx* mem;         // [n] members of the visited unit, ascending (= rank order)
-  uint32_t* mask;   // [umax][nwords] walks sitting on each unit (bitsets)
-  int nwords;       // ceil(n / 32)
+  int8_t* cur;      // [n] current unit per walk (-1 = terminated)
   uint32_t* cnt;    // [counters]
   double* tmp;      // [n] own-input path: input draw / stage time per rank (global)
   uint16_t* bkt;    // [n] own-input path: input bucket per rank (global)
@@ -285,8 +285,8 @@ __device__ __forceinline__ void close_group(Stream& g, uint32_t C, const Cursor&
 // ---------------------------------------------------------------------------
 template <typename Idx>
 __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& ovp,
-                           bool has_ov, int cur_unit, const WarpState<Idx>& ws, Stream& g,
-                           int lane) {
+                           bool has_ov, int cur_unit, const WarpState<Idx>& ws, uint32_t na,
+                           Stream& g, int lane) {
   const uint64_t* jt = a.b.jump;
   const unsigned lt = lanemask_lt();
   const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u];
@@ -295,24 +295,19 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
   const bool own = llm && (d.flags & F_OWN) && !(has_ov && u == cur_unit);
   SuccCache sc;
   sc.load(a, d);
-  // members of this visit, in walk order: list position == rank.  The
-  // unit's bitset is read word-parallel, then cleared (members re-enter the
-  // bitsets of their next units below).
+  // members of this visit, in walk order: list position == rank
   uint32_t m = 0;
-  uint32_t* um = ws.mask + size_t(u) * ws.nwords;
-  for (int base = 0; base < ws.nwords; base += 32) {
-    const int wi = base + lane;
-    uint32_t word = wi < ws.nwords ? um[wi] : 0u;
-    const uint32_t c = __popc(word);
-    const uint32_t incl = warp_incl_scan(c, lane);
-    uint32_t off = m + incl - c;
-    while (word) {
-      const int b = __ffs(word) - 1;
-      word &= word - 1;
-      ws.mem[off++] = Idx(wi * 32 + b);
+  for (uint32_t base = 0; base < na; base += 32) {
+    const uint32_t idx = base + lane;
+    bool is = false;
+    Idx w = 0;
+    if (idx < na) {
+      w = ws.act[idx];
+      is = ws.cur[w] == u;
     }
-    if (wi < ws.nwords) um[wi] = 0u;
-    m += __shfl_sync(kFull, incl, 31);
+    const unsigned bal = __ballot_sync(kFull, is);
+    if (is) ws.mem[m + __popc(bal & lt)] = w;
+    m += __popc(bal);
   }
   __syncwarp();
   const uint32_t per = (m + 31) >> 5;
@@ -338,8 +333,7 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
       // random(m) word of member k, then the successor jump (estimator.py:350-353)
       const double uu = u53_double(cursor_word(cd, jt, g.inc, words + k));
       const Idx w = ws.mem[k];
-      const int nx = sc.next(a, d, uu);
-      if (nx >= 0) atomicOr(ws.mask + size_t(nx) * ws.nwords + (w >> 5), 1u << (w & 31));
+      ws.cur[w] = int8_t(sc.next(a, d, uu));
       ws.tot[w] = dadd(ws.tot[w], t);
     }
     if (__any_sync(kFull, rej)) return false;
@@ -430,8 +424,7 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
   for (uint32_t k = k0; k < k1; ++k) {
     const double uu = u53_double(cursor_word(cd, jt, g.inc, words + k));
     const Idx w = ws.mem[k];
-    const int nx = sc.next(a, d, uu);
-    if (nx >= 0) atomicOr(ws.mask + size_t(nx) * ws.nwords + (w >> 5), 1u << (w & 31));
+    ws.cur[w] = int8_t(sc.next(a, d, uu));
     ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
   }
   const unsigned last_lane = (m - 1) / per;
@@ -444,17 +437,20 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
 // ---------------------------------------------------------------------------
 // shared epilogue: samples out, capped count, bucketing (distributions.py:79-105)
 // ---------------------------------------------------------------------------
-__device__ void write_result(const EngineArgs& a, int64_t job, const double* tot, int capped,
-                             uint32_t* cnt, bool conditioned, bool has_ov, bool replayed,
-                             int lane) {
+__device__ void write_result(const EngineArgs& a, int64_t job, const double* tot,
+                             const int8_t* cur, uint32_t* cnt, bool conditioned, bool has_ov,
+                             bool replayed, int lane) {
   const int n = a.n;
+  int capped = 0;
   double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
   for (int w = lane; w < n; w += 32) {
+    capped += cur[w] >= 0;
     const double sv = tot[w];
     lo = fmin(lo, sv);
     hi = fmax(hi, sv);
     if (a.o.samples) a.o.samples[job * a.o.samples_stride + w] = sv;
   }
+  capped = warp_sum(capped);
   for (int o = 16; o > 0; o >>= 1) {
     lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
     hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
@@ -495,11 +491,7 @@ __device__ void write_result(const EngineArgs& a, int64_t job, const double* tot
 // per-warp footprints
 // ---------------------------------------------------------------------------
 template <typename Idx>
-__host__ __device__ constexpr size_t smem_walk_bytes() { return 8 + sizeof(Idx); }
-// per-warp bitsets: umax units x ceil(n/32) words
-__host__ __device__ inline size_t mask_bytes(int umax, int n) {
-  return size_t(umax) * size_t((n + 31) >> 5) * 4;
-}
+__host__ __device__ constexpr size_t smem_walk_bytes() { return 8 + 2 * sizeof(Idx) + 1; }
 template <typename Idx>
 __host__ __device__ constexpr size_t gmem_walk_bytes() {   // own-input arrays
   return 8 + 2 + sizeof(Idx);
@@ -509,12 +501,12 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 
 template <typename Idx>
 __device__ WarpState<Idx> carve(unsigned char* walk_base, unsigned char* gbase, int nw,
-                                int n, int umax, uint32_t* cnt, int max_pairs) {
+                                uint32_t* cnt, int max_pairs) {
   WarpState<Idx> ws;
   ws.tot = reinterpret_cast<double*>(walk_base);
-  ws.mem = reinterpret_cast<Idx*>(ws.tot + nw);
-  ws.mask = reinterpret_cast<uint32_t*>(walk_base + align16(size_t(nw) * smem_walk_bytes<Idx>()));
-  ws.nwords = (n + 31) >> 5;
+  ws.act = reinterpret_cast<Idx*>(ws.tot + nw);
+  ws.mem = ws.act + nw;
+  ws.cur = reinterpret_cast<int8_t*>(ws.mem + nw);
   ws.cnt = cnt;
   ws.tmp = reinterpret_cast<double*>(gbase);
   ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + nw);
@@ -542,22 +534,20 @@ __global__ void __launch_bounds__(kWarps * 32, 5) mc_engine_kernel(EngineArgs a)
   const int n = a.n;
   const bool in_smem = n <= kSmemWalks;
   const int nw = in_smem ? kSmemWalks : ((n + 15) & ~15);
-  const int umax = a.b.max_units;
   const size_t cnt_bytes = align16(size_t(a.counters) * 4);
-  const size_t walk_bytes = align16(size_t(nw) * smem_walk_bytes<Idx>()) + align16(mask_bytes(umax, nw));
-  const size_t per_warp_smem = cnt_bytes + (in_smem ? walk_bytes : 0);
+  const size_t per_warp_smem =
+      cnt_bytes + (in_smem ? size_t(kSmemWalks) * smem_walk_bytes<Idx>() : 0);
   unsigned char* sb = smem + per_warp_smem * wib;
   const int64_t gwarp = int64_t(blockIdx.x) * kWarps + wib;
   unsigned char* gs =
       reinterpret_cast<unsigned char*>(a.scratch) + size_t(gwarp) * a.scratch_per_warp;
-  unsigned char* gown = gs + (in_smem ? 0 : walk_bytes);
-  const WarpState<Idx> ws = carve<Idx>(in_smem ? sb + cnt_bytes : gs, gown, nw, n, umax,
+  unsigned char* gown = gs + (in_smem ? 0 : align16(size_t(nw) * smem_walk_bytes<Idx>()));
+  const WarpState<Idx> ws = carve<Idx>(in_smem ? sb + cnt_bytes : gs, gown, nw,
                                        reinterpret_cast<uint32_t*>(sb), a.max_pairs);
-  const int nwords = ws.nwords;
+  const unsigned lt = lanemask_lt();
   const int64_t stride = int64_t(gridDim.x) * kWarps;
   for (int64_t job = gwarp; job < a.n_jobs; job += stride) {
     const int gbase = a.b.graph_base[a.j.graph[job]];
-    const int gn = a.b.graph_n[a.j.graph[job]];
     const int u0 = a.j.unit[job];
     Stream g;
     pcg_seed(a.j.seed[job], g.s, g.inc);
@@ -570,28 +560,41 @@ __global__ void __launch_bounds__(kWarps * 32, 5) mc_engine_kernel(EngineArgs a)
     job_obs(a, job, obs_up, obs);
     const bool has_ov =
         condition(a, gbase, u0, obs_up, obs, ws.kin, ws.kout, ovp, conditioned, lane);
-    for (int w = lane; w < n; w += 32) ws.tot[w] = 0.0;
-    for (int i = lane; i < gn * nwords; i += 32) {
-      const int uu = i / nwords, wi = i - uu * nwords;
-      uint32_t v = 0u;
-      if (uu == u0) v = (wi + 1) * 32 <= n ? 0xffffffffu : ((1u << (n & 31)) - 1u);
-      ws.mask[i] = v;
+    for (int w = lane; w < n; w += 32) {
+      ws.cur[w] = int8_t(u0);
+      ws.tot[w] = 0.0;
+      ws.act[w] = Idx(w);
     }
     __syncwarp();
+    uint32_t na = uint32_t(n);
     bool ok = true;
     for (int step = 0; step < a.cap && ok; ++step) {
-      // occupied units at the start of the step (frozen, estimator.py:347)
+      // compact the still-active walks (order kept) and collect occupied units
       unsigned occ = 0;
-      for (int uu = 0; uu < gn; ++uu) {
-        uint32_t any = 0u;
-        for (int wi = lane; wi < nwords; wi += 32) any |= ws.mask[uu * nwords + wi];
-        if (__any_sync(kFull, any != 0u)) occ |= 1u << uu;
+      uint32_t nn = 0;
+      for (uint32_t base = 0; base < na; base += 32) {
+        const uint32_t idx = base + lane;
+        Idx w = 0;
+        int c = -1;
+        if (idx < na) {
+          w = ws.act[idx];
+          c = ws.cur[w];
+        }
+        const unsigned bal = __ballot_sync(kFull, c >= 0);
+        if (c >= 0) {
+          ws.act[nn + __popc(bal & lt)] = w;
+          occ |= 1u << c;
+        }
+        nn += __popc(bal);
       }
+      na = nn;
+      occ = __reduce_or_sync(kFull, occ);
+      __syncwarp();
       if (!occ) break;
       while (occ && ok) {
         const int u = __ffs(occ) - 1;
         occ &= occ - 1;
-        ok = visit_unit<Idx>(a, gbase, u, ovp, has_ov, u0, ws, g, lane);
+        ok = visit_unit<Idx>(a, gbase, u, ovp, has_ov, u0, ws, na, g, lane);
       }
     }
     if (!ok) {                     // Lemire rejection: leave it to mc_serial_kernel
@@ -599,10 +602,7 @@ __global__ void __launch_bounds__(kWarps * 32, 5) mc_engine_kernel(EngineArgs a)
       __syncwarp();
       continue;
     }
-    int capped = 0;                // walks still active after the visit cap
-    for (int i = lane; i < gn * nwords; i += 32) capped += __popc(ws.mask[i]);
-    capped = warp_sum(capped);
-    write_result(a, job, ws.tot, capped, ws.cnt, conditioned, has_ov, false, lane);
+    write_result(a, job, ws.tot, ws.cur, ws.cnt, conditioned, has_ov, false, lane);
   }
 }
 
@@ -688,10 +688,7 @@ __global__ void __launch_bounds__(32) mc_serial_kernel(EngineArgs a) {
       }
     }
     __syncwarp();
-    int capped = 0;
-    for (int w = lane; w < n; w += 32) capped += cur[w] >= 0;
-    capped = warp_sum(capped);
-    write_result(a, job, tot, capped, cnt, conditioned, has_ov, true, lane);
+    write_result(a, job, tot, cur, cnt, conditioned, has_ov, true, lane);
   }
 }
 
@@ -701,12 +698,11 @@ using namespace pdg;
 
 static bool small_idx(int n) { return n <= 65535; }
 
-static size_t walk_scratch(int n, int umax) {
+static size_t walk_scratch(int n) {
   const size_t nw = size_t((n + 15) & ~15);
   const bool si = small_idx(n);
   const size_t smem_part = n <= kSmemWalks ? 0
-      : align16(nw * (si ? smem_walk_bytes<uint16_t>() : smem_walk_bytes<uint32_t>())) +
-            align16(mask_bytes(umax, int(nw)));
+      : align16(nw * (si ? smem_walk_bytes<uint16_t>() : smem_walk_bytes<uint32_t>()));
   const size_t own = align16(nw * (si ? gmem_walk_bytes<uint16_t>() : gmem_walk_bytes<uint32_t>()));
   const size_t fast = smem_part + own;
   const size_t serial = serial_bytes(int(nw));
@@ -714,7 +710,7 @@ static size_t walk_scratch(int n, int umax) {
 }
 
 static size_t scratch_per_warp(int n, int max_pairs) {
-  return (walk_scratch(n, 32) + align16(size_t(max_pairs) * 16) + 64 + 255) & ~size_t(255);
+  return (walk_scratch(n) + align16(size_t(max_pairs) * 16) + 64 + 255) & ~size_t(255);
 }
 
 // scratch = per-warp regions + 256 B (serial counter) + one int per job
@@ -730,7 +726,6 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
                                        int32_t max_pairs, const pdg_mc_out* out,
                                        void* scratch, size_t scratch_bytes, void* stream) {
   if (!bank || !jobs || !out || n_jobs < 0 || n_jobs > INT32_MAX || n_samples < 1 ||
-      bank->max_units < 1 || bank->max_units > 32 ||
       n_samples > (1 << 19) || visit_cap < 0 || bucket_count < 1 || bucket_count > 1024 ||
       max_unit_k < 0 || max_unit_k > 1024 || max_pairs < 0) {
     set_error("pdg_mc_remaining_demand: invalid arguments");
@@ -789,9 +784,8 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
     return PDG_OK;
   };
   if (small_idx(n_samples)) {
-    const size_t wb = align16(size_t(kSmemWalks) * smem_walk_bytes<uint16_t>()) +
-                      align16(mask_bytes(bank->max_units, kSmemWalks));
-    const size_t smem = size_t(kWarps) * (cnt_bytes + (sm ? wb : 0));
+    const size_t smem =
+        size_t(kWarps) * (cnt_bytes + (sm ? size_t(kSmemWalks) * smem_walk_bytes<uint16_t>() : 0));
     if (int r = launch(mc_engine_kernel<uint16_t>, smem)) return r;
   } else {
     if (int r = launch(mc_engine_kernel<uint32_t>, size_t(kWarps) * cnt_bytes)) return r;

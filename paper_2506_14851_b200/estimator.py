@@ -30,7 +30,7 @@ WALK_VISIT_CAP = 64
 
 class GraphBankC(C.Structure):
     _fields_ = [("units", C.c_void_p), ("graph_base", C.c_void_p), ("graph_n", C.c_void_p),
-                ("max_units", C.c_int32), ("unit_capacity", C.c_void_p), ("vals", C.c_void_p),
+                ("unit_capacity", C.c_void_p), ("vals", C.c_void_p),
                 ("pool_off", C.c_void_p), ("pool_len", C.c_void_p),
                 ("succ_cum", C.c_void_p), ("succ_nxt", C.c_void_p), ("conds", C.c_void_p),
                 ("pairs", C.c_void_p), ("jump", C.c_void_p), ("prefill_rate", C.c_double),
@@ -92,7 +92,7 @@ class DemandEngine:
         b = self.bank
         self.jump = _jump_tensor(self.device)
         self.c_bank = GraphBankC(
-            _lib.ptr(b.units), _lib.ptr(b.graph_base), _lib.ptr(b.graph_n), b.max_units,
+            _lib.ptr(b.units), _lib.ptr(b.graph_base), _lib.ptr(b.graph_n),
             _lib.ptr(b.unit_capacity), _lib.ptr(b.vals), _lib.ptr(b.pool_off),
             _lib.ptr(b.pool_len), _lib.ptr(b.succ_cum), _lib.ptr(b.succ_nxt),
             _lib.ptr(b.conds), _lib.ptr(b.pairs), _lib.ptr(self.jump),

@@ -347,7 +347,6 @@ class GraphBank:
         self.conds = t(ca.view(np.uint8).reshape(-1), np.uint8)
         self.pairs = t(pa.view(np.uint8).reshape(-1), np.uint8)
         self.max_unit_k = int(units["ib_k"].max()) if len(units) else 1
-        self.max_units = int(np.max(gn)) if len(gn) else 1
         self.max_pairs = int(ca["pair_len"].max())
 
     def local_unit(self, name: str, uid: str) -> int:
