@@ -135,6 +135,15 @@ class DemandEngine:
             raise EstimationError("u16 histogram counts need n <= 65535")
         N = int(graph_idx.numel())
         dev = self.device
+        if self.bank.empty_units:
+            # the reference builds a sampler for every unit and raises before
+            # walking (estimator.py:246-268): reject jobs on such graphs
+            bad = {self.bank.index[nm] for nm in self.bank.empty_units}
+            used = set(graph_idx.cpu().tolist())
+            hit = sorted(bad & used)
+            if hit:
+                nm = self.bank.names[hit[0]]
+                raise EstimationError(self.bank.empty_units[nm][0][1])
         out_samples = torch.empty((N, n), dtype=torch.float64, device=dev) if samples else None
         capped = torch.empty(N, dtype=torch.int32, device=dev)
         flags = torch.empty(N, dtype=torch.uint8, device=dev)

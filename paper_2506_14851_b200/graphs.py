@@ -222,10 +222,20 @@ class GraphBank:
             vals.extend(float(x) for x in xs)
             return off, len(xs)
 
+        self.empty_units = {}       # name -> [(uid, message)] (estimator.py:246-268)
         for nm in self.names:
             g = graphs[nm]
             order = sorted(g.units)
             self.unit_order[nm] = order
+            for uid in order:
+                u = g.units[uid]
+                if u.is_llm and (not list(u.input_dist.samples) or
+                                 not list(u.output_dist.samples)):
+                    self.empty_units.setdefault(nm, []).append(
+                        (uid, f"unit {uid!r} has no token-length samples"))
+                elif not u.is_llm and not list(u.duration_dist.samples):
+                    self.empty_units.setdefault(nm, []).append(
+                        (uid, f"unit {uid!r} has no duration samples"))
             pos = {u: i for i, u in enumerate(order)}
             gbase.append(len(units))
             gn.append(len(order))
@@ -311,6 +321,7 @@ class GraphBank:
         layout the compiler produces.  No K3 records, no own-input pools."""
         self = cls.__new__(cls)
         g = len(graph_base)
+        self.empty_units = {}
         self.names = list(names) if names is not None else [str(i) for i in range(g)]
         self.index = {nm: i for i, nm in enumerate(self.names)}
         self.unit_order = unit_order or {}

@@ -187,3 +187,28 @@ def test_lemire_rejection_replayed_exactly():
     want = O.mc_remaining_demand(og, "a", [], n, seed, steps)
     np.testing.assert_array_equal(got[0][0], want.samples)
     assert got[0][2] & 4, "the sequential replay path was not exercised"
+
+
+def test_visit_cap_zero_and_empty_units(kb_graphs):
+    """visit_cap=0: no step runs, every walk is capped at 0 (estimator.py:343);
+    a graph with a sample-less unit raises like the reference sampler."""
+    import torch
+    from paper_2506_14851_b200 import estimator as E
+    from paper_2506_14851_b200.errors import EstimationError
+    from paper_2506_14851_b200.graphs import graph_from_kb
+
+    class Env:
+        prefill_rate, decode_rate = 10000.0, 50.0
+
+    g = graph_from_kb(kb_graphs["chain"])
+    r = E.monte_carlo_remaining_demand(g, "a", [], Env, n=64, seed=3, visit_cap=0)
+    og = O.graph_from_kb(kb_graphs["chain"])
+    want = O.mc_remaining_demand(og, "a", [], 64, 3, visit_cap=0)
+    np.testing.assert_array_equal(np.asarray(r.samples), want.samples)
+    assert r.capped_walks == want.capped == 64
+    doc = dict(kb_graphs["chain"])
+    doc["units"] = [dict(u) for u in doc["units"]]
+    doc["units"][1]["records"] = []             # unit "b" loses its samples
+    g2 = graph_from_kb(doc)
+    with pytest.raises(EstimationError, match="no duration samples"):
+        E.monte_carlo_remaining_demand(g2, "a", [], Env, n=8, seed=1)

@@ -22,4 +22,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:mc_e
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gittins \
   -s 3 -c 1 -o gpurun_out/k1 -f python bench.py --steps 1 --warmup 2 --ncu \
   > gpurun_out/ncu_k1.log 2>&1
+
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:prewarm_need \
+  -s 2 -c 1 -o gpurun_out/need -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline \
+  > gpurun_out/ncu_need.log 2>&1
 echo done
