@@ -153,24 +153,35 @@ __device__ __forceinline__ int lower_bound_abs(const double* s, int n, double no
   return lo;
 }
 
-__global__ void __launch_bounds__(256) prewarm_need_kernel(NeedArgs a) {
-  extern __shared__ double sagg[];                  // [T*K] block partial aggregate
-  const int lane = threadIdx.x & 31;
+constexpr int kNeedWarps = 8;
+constexpr int kNeedStage = 256;       // service samples staged in shared memory per warp
+
+__global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs a) {
+  // per warp: staged service samples + a private [T][K] aggregate (each lane
+  // owns window column k, so no atomics until the block reduction)
+  extern __shared__ double nsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int TK = a.n_types * a.n_windows;
-  if (a.agg) {
-    for (int i = threadIdx.x; i < TK; i += blockDim.x) sagg[i] = 0.0;
-    __syncthreads();
-  }
-  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  double* stage = nsm + size_t(wib) * kNeedStage;
+  double* wagg = nsm + size_t(kNeedWarps) * kNeedStage + size_t(wib) * TK;
+  if (a.agg)
+    for (int i = lane; i < TK; i += 32) wagg[i] = 0.0;
+  const int64_t gw = int64_t(blockIdx.x) * kNeedWarps + wib;
+  const int64_t nw = int64_t(gridDim.x) * kNeedWarps;
   const int kwin = lane < a.n_windows ? lane : -1;
   const double wk = kwin >= 0 ? a.windows[kwin] : 0.0;
   for (int64_t app = gw; app < a.n; app += nw) {
     const int gbase = a.graph_base[a.graph[app]];
     const int u = gbase + a.unit[app];
     const double now = a.now[app];
-    const double* s = a.svc_sorted + a.svc_off[u];
     const int n = a.svc_len[u];
+    const double* gsrc = a.svc_sorted + a.svc_off[u];
+    const double* s = gsrc;
+    if (n <= kNeedStage) {                           // coalesced stage, then LDS searches
+      for (int i = lane; i < n; i += 32) stage[i] = gsrc[i];
+      __syncwarp();
+      s = stage;
+    }
     // completion = now + s; conditioned on > now (all if none).  Samples
     // ascend; the common case (every sample finishes after now) is one test.
     int first_live = 0;
@@ -180,41 +191,53 @@ __global__ void __launch_bounds__(256) prewarm_need_kernel(NeedArgs a) {
     const int live = n - first_live;
     const int base = live > 0 ? first_live : 0;
     const int m = live > 0 ? live : n;
-    double pneed = 0.0;
+    float pneed = 0.f;                               // P(completion < now + W_k)
     if (kwin >= 0 && m > 0) {
       const double x = dadd(now, wk);
       const int cnt_ge = (n - base) - lower_bound_abs(s + base, n - base, now, x);
-      pneed = 1.0 - __ddiv_rn(small_int_to_double(cnt_ge), small_int_to_double(m));
+      pneed = 1.f - __fdiv_rn(float(cnt_ge), float(m));
     }
-    // up to 4 successors in registers; same-type successors add up
+    // up to 4 successors; successors of equal type are merged first
     const int so = a.succ_off[u];
     const int ns = a.succ_len[u] < 4 ? a.succ_len[u] : 4;
     int t0 = -1, t1 = -1, t2 = -1, t3 = -1;
-    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-    if (ns > 0) { t0 = a.unit_type[gbase + a.succ_nxt[so]];     p0 = dmul(a.succ_p[so], pneed); }
-    if (ns > 1) { t1 = a.unit_type[gbase + a.succ_nxt[so + 1]]; p1 = dmul(a.succ_p[so + 1], pneed); }
-    if (ns > 2) { t2 = a.unit_type[gbase + a.succ_nxt[so + 2]]; p2 = dmul(a.succ_p[so + 2], pneed); }
-    if (ns > 3) { t3 = a.unit_type[gbase + a.succ_nxt[so + 3]]; p3 = dmul(a.succ_p[so + 3], pneed); }
-    if (a.need && kwin >= 0) {
-      const float f0 = float(p0), f1 = float(p1), f2 = float(p2), f3 = float(p3);
-      float* row = a.need + app * int64_t(TK) + kwin;
-      for (int t = 0; t < a.n_types; ++t) {
-        const float acc = (t0 == t ? f0 : 0.f) + (t1 == t ? f1 : 0.f) +
-                          (t2 == t ? f2 : 0.f) + (t3 == t ? f3 : 0.f);
-        __stcs(row + t * a.n_windows, acc);
+    float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
+    if (ns > 0) { t0 = a.unit_type[gbase + a.succ_nxt[so]];     f0 = float(a.succ_p[so]) * pneed; }
+    if (ns > 1) { t1 = a.unit_type[gbase + a.succ_nxt[so + 1]]; f1 = float(a.succ_p[so + 1]) * pneed; }
+    if (ns > 2) { t2 = a.unit_type[gbase + a.succ_nxt[so + 2]]; f2 = float(a.succ_p[so + 2]) * pneed; }
+    if (ns > 3) { t3 = a.unit_type[gbase + a.succ_nxt[so + 3]]; f3 = float(a.succ_p[so + 3]) * pneed; }
+    if (t1 >= 0 && t1 == t0) { f0 += f1; t1 = -1; }
+    if (t2 >= 0 && t2 == t0) { f0 += f2; t2 = -1; }
+    if (t2 >= 0 && t2 == t1) { f1 += f2; t2 = -1; }
+    if (t3 >= 0 && t3 == t0) { f0 += f3; t3 = -1; }
+    if (t3 >= 0 && t3 == t1) { f1 += f3; t3 = -1; }
+    if (t3 >= 0 && t3 == t2) { f2 += f3; t3 = -1; }
+    if (kwin >= 0) {
+      if (a.need) {                                  // dense row: zeros, then the <= 4 types
+        float* row = a.need + app * int64_t(TK) + kwin;
+        for (int t = 0; t < a.n_types; ++t) __stcs(row + t * a.n_windows, 0.f);
+        if (t0 >= 0) __stcs(row + t0 * a.n_windows, f0);
+        if (t1 >= 0) __stcs(row + t1 * a.n_windows, f1);
+        if (t2 >= 0) __stcs(row + t2 * a.n_windows, f2);
+        if (t3 >= 0) __stcs(row + t3 * a.n_windows, f3);
+      }
+      if (a.agg) {
+        if (t0 >= 0) wagg[t0 * a.n_windows + kwin] += f0;
+        if (t1 >= 0) wagg[t1 * a.n_windows + kwin] += f1;
+        if (t2 >= 0) wagg[t2 * a.n_windows + kwin] += f2;
+        if (t3 >= 0) wagg[t3 * a.n_windows + kwin] += f3;
       }
     }
-    if (a.agg && kwin >= 0) {
-      if (t0 >= 0) atomicAdd(&sagg[t0 * a.n_windows + kwin], p0);
-      if (t1 >= 0) atomicAdd(&sagg[t1 * a.n_windows + kwin], p1);
-      if (t2 >= 0) atomicAdd(&sagg[t2 * a.n_windows + kwin], p2);
-      if (t3 >= 0) atomicAdd(&sagg[t3 * a.n_windows + kwin], p3);
-    }
+    __syncwarp();
   }
   if (a.agg) {
     __syncthreads();
-    for (int i = threadIdx.x; i < TK; i += blockDim.x)
-      if (sagg[i] != 0.0) atomicAdd(a.agg + i, sagg[i]);
+    for (int i = threadIdx.x; i < TK; i += blockDim.x) {
+      double acc = 0.0;
+      for (int q = 0; q < kNeedWarps; ++q)
+        acc += nsm[size_t(kNeedWarps) * kNeedStage + size_t(q) * TK + i];
+      if (acc != 0.0) atomicAdd(a.agg + i, acc);
+    }
   }
 }
 
@@ -255,10 +278,16 @@ extern "C" int pdg_prewarm_need(const pdg_prewarm_tables* t, const int32_t* grap
   NeedArgs a{t->svc_sorted, t->svc_off, t->svc_len, t->graph_base, t->succ_off, t->succ_len,
              t->succ_nxt, t->succ_p, t->unit_type, graph, unit, now, windows, n_types,
              n_windows, n, need, agg};
-  int64_t blocks = (n * 32 + 255) / 256;
-  const int64_t cap = int64_t(sm_count()) * 8;
+  const size_t smem = sizeof(double) * size_t(kNeedWarps) *
+                      (kNeedStage + (agg ? size_t(n_types) * n_windows : 0));
+  cudaError_t e = cudaFuncSetAttribute(prewarm_need_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(prewarm_need_kernel)");
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prewarm_need_kernel, kNeedWarps * 32, smem);
+  int64_t blocks = (n + kNeedWarps - 1) / kNeedWarps;
+  const int64_t cap = int64_t(sm_count()) * (per_sm > 0 ? per_sm : 1);
   if (blocks > cap) blocks = cap;
-  const size_t smem = agg ? size_t(n_types) * n_windows * sizeof(double) : 0;
-  prewarm_need_kernel<<<unsigned(blocks), 256, smem, (cudaStream_t)stream>>>(a);
+  prewarm_need_kernel<<<unsigned(blocks), kNeedWarps * 32, smem, (cudaStream_t)stream>>>(a);
   return launch_status("prewarm_need_kernel");
 }
