@@ -133,7 +133,7 @@ typedef struct {
   const int32_t* succ_nxt;        /* next local unit, -1 = terminate        */
   const void* conds;              /* K3 (unit, upstream) descriptors        */
   const void* pairs;              /* K3 joined records                      */
-  const uint64_t* jump;           /* PCG64 jump tables [2][1024][4]         */
+  const uint64_t* jump;           /* PCG64 jump tables [3][1024][4]         */
   double prefill_rate, decode_rate; /* RateProfile (pdgraph.py:282-291)     */
 } pdg_graph_bank;
 

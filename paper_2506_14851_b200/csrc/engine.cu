@@ -439,18 +439,18 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
 // ---------------------------------------------------------------------------
 __device__ void write_result(const EngineArgs& a, int64_t job, const double* tot,
                              const int8_t* cur, uint32_t* cnt, bool conditioned, bool has_ov,
-                             bool replayed, int lane) {
+                             bool replayed, int lane, int capped_walks = -1) {
   const int n = a.n;
   int capped = 0;
   double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
   for (int w = lane; w < n; w += 32) {
-    capped += cur[w] >= 0;
+    if (cur) capped += cur[w] >= 0;
     const double sv = tot[w];
     lo = fmin(lo, sv);
     hi = fmax(hi, sv);
     if (a.o.samples) a.o.samples[job * a.o.samples_stride + w] = sv;
   }
-  capped = warp_sum(capped);
+  capped = cur ? warp_sum(capped) : capped_walks;
   for (int o = 16; o > 0; o >>= 1) {
     lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
     hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
@@ -692,6 +692,370 @@ __global__ void __launch_bounds__(32) mc_serial_kernel(EngineArgs a) {
   }
 }
 
+// ===========================================================================
+// mc_walk_kernel: the demand engine for n <= kSmemWalks walks per application
+// (larger n: mc_engine_kernel above).
+//
+// Walk membership is one bitset per unit in shared memory (bit w set = walk w
+// sits on the unit).  A unit visit extracts its members in ascending walk
+// order (list position = rank = draw index inside the reference's
+// choice()/random() calls), clears the bitset, draws, and moves every member
+// by setting its bit in the successor's bitset -- a walk entering a later
+// unit of the same step is visited again in that step, exactly as the
+// reference's `cur == ui` test at visit time does (estimator.py:343-353).
+//
+// The visit's stream segment is wb words of 32-bit bounded halves (A draws
+// for ranks 0..mA-1, then B draws), then m words of random(m).  For duration
+// units (the common case) lane l owns a contiguous run of bounded words: word
+// j holds the draws of ranks 2j+pin and 2j+pin+1, whose uniforms are words
+// wb+2j+pin and wb+2j+pin+1, so a lane walks two LCG cursors forward in
+// lock-step with its neighbours (one jump each per visit, then single
+// steps) and finishes its members in registers.  Uniform -> successor uses
+// integer thresholds ceil(cum * 2^53) against word >> 11, which is exact.
+// LLM units use per-member cursors over the A/B/U groups; own-input units
+// (draw order depends on the drawn inputs) add a counting sort by bucket.
+// ===========================================================================
+constexpr int kWalkUnits = 32;
+constexpr int kWalkWords = kSmemWalks / 32;
+
+struct WalkState {
+  double* tot;       // [kSmemWalks] accumulated remaining demand per walk
+  uint16_t* mem;     // [kSmemWalks] members of the visited unit, ascending
+  uint32_t* bits;    // [kWalkUnits][kWalkWords] walks per unit
+  uint32_t* cnt;     // [counters] histogram / own-input bucket counters
+  uint16_t* ia;      // [kSmemWalks] staged A-draw index per rank (over cnt)
+  uint16_t* ib;      // [kSmemWalks] staged B-draw index per rank
+  double* tmp;       // own-input path (global scratch)
+  uint16_t* bkt;
+  uint16_t* osrt;
+  double* kin;       // [max_pairs] K3 kept inputs / outputs (global scratch)
+  double* kout;
+};
+
+// shared memory per warp: [counters] [tot] [mem] [bitsets]
+__host__ __device__ inline size_t walk_union_bytes(int counters) {
+  const size_t c = size_t(counters) * 4, s = size_t(kSmemWalks) * 4;
+  return align16(c > s ? c : s);
+}
+__host__ __device__ inline size_t walk_smem_bytes(int counters) {
+  return walk_union_bytes(counters) + size_t(kSmemWalks) * 10 +
+         size_t(kWalkUnits) * kWalkWords * 4;
+}
+// global scratch per warp: [own-input arrays] [K3 pairs]
+__host__ __device__ inline size_t walk_gmem_bytes() {
+  return align16(size_t(kSmemWalks) * gmem_walk_bytes<uint16_t>());
+}
+
+// the threshold form of searchsorted(cum, u, "right") for u = k * 2^-53
+struct SuccTab {
+  uint64_t t0, t1, t2;
+  int n0, n1, n2, n3, ns;
+  __device__ __forceinline__ void load(const EngineArgs& a, const UnitDesc& d) {
+    const double* cum = a.b.succ_cum + d.succ_off;
+    const int32_t* nxt = a.b.succ_nxt + d.succ_off;
+    ns = d.succ_len;
+    constexpr double k53 = 9007199254740992.0;
+    constexpr uint64_t never = 1ull << 54;          // above every k < 2^53
+    t0 = ns > 0 ? __double2ull_ru(__ldg(cum) * k53) : never;
+    t1 = ns > 1 ? __double2ull_ru(__ldg(cum + 1) * k53) : never;
+    t2 = ns > 2 ? __double2ull_ru(__ldg(cum + 2) * k53) : never;
+    n0 = __ldg(nxt);
+    n1 = ns > 0 ? __ldg(nxt + 1) : -1;
+    n2 = ns > 1 ? __ldg(nxt + 2) : -1;
+    n3 = ns > 2 ? __ldg(nxt + 3) : -1;
+  }
+  // successor of the uniform carried by a raw 64-bit word
+  __device__ __forceinline__ int next(const EngineArgs& a, const UnitDesc& d, uint64_t w) const {
+    const uint64_t k = w >> 11;
+    if (ns > 3) return next_unit(a, d, u53_double(w));
+    return k < t0 ? n0 : k < t1 ? n1 : k < t2 ? n2 : n3;
+  }
+};
+
+__device__ __forceinline__ void arrive(const WalkState& ws, uint32_t w, int v, unsigned& targets) {
+  if (v >= 0) {
+    atomicOr(ws.bits + v * kWalkWords + (w >> 5), 1u << (w & 31));
+    targets |= 1u << v;
+  }
+}
+
+// members of unit u in ascending walk order -> ws.mem; clears the bitset
+__device__ __forceinline__ uint32_t take_members(const WalkState& ws, int u, int lane) {
+  uint32_t* bu = ws.bits + u * kWalkWords;
+  // kSmemWalks = 512: one 16-bit slice per lane
+  uint32_t x = (bu[lane >> 1] >> ((lane & 1) << 4)) & 0xffffu;
+  const uint32_t c = __popc(x);
+  const uint32_t incl = warp_incl_scan(c, lane);
+  uint32_t o = incl - c;
+  while (x) {
+    const int b = __ffs(x) - 1;
+    x &= x - 1;
+    ws.mem[o++] = uint16_t(lane * 16 + b);
+  }
+  __syncwarp();
+  if (lane < kWalkWords) bu[lane] = 0u;
+  __syncwarp();
+  return __shfl_sync(kFull, incl, 31);
+}
+
+// per-application stride constants: lane l starts one stride before word l
+// of a visit's segment (state A'_l s + cl) and advances 32 words at a time
+struct LaneConst {
+  U128 cl;     // K_l * inc
+  U128 c32;    // G_32 * inc
+};
+
+__device__ __forceinline__ LaneConst lane_const(const uint64_t* jt, const U128& inc, int lane) {
+  const ulonglong2* l2 = reinterpret_cast<const ulonglong2*>(jt) + 2 * 2048;
+  const ulonglong2 k = __ldg(l2 + 2 * lane + 1), g32 = __ldg(l2 + 2 * 32 + 1);
+  LaneConst c;
+  c.cl = mul128(U128{k.x, k.y}, inc);
+  c.c32 = mul128(U128{g32.x, g32.y}, inc);
+  return c;
+}
+
+// a unit visit without own-input sampling: lane l decodes words l, l+32, ...
+// of the segment [wb bounded words | m uniforms]; bounded halves stage the
+// draw indices per rank, the uniform of rank k then adds the stage time and
+// moves the walk
+__device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Pools& pl,
+                              const WalkState& ws, uint32_t m, Stream& g, const LaneConst& lc,
+                              unsigned& targets, int lane) {
+  const bool llm = d.flags & F_LLM;
+  SuccTab sc;
+  sc.load(a, d);
+  const uint32_t mA = pl.pa > 1 ? m : 0u;
+  const uint32_t C = mA + ((llm && pl.pb > 1) ? m : 0u);
+  const uint32_t pin = g.pend ? 1u : 0u;
+  const uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
+  const uint32_t W = wb + m;
+  const ulonglong2 ap =
+      __ldg(reinterpret_cast<const ulonglong2*>(a.b.jump) + 2 * (2048 + lane));
+  U128 st = add128(mul128(g.s, U128{ap.x, ap.y}), lc.cl);   // one stride before word lane
+  bool rej = false;
+  uint32_t pend_hi = 0;
+  uint32_t q = lane;
+  for (; q < wb; q += 32) {                       // bounded halves -> draw indices
+    st = pcg_stride32(st, lc.c32);
+    const uint64_t wd = pcg_out(st);
+    const uint32_t R = 2u * q + pin;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t r = R + t, h = t ? uint32_t(wd >> 32) : uint32_t(wd);
+      if (r < mA) ws.ia[r] = uint16_t(lemire(h, uint32_t(pl.pa), rej));
+      else if (r < C) ws.ib[r - mA] = uint16_t(lemire(h, uint32_t(pl.pb), rej));
+      else pend_hi = h;
+    }
+  }
+  if (pin && C && lane == 0) {                    // half 0 is numpy's buffered half
+    if (mA) ws.ia[0] = uint16_t(lemire(g.pv, uint32_t(pl.pa), rej));
+    else ws.ib[0] = uint16_t(lemire(g.pv, uint32_t(pl.pb), rej));
+  }
+  __syncwarp();
+  const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
+  const bool hb = C > mA;
+  for (; q < W; q += 32) {                        // random(m): stage time + successor
+    st = pcg_stride32(st, lc.c32);
+    const uint32_t k = q - wb;
+    const int v = sc.next(a, d, pcg_out(st));
+    const uint32_t w = ws.mem[k];
+    double t = pl.A[mA ? ws.ia[k] : 0u];
+    if (llm) t = dadd(__ddiv_rn(t, pre), __ddiv_rn(pl.B[hb ? ws.ib[k] : 0u], dec));
+    ws.tot[w] = dadd(ws.tot[w], t);
+    arrive(ws, w, v, targets);
+  }
+  if (__any_sync(kFull, rej)) return false;
+  const unsigned last = (W - 1) & 31u;            // it decoded word W - 1
+  g.s.lo = __shfl_sync(kFull, st.lo, last);
+  g.s.hi = __shfl_sync(kFull, st.hi, last);
+  const uint32_t pv = __shfl_sync(kFull, pend_hi, (wb - 1) & 31u);
+  if (C) {
+    g.pend = ((pin + C) & 1u) != 0;
+    if (g.pend) g.pv = pv;
+  }
+  __syncwarp();
+  return true;
+}
+
+// own-input LLM unit: outputs drawn per input bucket, buckets ascending,
+// walks in order within a bucket (estimator.py:275-283)
+__device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& pl,
+                          const WalkState& ws, uint32_t m, Stream& g, unsigned& targets,
+                          int lane) {
+  const uint64_t* jt = a.b.jump;
+  const unsigned lt = lanemask_lt();
+  SuccTab sc;
+  sc.load(a, d);
+  const uint32_t per = (m + 31) >> 5;
+  const uint32_t k0 = min(lane * per, m), k1 = min(k0 + per, m);
+  const uint32_t c1 = pl.pa > 1 ? m : 0u;
+  const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
+  bool rej = false;
+  Cursor ca{g.s, 0xffffffffu, 0}, cb{g.s, 0xffffffffu, 0};
+  const int K = d.ib_k;
+  uint32_t* cnt = ws.cnt;
+  uint32_t* start = ws.cnt + a.max_unit_k;
+  uint32_t* effo = ws.cnt + 2 * a.max_unit_k;
+  for (int b = lane; b < K; b += 32) cnt[b] = 0;
+  __syncwarp();
+  for (uint32_t k = k0; k < k1; ++k) {
+    const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(ca, jt, g, k), uint32_t(pl.pa), rej) : 0u;
+    const double iv = pl.A[ia];
+    ws.tmp[k] = iv;
+    const int bb = bucket_of(iv, d.ib_lo, d.ib_hi, K);
+    ws.bkt[k] = uint16_t(bb);
+    atomicAdd(&cnt[bb], 1u);
+  }
+  __syncwarp();
+  const int perb = (K + 31) >> 5;
+  uint32_t la = 0, le = 0;
+  for (int q = 0; q < perb; ++q) {
+    const int bb = lane * perb + q;
+    if (bb < K) {
+      const int pln = a.b.pool_len[d.pool_off + bb];
+      const int P = pln > 0 ? pln : pl.pb;
+      la += cnt[bb];
+      le += P > 1 ? cnt[bb] : 0u;
+    }
+  }
+  const uint32_t ia_incl = warp_incl_scan(la, lane), ie_incl = warp_incl_scan(le, lane);
+  const uint32_t eff_total = __shfl_sync(kFull, ie_incl, 31);
+  uint32_t ra = ia_incl - la, re = ie_incl - le;
+  __syncwarp();
+  for (int q = 0; q < perb; ++q) {
+    const int bb = lane * perb + q;
+    if (bb < K) {
+      const int pln = a.b.pool_len[d.pool_off + bb];
+      const int P = pln > 0 ? pln : pl.pb;
+      const uint32_t c = cnt[bb];
+      start[bb] = ra;
+      effo[bb] = re;
+      cnt[bb] = ra;
+      ra += c;
+      re += P > 1 ? c : 0u;
+    }
+  }
+  __syncwarp();
+  for (uint32_t base = 0; base < m; base += 32) {   // stable counting sort by bucket
+    const uint32_t k = base + lane;
+    const bool valid = k < m;
+    const int bb = valid ? int(ws.bkt[k]) : (0x10000 + lane);
+    const unsigned peers = __match_any_sync(kFull, bb);
+    uint32_t dest = 0;
+    if (valid) dest = cnt[bb];
+    __syncwarp();
+    if (valid && (__ffs(peers) - 1) == lane) cnt[bb] = dest + __popc(peers);
+    __syncwarp();
+    if (valid) ws.osrt[dest + __popc(peers & lt)] = uint16_t(k);
+  }
+  __syncwarp();
+  for (uint32_t j = k0; j < k1; ++j) {
+    const uint32_t k = ws.osrt[j];
+    const int bb = ws.bkt[k];
+    const int pln = a.b.pool_len[d.pool_off + bb];
+    const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
+    const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
+    const uint32_t pos = c1 + effo[bb] + (j - start[bb]);
+    const uint32_t ob = P > 1 ? lemire(cursor_half(cb, jt, g, pos), P, rej) : 0u;
+    ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], pre), __ddiv_rn(pool[ob], dec));
+  }
+  if (__any_sync(kFull, rej)) return false;
+  const uint32_t C = c1 + eff_total;
+  const uint32_t F = C == 0 ? 0u : C - (g.pend ? 1u : 0u);
+  const uint32_t words = (F + 1) >> 1;
+  close_group(g, C, ca, cb);
+  __syncwarp();
+  Cursor cd{g.s, 0xffffffffu, 0};
+  for (uint32_t k = k0; k < k1; ++k) {
+    const uint64_t uw = cursor_word(cd, jt, g.inc, words + k);
+    const uint32_t w = ws.mem[k];
+    arrive(ws, w, sc.next(a, d, uw), targets);
+    ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
+  }
+  const unsigned last_lane = (m - 1) / per;
+  g.s.lo = __shfl_sync(kFull, cd.st.lo, last_lane);
+  g.s.hi = __shfl_sync(kFull, cd.st.hi, last_lane);
+  __syncwarp();
+  return true;
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 6) mc_walk_kernel(EngineArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int n = a.n;
+  unsigned char* sb = smem + walk_smem_bytes(a.counters) * wib;
+  const int64_t gwarp = int64_t(blockIdx.x) * kWarps + wib;
+  unsigned char* gs =
+      reinterpret_cast<unsigned char*>(a.scratch) + size_t(gwarp) * a.scratch_per_warp;
+  WalkState ws;
+  ws.cnt = reinterpret_cast<uint32_t*>(sb);
+  ws.ia = reinterpret_cast<uint16_t*>(sb);
+  ws.ib = ws.ia + kSmemWalks;
+  ws.tot = reinterpret_cast<double*>(sb + walk_union_bytes(a.counters));
+  ws.mem = reinterpret_cast<uint16_t*>(ws.tot + kSmemWalks);
+  ws.bits = reinterpret_cast<uint32_t*>(ws.mem + kSmemWalks);
+  ws.tmp = reinterpret_cast<double*>(gs);
+  ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + kSmemWalks);
+  ws.osrt = ws.bkt + kSmemWalks;
+  ws.kin = reinterpret_cast<double*>(gs + walk_gmem_bytes());
+  ws.kout = ws.kin + a.max_pairs;
+  const int64_t stride = int64_t(gridDim.x) * kWarps;
+  for (int64_t job = gwarp; job < a.n_jobs; job += stride) {
+    const int gi = a.j.graph[job];
+    const int gbase = a.b.graph_base[gi];
+    const int gn = a.b.graph_n[gi];
+    const int u0 = a.j.unit[job];
+    Stream g;
+    pcg_seed(a.j.seed[job], g.s, g.inc);
+    g.pend = false;
+    g.pv = 0;
+    Pools ovp{nullptr, 0, nullptr, 0};
+    bool conditioned = false;
+    int obs_up;
+    double obs[3];
+    job_obs(a, job, obs_up, obs);
+    const bool has_ov =
+        condition(a, gbase, u0, obs_up, obs, ws.kin, ws.kout, ovp, conditioned, lane);
+    const LaneConst lc = lane_const(a.b.jump, g.inc, lane);
+    for (int i = lane; i < gn * kWalkWords; i += 32) {
+      const int u = i / kWalkWords, wi = i - u * kWalkWords;
+      const int rem = n - 32 * wi;
+      ws.bits[i] = (u != u0 || rem <= 0) ? 0u : (rem >= 32 ? 0xffffffffu : (1u << rem) - 1u);
+    }
+    for (int w = lane; w < n; w += 32) ws.tot[w] = 0.0;
+    __syncwarp();
+    unsigned pending = 1u << u0;                 // units holding walks
+    bool ok = true;
+    for (int step = 0; step < a.cap && ok && pending; ++step) {
+      unsigned occ = pending;                    // frozen occupied set of the step
+      while (occ && ok) {
+        const int u = __ffs(occ) - 1;
+        occ &= occ - 1;
+        const uint32_t m = take_members(ws, u, lane);
+        pending &= ~(1u << u);
+        const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u];
+        const bool ov = has_ov && u == u0;
+        const Pools pl = pools_for(a, d, ov, ovp);
+        unsigned targets = 0;
+        if ((d.flags & F_LLM) && (d.flags & F_OWN) && !ov)
+          ok = visit_own(a, d, pl, ws, m, g, targets, lane);
+        else
+          ok = visit_strided(a, d, pl, ws, m, g, lc, targets, lane);
+        pending |= __reduce_or_sync(kFull, targets);
+      }
+    }
+    if (!ok) {                     // Lemire rejection: leave it to mc_serial_kernel
+      if (lane == 0) a.serial_list[atomicAdd(a.serial_count, 1)] = int32_t(job);
+      __syncwarp();
+      continue;
+    }
+    int capped = 0;
+    for (int i = lane; i < gn * kWalkWords; i += 32) capped += __popc(ws.bits[i]);
+    capped = warp_sum(capped);
+    write_result(a, job, ws.tot, nullptr, ws.cnt, conditioned, has_ov, false, lane, capped);
+  }
+}
+
 }  // namespace pdg
 
 using namespace pdg;
@@ -706,7 +1070,9 @@ static size_t walk_scratch(int n) {
   const size_t own = align16(nw * (si ? gmem_walk_bytes<uint16_t>() : gmem_walk_bytes<uint32_t>()));
   const size_t fast = smem_part + own;
   const size_t serial = serial_bytes(int(nw));
-  return fast > serial ? fast : serial;
+  const size_t walk = n <= kSmemWalks ? walk_gmem_bytes() : 0;
+  const size_t r = fast > serial ? fast : serial;
+  return r > walk ? r : walk;
 }
 
 static size_t scratch_per_warp(int n, int max_pairs) {
@@ -783,10 +1149,10 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
     kern<<<unsigned(nb), kWarps * 32, smem, st>>>(a);
     return PDG_OK;
   };
-  if (small_idx(n_samples)) {
-    const size_t smem =
-        size_t(kWarps) * (cnt_bytes + (sm ? size_t(kSmemWalks) * smem_walk_bytes<uint16_t>() : 0));
-    if (int r = launch(mc_engine_kernel<uint16_t>, smem)) return r;
+  if (sm) {
+    if (int r = launch(mc_walk_kernel, size_t(kWarps) * walk_smem_bytes(a.counters))) return r;
+  } else if (small_idx(n_samples)) {
+    if (int r = launch(mc_engine_kernel<uint16_t>, size_t(kWarps) * cnt_bytes)) return r;
   } else {
     if (int r = launch(mc_engine_kernel<uint32_t>, size_t(kWarps) * cnt_bytes)) return r;
   }

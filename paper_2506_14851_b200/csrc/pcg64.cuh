@@ -45,6 +45,14 @@ __device__ __forceinline__ U128 pcg_step(U128 s, U128 inc) {
   return add128(mul128(s, U128{kMultLo, kMultHi}), inc);
 }
 
+// 32 steps at once: s -> A_32 * s + c32 with c32 = G_32 * inc (per stream)
+constexpr uint64_t kA32Lo = 0x82B631BA6B261781ull;
+constexpr uint64_t kA32Hi = 0x2C82901AD1CB0CD1ull;
+
+__device__ __forceinline__ U128 pcg_stride32(U128 s, U128 c32) {
+  return add128(mul128(s, U128{kA32Lo, kA32Hi}), c32);
+}
+
 // Jump tables: jt[(level*1024 + j)*4 + {A.lo, A.hi, G.lo, G.hi}];
 // after j steps: s -> A_j * s + inc * G_j.  Level 1 holds j = 1024*q.
 __device__ __forceinline__ U128 jump_apply(const uint64_t* __restrict__ jt, int level,

@@ -373,17 +373,32 @@ _M128 = (1 << 128) - 1
 
 
 def jump_tables() -> np.ndarray:
-    """uint64 [2, 1024, 4]: level 0 = j in [0,1024), level 1 = j = 1024*q.
-    Entry = (A.lo, A.hi, G.lo, G.hi)."""
-    out = np.zeros((2, 1024, 4), dtype=np.uint64)
+    """uint64 [3, 1024, 4]: level 0 = j in [0,1024), level 1 = j = 1024*q,
+    entry = (A.lo, A.hi, G.lo, G.hi).  Level 2 drives the engine's strided
+    decode (lane l reads words l, l+32, ... of a visit's stream segment):
+    entry l < 32 = (A'_l, K_l) with A'_l = A_32^-1 A_{l+1} and
+    K_l = A_32^-1 (G_{l+1} - G_32), so that the state one stride before word l
+    is A'_l s + K_l inc; entry 32 = (A_32, G_32)."""
+    out = np.zeros((3, 1024, 4), dtype=np.uint64)
+    lo = lambda x: x & (2**64 - 1)  # noqa: E731
     A, G = 1, 0
     for j in range(1024):
-        out[0, j] = [A & (2**64 - 1), A >> 64, G & (2**64 - 1), G >> 64]
+        out[0, j] = [lo(A), A >> 64, lo(G), G >> 64]
         A, G = (A * PCG_MULT) & _M128, (G * PCG_MULT + 1) & _M128
     A1024, G1024 = A, G       # one step of level 1
     A, G = 1, 0
     for q in range(1024):
-        out[1, q] = [A & (2**64 - 1), A >> 64, G & (2**64 - 1), G >> 64]
+        out[1, q] = [lo(A), A >> 64, lo(G), G >> 64]
         # compose: (A,G) o (A1024,G1024): s -> A1024*(A*s + inc*G) + inc*G1024
         A, G = (A1024 * A) & _M128, (A1024 * G + G1024) & _M128
+    a32 = int(out[0, 32, 0]) | (int(out[0, 32, 1]) << 64)
+    g32 = int(out[0, 32, 2]) | (int(out[0, 32, 3]) << 64)
+    inv = pow(a32, -1, 1 << 128)
+    for lane in range(32):
+        al = int(out[0, lane + 1, 0]) | (int(out[0, lane + 1, 1]) << 64)
+        gl = int(out[0, lane + 1, 2]) | (int(out[0, lane + 1, 3]) << 64)
+        ap = (inv * al) & _M128
+        kp = (inv * (gl - g32)) & _M128
+        out[2, lane] = [lo(ap), ap >> 64, lo(kp), kp >> 64]
+    out[2, 32] = [lo(a32), a32 >> 64, lo(g32), g32 >> 64]
     return out

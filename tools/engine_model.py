@@ -213,3 +213,86 @@ def walk(g, current, override, n, seed, cap, tables, prefill=1e4, decode=50.0):
             st.advance(m)
             cur[mem] = nxt[np.searchsorted(cum, uu, side="right")] if len(cum) else -1
     return tot, int((cur >= 0).sum())
+
+
+
+def walk_units(g, current, override, n, seed, cap, tables, prefill=1e4, decode=50.0):
+    """Model of the kernel's per-visit word decode (engine.cu visit_words):
+    a unit visit's stream segment -- wb words of bounded-halves, then m
+    uniforms -- is cut into contiguous word ranges, each decoded from the
+    visit's base state by position.  The occupied set of the next step is
+    tracked as a pending mask (arrivals after a unit's visit).  Own-input
+    units are not modelled (returns None)."""
+    order = sorted(g.units)
+    pos = {u: i for i, u in enumerate(order)}
+    units = [g.units[u] for u in order]
+    s0, inc = seed_state(seed)
+    A, G = tables
+    st = {"base": s0, "pend": 0, "pv": 0}
+
+    def word(q):
+        j = q + 1
+        return out64((A[j] * st["base"] + inc * G[j]) & M128)
+
+    cur = np.full(n, pos[current], dtype=np.int64)
+    tot = np.zeros(n)
+    pending = {pos[current]}
+    for _ in range(cap):
+        occ = sorted(pending)
+        assert occ == sorted(set(int(c) for c in cur if c >= 0))
+        if not occ:
+            break
+        for ui in occ:
+            mem = np.flatnonzero(cur == ui)
+            pending.discard(ui)
+            m = len(mem)
+            u = units[ui]
+            ov = override if order[ui] == current else None
+            if u.is_llm:
+                if u.masks.get("output_own_input") and ov is None and u.records:
+                    return None
+                pa = np.asarray(ov.input_vals if ov else u.samples("input"))
+                pb = np.asarray(ov.output_vals if ov else u.samples("output"))
+            else:
+                pa = np.asarray(u.samples("duration"))
+                pb = None
+            mA = m if len(pa) > 1 else 0
+            C = mA + (m if (u.is_llm and len(pb) > 1) else 0)
+            pin = st["pend"]
+            wb = (C - pin + 1) >> 1 if C else 0
+            W = wb + m
+            ia = np.zeros(m, dtype=np.int64)
+            ib = np.zeros(m, dtype=np.int64)
+            pend_hi = None
+            for q in range(wb):
+                wd = word(q)
+                for t, h in enumerate((wd & M32, wd >> 32)):
+                    r = 2 * q + pin + t
+                    if r < mA:
+                        ia[r] = lemire(h, len(pa))
+                    elif r < C:
+                        ib[r - mA] = lemire(h, len(pb))
+                    elif r == C:
+                        pend_hi = h
+            if pin and C:
+                if mA:
+                    ia[0] = lemire(st["pv"], len(pa))
+                else:
+                    ib[0] = lemire(st["pv"], len(pb))
+            t = pa[ia]
+            if u.is_llm:
+                t = t / prefill + pb[ib] / decode
+            tot[mem] += t
+            succ = sorted(u.succ.items())
+            cum = np.cumsum([p for _, p in succ])
+            nx = np.array([pos[s] for s, _ in succ] + [-1])
+            uu = np.array([(word(wb + k) >> 11) * (1.0 / 9007199254740992.0) for k in range(m)])
+            v = nx[np.searchsorted(cum, uu, side="right")] if len(cum) else np.full(m, -1)
+            cur[mem] = v
+            pending |= set(int(x) for x in v if x >= 0)
+            st["base"] = (A[W] * st["base"] + inc * G[W]) & M128
+            if C:
+                st["pend"] = (pin + C) & 1
+                if st["pend"]:
+                    st["pv"] = pend_hi
+    return tot, int((cur >= 0).sum())

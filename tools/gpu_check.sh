@@ -16,7 +16,7 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 2 --ncu \
   > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:mc_engine \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mc_walk|mc_engine" \
   -s 3 -c 1 -o gpurun_out/engine -f python bench.py --steps 1 --warmup 2 --ncu \
   > gpurun_out/ncu_engine.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gittins \
