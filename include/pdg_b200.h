@@ -135,6 +135,8 @@ typedef struct {
   const void* pairs;              /* K3 joined records                      */
   const uint64_t* jump;           /* PCG64 jump tables [3][1024][4]         */
   double prefill_rate, decode_rate; /* RateProfile (pdgraph.py:282-291)     */
+  const uint64_t* succ_thr;       /* ceil(succ_cum * 2^53): integer cum <= u */
+  int32_t max_units;              /* max over graph_n                        */
 } pdg_graph_bank;
 
 typedef struct {

@@ -71,6 +71,7 @@ struct EngineArgs {
   size_t scratch_per_warp;
   int32_t* serial_list;   // [n_jobs] apps left to mc_serial_kernel
   int32_t* serial_count;  // [1]
+  int32_t* job_next;      // [1] dynamic job counter (mc_walk_kernel)
 };
 
 // distributions.py:107-118 with (lo, hi = last bucket edge, k)
@@ -715,7 +716,6 @@ __global__ void __launch_bounds__(32) mc_serial_kernel(EngineArgs a) {
 // LLM units use per-member cursors over the A/B/U groups; own-input units
 // (draw order depends on the drawn inputs) add a counting sort by bucket.
 // ===========================================================================
-constexpr int kWalkUnits = 32;
 constexpr int kWalkWords = kSmemWalks / 32;
 
 struct WalkState {
@@ -732,14 +732,14 @@ struct WalkState {
   double* kout;
 };
 
-// shared memory per warp: [counters] [tot] [mem] [bitsets]
+// shared memory per warp: [counters | LLM staging] [tot] [mem] [bitsets of
+// max_units units]
 __host__ __device__ inline size_t walk_union_bytes(int counters) {
   const size_t c = size_t(counters) * 4, s = size_t(kSmemWalks) * 4;
   return align16(c > s ? c : s);
 }
-__host__ __device__ inline size_t walk_smem_bytes(int counters) {
-  return walk_union_bytes(counters) + size_t(kSmemWalks) * 10 +
-         size_t(kWalkUnits) * kWalkWords * 4;
+__host__ __device__ inline size_t walk_smem_bytes(int counters, int units) {
+  return walk_union_bytes(counters) + size_t(kSmemWalks) * 10 + size_t(units) * kWalkWords * 4;
 }
 // global scratch per warp: [own-input arrays] [K3 pairs]
 __host__ __device__ inline size_t walk_gmem_bytes() {
@@ -751,14 +751,13 @@ struct SuccTab {
   uint64_t t0, t1, t2;
   int n0, n1, n2, n3, ns;
   __device__ __forceinline__ void load(const EngineArgs& a, const UnitDesc& d) {
-    const double* cum = a.b.succ_cum + d.succ_off;
+    const uint64_t* thr = a.b.succ_thr + d.succ_off;
     const int32_t* nxt = a.b.succ_nxt + d.succ_off;
     ns = d.succ_len;
-    constexpr double k53 = 9007199254740992.0;
     constexpr uint64_t never = 1ull << 54;          // above every k < 2^53
-    t0 = ns > 0 ? __double2ull_ru(__ldg(cum) * k53) : never;
-    t1 = ns > 1 ? __double2ull_ru(__ldg(cum + 1) * k53) : never;
-    t2 = ns > 2 ? __double2ull_ru(__ldg(cum + 2) * k53) : never;
+    t0 = ns > 0 ? __ldg(thr) : never;
+    t1 = ns > 1 ? __ldg(thr + 1) : never;
+    t2 = ns > 2 ? __ldg(thr + 2) : never;
     n0 = __ldg(nxt);
     n1 = ns > 0 ? __ldg(nxt + 1) : -1;
     n2 = ns > 1 ? __ldg(nxt + 2) : -1;
@@ -854,15 +853,27 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Pool
   __syncwarp();
   const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
   const bool hb = C > mA;
-  for (; q < W; q += 32) {                        // random(m): stage time + successor
+  // random(m): stage time + successor; the pool loads of the next word are
+  // issued before the current word is finished
+  uint32_t k = q - wb;
+  double xa = 0.0, xb = 0.0;
+  if (q < W) {
+    xa = pl.A[mA ? ws.ia[k] : 0u];
+    if (llm) xb = pl.B[hb ? ws.ib[k] : 0u];
+  }
+  for (; q < W; q += 32) {
+    const double ca = xa, cb = xb;
+    if (q + 32 < W) {
+      xa = pl.A[mA ? ws.ia[k + 32] : 0u];
+      if (llm) xb = pl.B[hb ? ws.ib[k + 32] : 0u];
+    }
     st = pcg_stride32(st, lc.c32);
-    const uint32_t k = q - wb;
     const int v = sc.next(a, d, pcg_out(st));
     const uint32_t w = ws.mem[k];
-    double t = pl.A[mA ? ws.ia[k] : 0u];
-    if (llm) t = dadd(__ddiv_rn(t, pre), __ddiv_rn(pl.B[hb ? ws.ib[k] : 0u], dec));
+    const double t = llm ? dadd(__ddiv_rn(ca, pre), __ddiv_rn(cb, dec)) : ca;
     ws.tot[w] = dadd(ws.tot[w], t);
     arrive(ws, w, v, targets);
+    k += 32;
   }
   if (__any_sync(kFull, rej)) return false;
   const unsigned last = (W - 1) & 31u;            // it decoded word W - 1
@@ -983,7 +994,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) mc_walk_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;
-  unsigned char* sb = smem + walk_smem_bytes(a.counters) * wib;
+  unsigned char* sb = smem + walk_smem_bytes(a.counters, a.b.max_units) * wib;
   const int64_t gwarp = int64_t(blockIdx.x) * kWarps + wib;
   unsigned char* gs =
       reinterpret_cast<unsigned char*>(a.scratch) + size_t(gwarp) * a.scratch_per_warp;
@@ -999,8 +1010,11 @@ __global__ void __launch_bounds__(kWarps * 32, 6) mc_walk_kernel(EngineArgs a) {
   ws.osrt = ws.bkt + kSmemWalks;
   ws.kin = reinterpret_cast<double*>(gs + walk_gmem_bytes());
   ws.kout = ws.kin + a.max_pairs;
-  const int64_t stride = int64_t(gridDim.x) * kWarps;
-  for (int64_t job = gwarp; job < a.n_jobs; job += stride) {
+  for (;;) {
+    int job = 0;
+    if (lane == 0) job = atomicAdd(a.job_next, 1);
+    job = __shfl_sync(kFull, job, 0);
+    if (job >= a.n_jobs) break;
     const int gi = a.j.graph[job];
     const int gbase = a.b.graph_base[gi];
     const int gn = a.b.graph_n[gi];
@@ -1125,9 +1139,10 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   a.scratch_per_warp = scratch_per_warp(n_samples, max_pairs);
   char* tail = static_cast<char*>(scratch) + a.scratch_per_warp * size_t(grid_warps);
   a.serial_count = reinterpret_cast<int32_t*>(tail);
+  a.job_next = reinterpret_cast<int32_t*>(tail + 4);
   a.serial_list = reinterpret_cast<int32_t*>(tail + 256);
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(a.serial_count, 0, sizeof(int32_t), st);
+  cudaError_t e = cudaMemsetAsync(a.serial_count, 0, 2 * sizeof(int32_t), st);
   if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(serial_count)");
   const bool sm = n_samples <= kSmemWalks;
   const size_t cnt_bytes = align16(size_t(a.counters) * 4);
@@ -1150,7 +1165,8 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
     return PDG_OK;
   };
   if (sm) {
-    if (int r = launch(mc_walk_kernel, size_t(kWarps) * walk_smem_bytes(a.counters))) return r;
+    const int mu = bank->max_units < 1 ? 1 : bank->max_units;
+    if (int r = launch(mc_walk_kernel, size_t(kWarps) * walk_smem_bytes(a.counters, mu))) return r;
   } else if (small_idx(n_samples)) {
     if (int r = launch(mc_engine_kernel<uint16_t>, size_t(kWarps) * cnt_bytes)) return r;
   } else {

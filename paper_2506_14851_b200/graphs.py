@@ -351,7 +351,12 @@ class GraphBank:
         self.pool_off = t(pools_off, np.int32)
         self.pool_len = t(pools_len, np.int32)
         self.succ_cum = t(succ_cum, np.float64)
+        # integer form of `cum <= u` for u = k * 2^-53: k >= ceil(cum * 2^53)
+        # (exact: scaling by 2^53 and ceil are exact for cum in [0, 2))
+        cum = np.asarray(succ_cum, dtype=np.float64)
+        self.succ_thr = t(np.ceil(cum * 2.0 ** 53).astype(np.uint64).view(np.int64), np.int64)
         self.succ_nxt = t(succ_nxt, np.int32)
+        self.max_units = int(np.max(gn)) if len(gn) else 1
         ca = np.array(conds, dtype=COND_DTYPE) if len(conds) else np.zeros(1, COND_DTYPE)
         pa = np.array(pairs, dtype=PAIR_DTYPE) if len(pairs) else np.zeros(1, PAIR_DTYPE)
         self.host_conds = ca
