@@ -725,6 +725,7 @@ struct WalkState {
   uint32_t* cnt;     // [counters] histogram / own-input bucket counters
   uint16_t* ia;      // [kSmemWalks] staged A-draw index per rank (over cnt)
   uint16_t* ib;      // [kSmemWalks] staged B-draw index per rank
+  struct UnitCache* uc;  // [max_units] the application's unit descriptors
   double* tmp;       // own-input path (global scratch)
   uint16_t* bkt;
   uint16_t* osrt;
@@ -739,7 +740,8 @@ __host__ __device__ inline size_t walk_union_bytes(int counters) {
   return align16(c > s ? c : s);
 }
 __host__ __device__ inline size_t walk_smem_bytes(int counters, int units) {
-  return walk_union_bytes(counters) + size_t(kSmemWalks) * 10 + size_t(units) * kWalkWords * 4;
+  return walk_union_bytes(counters) + size_t(kSmemWalks) * 10 + size_t(units) * kWalkWords * 4 +
+         size_t(units) * 112;
 }
 // global scratch per warp: [own-input arrays] [K3 pairs]
 __host__ __device__ inline size_t walk_gmem_bytes() {
@@ -770,6 +772,30 @@ struct SuccTab {
     return k < t0 ? n0 : k < t1 ? n1 : k < t2 ? n2 : n3;
   }
 };
+
+// an application's unit, staged in shared memory once per application
+struct __align__(16) UnitCache {
+  UnitDesc d;
+  uint64_t t0, t1, t2;
+  int32_t ns;
+  int8_t n[4];
+  int32_t pad[2];
+};
+static_assert(sizeof(UnitCache) == 112, "unit cache layout");
+
+__device__ __forceinline__ SuccTab succ_of(const UnitCache& c) {
+  SuccTab s;
+  s.t0 = c.t0;
+  s.t1 = c.t1;
+  s.t2 = c.t2;
+  s.ns = c.ns;
+  const char4 n = *reinterpret_cast<const char4*>(c.n);
+  s.n0 = n.x;
+  s.n1 = n.y;
+  s.n2 = n.z;
+  s.n3 = n.w;
+  return s;
+}
 
 __device__ __forceinline__ void arrive(const WalkState& ws, uint32_t w, int v, unsigned& targets) {
   if (v >= 0) {
@@ -817,12 +843,11 @@ __device__ __forceinline__ LaneConst lane_const(const uint64_t* jt, const U128& 
 // of the segment [wb bounded words | m uniforms]; bounded halves stage the
 // draw indices per rank, the uniform of rank k then adds the stage time and
 // moves the walk
-__device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Pools& pl,
-                              const WalkState& ws, uint32_t m, Stream& g, const LaneConst& lc,
-                              unsigned& targets, int lane) {
-  const bool llm = d.flags & F_LLM;
-  SuccTab sc;
-  sc.load(a, d);
+template <bool LLM>
+__device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const SuccTab& sc,
+                              const Pools& pl, const WalkState& ws, uint32_t m, Stream& g,
+                              const LaneConst& lc, unsigned& targets, int lane) {
+  constexpr bool llm = LLM;
   const uint32_t mA = pl.pa > 1 ? m : 0u;
   const uint32_t C = mA + ((llm && pl.pb > 1) ? m : 0u);
   const uint32_t pin = g.pend ? 1u : 0u;
@@ -838,12 +863,18 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Pool
     st = pcg_stride32(st, lc.c32);
     const uint64_t wd = pcg_out(st);
     const uint32_t R = 2u * q + pin;
+    if (!LLM) {                                   // every low half is an A draw
+      ws.ia[R] = uint16_t(lemire(uint32_t(wd), uint32_t(pl.pa), rej));
+      if (R + 1 < mA) ws.ia[R + 1] = uint16_t(lemire(uint32_t(wd >> 32), uint32_t(pl.pa), rej));
+      else pend_hi = uint32_t(wd >> 32);
+    } else {
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const uint32_t r = R + t, h = t ? uint32_t(wd >> 32) : uint32_t(wd);
-      if (r < mA) ws.ia[r] = uint16_t(lemire(h, uint32_t(pl.pa), rej));
-      else if (r < C) ws.ib[r - mA] = uint16_t(lemire(h, uint32_t(pl.pb), rej));
-      else pend_hi = h;
+      for (int t = 0; t < 2; ++t) {
+        const uint32_t r = R + t, h = t ? uint32_t(wd >> 32) : uint32_t(wd);
+        if (r < mA) ws.ia[r] = uint16_t(lemire(h, uint32_t(pl.pa), rej));
+        else if (r < C) ws.ib[r - mA] = uint16_t(lemire(h, uint32_t(pl.pb), rej));
+        else pend_hi = h;
+      }
     }
   }
   if (pin && C && lane == 0) {                    // half 0 is numpy's buffered half
@@ -855,22 +886,20 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Pool
   const bool hb = C > mA;
   // random(m): stage time + successor; the pool loads of the next word are
   // issued before the current word is finished
+  // (reads past the last rank hit the staging area's slack and are clamped
+  // into the pool)
+  const uint32_t la = mA ? uint32_t(pl.pa - 1) : 0u, lb = hb ? uint32_t(pl.pb - 1) : 0u;
   uint32_t k = q - wb;
-  double xa = 0.0, xb = 0.0;
-  if (q < W) {
-    xa = pl.A[mA ? ws.ia[k] : 0u];
-    if (llm) xb = pl.B[hb ? ws.ib[k] : 0u];
-  }
+  double xa = pl.A[min(uint32_t(ws.ia[k]), la)], xb = 0.0;
+  if (LLM) xb = pl.B[min(uint32_t(ws.ib[k]), lb)];
   for (; q < W; q += 32) {
     const double ca = xa, cb = xb;
-    if (q + 32 < W) {
-      xa = pl.A[mA ? ws.ia[k + 32] : 0u];
-      if (llm) xb = pl.B[hb ? ws.ib[k + 32] : 0u];
-    }
+    xa = pl.A[min(uint32_t(ws.ia[k + 32]), la)];
+    if (LLM) xb = pl.B[min(uint32_t(ws.ib[k + 32]), lb)];
     st = pcg_stride32(st, lc.c32);
     const int v = sc.next(a, d, pcg_out(st));
     const uint32_t w = ws.mem[k];
-    const double t = llm ? dadd(__ddiv_rn(ca, pre), __ddiv_rn(cb, dec)) : ca;
+    const double t = LLM ? dadd(__ddiv_rn(ca, pre), __ddiv_rn(cb, dec)) : ca;
     ws.tot[w] = dadd(ws.tot[w], t);
     arrive(ws, w, v, targets);
     k += 32;
@@ -1005,6 +1034,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) mc_walk_kernel(EngineArgs a) {
   ws.tot = reinterpret_cast<double*>(sb + walk_union_bytes(a.counters));
   ws.mem = reinterpret_cast<uint16_t*>(ws.tot + kSmemWalks);
   ws.bits = reinterpret_cast<uint32_t*>(ws.mem + kSmemWalks);
+  ws.uc = reinterpret_cast<UnitCache*>(ws.bits + a.b.max_units * kWalkWords);
   ws.tmp = reinterpret_cast<double*>(gs);
   ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + kSmemWalks);
   ws.osrt = ws.bkt + kSmemWalks;
@@ -1031,6 +1061,20 @@ __global__ void __launch_bounds__(kWarps * 32, 6) mc_walk_kernel(EngineArgs a) {
     const bool has_ov =
         condition(a, gbase, u0, obs_up, obs, ws.kin, ws.kout, ovp, conditioned, lane);
     const LaneConst lc = lane_const(a.b.jump, g.inc, lane);
+    if (lane < gn) {                             // stage the unit descriptors
+      UnitCache c;
+      c.d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + lane];
+      const SuccTab t = [&] { SuccTab x; x.load(a, c.d); return x; }();
+      c.t0 = t.t0;
+      c.t1 = t.t1;
+      c.t2 = t.t2;
+      c.ns = t.ns;
+      c.n[0] = int8_t(t.n0);
+      c.n[1] = int8_t(t.n1);
+      c.n[2] = int8_t(t.n2);
+      c.n[3] = int8_t(t.n3);
+      ws.uc[lane] = c;
+    }
     for (int i = lane; i < gn * kWalkWords; i += 32) {
       const int u = i / kWalkWords, wi = i - u * kWalkWords;
       const int rem = n - 32 * wi;
@@ -1047,14 +1091,16 @@ __global__ void __launch_bounds__(kWarps * 32, 6) mc_walk_kernel(EngineArgs a) {
         occ &= occ - 1;
         const uint32_t m = take_members(ws, u, lane);
         pending &= ~(1u << u);
-        const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u];
+        const UnitDesc d = ws.uc[u].d;
         const bool ov = has_ov && u == u0;
         const Pools pl = pools_for(a, d, ov, ovp);
         unsigned targets = 0;
-        if ((d.flags & F_LLM) && (d.flags & F_OWN) && !ov)
+        if (!(d.flags & F_LLM))
+          ok = visit_strided<false>(a, d, succ_of(ws.uc[u]), pl, ws, m, g, lc, targets, lane);
+        else if ((d.flags & F_OWN) && !ov)
           ok = visit_own(a, d, pl, ws, m, g, targets, lane);
         else
-          ok = visit_strided(a, d, pl, ws, m, g, lc, targets, lane);
+          ok = visit_strided<true>(a, d, succ_of(ws.uc[u]), pl, ws, m, g, lc, targets, lane);
         pending |= __reduce_or_sync(kFull, targets);
       }
     }
