@@ -11,7 +11,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpdg_b200.so")
+# PDG_LIB_PATH: development override (tools/engine_sweep.sh builds variants)
+LIB_PATH = os.environ.get("PDG_LIB_PATH") or os.path.join(_HERE, "libpdg_b200.so")
 
 _lock = threading.Lock()
 _lib = None

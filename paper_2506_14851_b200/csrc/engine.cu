@@ -26,6 +26,8 @@
 // position.  A warp vote detects it; the application is then abandoned by the
 // fast kernel and recomputed from scratch by mc_serial_kernel, which runs the
 // reference algorithm with the sequential generator (one lane per app).
+#include <type_traits>
+
 #include "common.cuh"
 #include "pcg64.cuh"
 
@@ -765,6 +767,11 @@ struct SuccTab {
     n2 = ns > 1 ? __ldg(nxt + 2) : -1;
     n3 = ns > 2 ? __ldg(nxt + 3) : -1;
   }
+  // successor of the uniform carried by a raw 64-bit word (<= 3 successors)
+  __device__ __forceinline__ int next3(uint64_t w) const {
+    const uint64_t k = w >> 11;
+    return k < t0 ? n0 : k < t1 ? n1 : k < t2 ? n2 : n3;
+  }
   // successor of the uniform carried by a raw 64-bit word
   __device__ __forceinline__ int next(const EngineArgs& a, const UnitDesc& d, uint64_t w) const {
     const uint64_t k = w >> 11;
@@ -892,18 +899,23 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
   uint32_t k = q - wb;
   double xa = pl.A[min(uint32_t(ws.ia[k]), la)], xb = 0.0;
   if (LLM) xb = pl.B[min(uint32_t(ws.ib[k]), lb)];
-  for (; q < W; q += 32) {
-    const double ca = xa, cb = xb;
-    xa = pl.A[min(uint32_t(ws.ia[k + 32]), la)];
-    if (LLM) xb = pl.B[min(uint32_t(ws.ib[k + 32]), lb)];
-    st = pcg_stride32(st, lc.c32);
-    const int v = sc.next(a, d, pcg_out(st));
-    const uint32_t w = ws.mem[k];
-    const double t = LLM ? dadd(__ddiv_rn(ca, pre), __ddiv_rn(cb, dec)) : ca;
-    ws.tot[w] = dadd(ws.tot[w], t);
-    arrive(ws, w, v, targets);
-    k += 32;
-  }
+  auto uniforms = [&](auto few_succ) {
+    for (; q < W; q += 32) {
+      const double ca = xa, cb = xb;
+      xa = pl.A[min(uint32_t(ws.ia[k + 32]), la)];
+      if (LLM) xb = pl.B[min(uint32_t(ws.ib[k + 32]), lb)];
+      st = pcg_stride32(st, lc.c32);
+      const uint64_t wd = pcg_out(st);
+      const int v = few_succ ? sc.next3(wd) : sc.next(a, d, wd);
+      const uint32_t w = ws.mem[k];
+      const double t = LLM ? dadd(__ddiv_rn(ca, pre), __ddiv_rn(cb, dec)) : ca;
+      ws.tot[w] = dadd(ws.tot[w], t);
+      arrive(ws, w, v, targets);
+      k += 32;
+    }
+  };
+  if (sc.ns <= 3) uniforms(std::true_type{});
+  else uniforms(std::false_type{});
   if (__any_sync(kFull, rej)) return false;
   const unsigned last = (W - 1) & 31u;            // it decoded word W - 1
   g.s.lo = __shfl_sync(kFull, st.lo, last);
@@ -1019,7 +1031,10 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& p
   return true;
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 6) mc_walk_kernel(EngineArgs a) {
+#ifndef PDG_WALK_MINB
+#define PDG_WALK_MINB 5      // resident CTAs per SM the register budget is cut for
+#endif
+__global__ void __launch_bounds__(kWarps * 32, PDG_WALK_MINB) mc_walk_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;

@@ -27,15 +27,21 @@ __device__ __forceinline__ U128 mul128(U128 a, U128 b) {
 
 __device__ __forceinline__ U128 add128(U128 a, U128 b) {
   U128 r;
-  r.lo = a.lo + b.lo;
-  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1ull : 0ull);
+  asm("add.cc.u64 %0, %2, %4;\n\taddc.u64 %1, %3, %5;"
+      : "=l"(r.lo), "=l"(r.hi)
+      : "l"(a.lo), "l"(a.hi), "l"(b.lo), "l"(b.hi));
   return r;
 }
 
+// XSL-RR output: rotr64(hi ^ lo, hi >> 58), as two 32-bit funnel shifts
 __device__ __forceinline__ uint64_t pcg_out(U128 s) {
   const uint64_t x = s.hi ^ s.lo;
-  const unsigned r = unsigned(s.hi >> 58);
-  return (x >> r) | (x << ((64u - r) & 63u));
+  const uint32_t r = uint32_t(s.hi >> 58);
+  const uint32_t xl = uint32_t(x), xh = uint32_t(x >> 32);
+  const bool sw = r & 32u;
+  const uint32_t a = sw ? xh : xl, b = sw ? xl : xh;   // rotate by 32 first
+  const uint32_t lo = __funnelshift_r(a, b, r), hi = __funnelshift_r(b, a, r);
+  return (uint64_t(hi) << 32) | lo;
 }
 
 constexpr uint64_t kMultLo = 0x4385DF649FCCF645ull;
