@@ -1034,12 +1034,17 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& p
 #ifndef PDG_WALK_MINB
 #define PDG_WALK_MINB 5      // resident CTAs per SM the register budget is cut for
 #endif
-__global__ void __launch_bounds__(kWarps * 32, PDG_WALK_MINB) mc_walk_kernel(EngineArgs a) {
+#ifndef PDG_WALK_WARPS
+#define PDG_WALK_WARPS 4     // applications (warps) per CTA
+#endif
+constexpr int kWalkWarps = PDG_WALK_WARPS;
+
+__global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;
   unsigned char* sb = smem + walk_smem_bytes(a.counters, a.b.max_units) * wib;
-  const int64_t gwarp = int64_t(blockIdx.x) * kWarps + wib;
+  const int64_t gwarp = int64_t(blockIdx.x) * kWalkWarps + wib;
   unsigned char* gs =
       reinterpret_cast<unsigned char*>(a.scratch) + size_t(gwarp) * a.scratch_per_warp;
   WalkState ws;
@@ -1207,31 +1212,33 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(serial_count)");
   const bool sm = n_samples <= kSmemWalks;
   const size_t cnt_bytes = align16(size_t(a.counters) * 4);
-  int64_t blocks = (n_jobs + kWarps - 1) / kWarps;
-  const int64_t capb = grid_warps / kWarps;
-  if (blocks > capb) blocks = capb;
   // persistent grid: exactly the resident CTAs (a second partial wave of
   // grid-stride CTAs would leave SMs idle at the tail)
-  auto launch = [&](auto kern, size_t smem) -> int {
+  auto launch = [&](auto kern, int warps, size_t smem) -> int {
+    int64_t blocks = (n_jobs + warps - 1) / warps;
+    const int64_t capb = grid_warps / warps;
+    if (blocks > capb) blocks = capb;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(smem));
     if (err != cudaSuccess) return cuda_status(err, "cudaFuncSetAttribute(mc_engine_kernel)");
     int per_sm = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
     if (err != cudaSuccess || per_sm < 1) per_sm = 1;
     int64_t nb = int64_t(per_sm) * sm_count();
     if (nb > capb) nb = capb;
     if (nb > blocks) nb = blocks;
-    kern<<<unsigned(nb), kWarps * 32, smem, st>>>(a);
+    kern<<<unsigned(nb), warps * 32, smem, st>>>(a);
     return PDG_OK;
   };
   if (sm) {
     const int mu = bank->max_units < 1 ? 1 : bank->max_units;
-    if (int r = launch(mc_walk_kernel, size_t(kWarps) * walk_smem_bytes(a.counters, mu))) return r;
+    if (int r = launch(mc_walk_kernel, kWalkWarps,
+                       size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu)))
+      return r;
   } else if (small_idx(n_samples)) {
-    if (int r = launch(mc_engine_kernel<uint16_t>, size_t(kWarps) * cnt_bytes)) return r;
+    if (int r = launch(mc_engine_kernel<uint16_t>, kWarps, size_t(kWarps) * cnt_bytes)) return r;
   } else {
-    if (int r = launch(mc_engine_kernel<uint32_t>, size_t(kWarps) * cnt_bytes)) return r;
+    if (int r = launch(mc_engine_kernel<uint32_t>, kWarps, size_t(kWarps) * cnt_bytes)) return r;
   }
   int rc = launch_status("mc_engine_kernel");
   if (rc != PDG_OK) return rc;
