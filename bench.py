@@ -14,9 +14,9 @@ One step = full re-score of the queue, the reference's policy runtime
 (monte_carlo_remaining_demand(n=512) +
 set_remaining(256) + one gittins_rank_batch row per app) plus the global
 order:
-  K2/a4  mc_engine_kernel     512-walk Monte Carlo from the current unit,
+  K2/a4  mc_walk_kernel       512-walk Monte Carlo from the current unit,
                               bit-identical to the reference, bucketed to 256
-  K1b    gittins_hist_kernel  Gittins key + overrun penalty + packed sort key
+  K1b    gittins_rows_kernel  Gittins key + overrun penalty + packed sort key
   K5     radix sort           global order (after the all-gather when N > 1)
 Each step uses fresh per-app seeds (a genuine re-estimate, nothing cached).
 
@@ -246,7 +246,7 @@ def count_launches(step):
         step(0)
         torch.cuda.synchronize()
     names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
-    ours = [nm for nm in names if ("pdg" in nm or "gittins" in nm or "mc_engine" in nm
+    ours = [nm for nm in names if ("pdg" in nm or "gittins" in nm or "mc_" in nm
                                    or "Radix" in nm or "cub" in nm.lower())]
     return len(ours), sorted(set(ours))
 
@@ -434,18 +434,21 @@ def run_ours(args):
     eng_avg = float(eng_ms.mean())
     achieved = bytes_per_app * n / (eng_avg / 1e3) / 1e9
     peak, peak_src = measured_peaks()
-    ns = ncu_summary("mc_engine_kernel")
-    traffic = ns.get("dram_bytes_per_launch")
+    ns = ncu_summary("engine")
+    traffic = ns.get("dram_bytes_per_launch") if ns.get("apps_per_launch") == n else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "mc_engine_kernel", "bytes_per_app": bytes_per_app,
+                "kernel": "mc_walk_kernel", "bytes_per_app": bytes_per_app,
                 "avg_launch_ms": eng_avg, "share_of_step": eng_avg / float(np.mean(step_ms)),
                 "peak_source": peak_src,
-                "note": "integer-issue bound (PCG64 128-bit jump-ahead per draw); the "
-                        "issue-rate roofline from ncu is in profiles/ncu_summary.json",
-                "issue_frac": ns.get("issue_active_frac")}
+                "note": "not HBM-bound: the kernel is integer-issue bound (one 128-bit PCG64 "
+                        "LCG step per consumed numpy word, ~1.5 words per walk visit); issue "
+                        "utilisation and warp instructions per launch from the committed ncu "
+                        "capture (profiles/ncu_summary.json)",
+                "issue_active_frac": ns.get("issue_active_frac"),
+                "warp_instructions": ns.get("warp_instructions")}
     k1_bytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
-    k1 = {"kernel": "gittins_hist_kernel<1>", "avg_launch_ms": float(k1_ms.mean()),
+    k1 = {"kernel": "gittins_rows_kernel", "avg_launch_ms": float(k1_ms.mean()),
           "bytes_per_app": k1_bytes,
           "achieved_gbs": k1_bytes * n / (float(k1_ms.mean()) / 1e3) / 1e9,
           "apps_per_s": n / (float(k1_ms.mean()) / 1e3)}

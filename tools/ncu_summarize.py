@@ -77,7 +77,8 @@ def summarize(rep, kernel, apps):
     clk = num(d, "sm__cycles_elapsed.avg.per_second")
     sms = 148
     issue_peak = 4 * sms * (clk or 1.965e9) * dur if dur else None
-    out = {"kernel": kernel, "report": os.path.basename(rep), "apps_per_launch": apps,
+    name = d.get("Kernel Name", (kernel, ""))[0] or kernel
+    out = {"kernel": name.split("(")[0], "report": os.path.basename(rep), "apps_per_launch": apps,
            "duration_s": dur, "dram_bytes_per_launch": (rd or 0) + (wr or 0),
            "dram_read": rd, "dram_write": wr, "warp_instructions": inst,
            "issue_active_frac": (num(d, "smsp__issue_active.avg.pct_of_peak_sustained_active")
@@ -124,14 +125,15 @@ def main():
     js_path = os.path.join(PROF, "ncu_summary.json")
     summ = json.load(open(js_path)) if os.path.exists(js_path) else {}
     lines = [f"# ncu summary ({tag})", ""]
-    for rep, kernel in (("engine.ncu-rep", "mc_engine_kernel"),
-                        ("k1.ncu-rep", "gittins_hist_kernel")):
+    # role -> report; bench.py reads the "engine" entry for roofline.traffic
+    for rep, role, n in (("engine.ncu-rep", "engine", apps), ("k1.ncu-rep", "k1", apps),
+                         ("need.ncu-rep", "need", 1_000_000)):
         p = os.path.join(OUT, rep)
         if not os.path.exists(p):
             continue
-        s = summarize(p, kernel, apps)
-        summ[kernel] = s
-        lines += [f"## {kernel} (`ncu --set full`, one launch, {apps} apps)", "",
+        s = summarize(p, role, n)
+        summ[role] = s
+        lines += [f"## {role}: {s['kernel']} (`ncu --set full`, one launch, {n} apps)", "",
                   "| metric | value |", "|---|---|"]
         for k, v in s.items():
             if k in ("kernel", "report"):
