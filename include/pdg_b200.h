@@ -159,6 +159,9 @@ typedef struct {
   const int32_t* slot;            /* [N] row written for job i (NULL: row i)          */
   int32_t* capped;                /* [N] walks that hit the visit cap (optional)      */
   uint8_t* flags;                 /* [N] bit0 conditioned, bit1 override, bit2 serial */
+  double* mean;                   /* [rows] RemainingDemand.mean() (optional; Python  */
+                                  /*   sum() semantics, see pdg_policy_keys)          */
+  double* worst;                  /* [rows] max(samples) = worst_case (optional)      */
 } pdg_mc_out;
 
 /* Scratch for pdg_mc_remaining_demand: pdg_mc_scratch_bytes(n, max_pairs,
@@ -172,6 +175,28 @@ int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_jobs* jobs,
                             int32_t bucket_count, int32_t max_unit_k, int32_t max_pairs,
                             const pdg_mc_out* out, void* scratch, size_t scratch_bytes,
                             void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K1c  the other demand-aware priority keys over the device queue
+ * (SURVEY.md 8(f) row 1), from the per-row outputs of the demand engine:
+ *   PDG_POLICY_SRPT_MEAN  key = mean - (age - est_age)
+ *                         compute_priority SRPT_MEAN (sched.py:216-218)
+ *   PDG_POLICY_LSTF       key = deadline - now - ((worst + est_age) - age)
+ *                         compute_priority LSTF -> lstf_slack (sched.py:219-224,
+ *                         132-140); max(s + e) == max(s) + e bit-exactly
+ * mean is RemainingDemand.mean() = sum(samples) / n (estimator.py:55-56) with
+ * CPython >= 3.12 sum() semantics (Neumaier-compensated, in sample order),
+ * written by the engine when pdg_mc_out.mean is set.  Keys are float64,
+ * bit-identical to the reference; out_key (optional) is the order-preserving
+ * uint64 image of the float64 key (sort with pdg_order, begin_bit = 0, on rows
+ * in arrival order).  deadline may be NULL for SRPT_MEAN.  row_idx as in
+ * pdg_gittins_score_hist.
+ * ------------------------------------------------------------------------- */
+enum { PDG_POLICY_SRPT_MEAN = 1, PDG_POLICY_LSTF = 2 };
+int pdg_policy_keys(int32_t policy, const double* mean, const double* worst,
+                    const double* est_age, const double* age, const double* deadline,
+                    double now, int64_t n, const int32_t* row_idx, double* out_key_f64,
+                    uint64_t* out_key, void* stream);
 
 /* ---------------------------------------------------------------------------
  * K4a  batched plan_prewarm (prewarm.py:42-96), bit-exact: one job per

@@ -179,6 +179,48 @@ def refresh_keys(rows_values: Sequence[np.ndarray], rows_probs: Sequence[np.ndar
 
 
 # ---------------------------------------------------------------------------
+# the other demand-aware keys (sched.py:132-140, 217-225)
+# ---------------------------------------------------------------------------
+
+def py_sum(xs: Sequence[float]) -> float:
+    """Python's built-in ``sum`` over floats, as RemainingDemand.mean() calls
+    it (estimator.py:55-56).  CPython >= 3.12 (the interpreter the reference
+    runs on here) compensates with Neumaier's algorithm
+    (Python/bltinmodule.c, builtin_sum_impl): the running total starts as
+    0 + x0, each further x adds its rounding error to c, and c is added at
+    the end when it is non-zero and finite."""
+    it = iter(xs)
+    try:
+        f = 0 + next(it)
+    except StopIteration:
+        return 0
+    c = 0.0
+    for x in it:
+        t = f + x
+        if abs(f) >= abs(x):
+            c += (f - t) + x
+        else:
+            c += (x - t) + f
+        f = t
+    if c and math.isfinite(c):
+        f += c
+    return f
+
+
+def srpt_mean_key(samples: Sequence[float], attained: float, estimate_age: float) -> float:
+    """compute_priority(SRPT_MEAN) (sched.py:216-218)."""
+    served_since = attained - estimate_age
+    return py_sum(samples) / len(samples) - served_since
+
+
+def lstf_key(samples: Sequence[float], attained: float, estimate_age: float,
+             deadline: float, now: float) -> float:
+    """compute_priority(LSTF) (sched.py:219-224) -> lstf_slack (132-140)."""
+    total = [s + estimate_age for s in samples]
+    return deadline - now - (max(total) - attained)
+
+
+# ---------------------------------------------------------------------------
 # a10: prewarm planner (prewarm.py:42-96)
 # ---------------------------------------------------------------------------
 

@@ -478,7 +478,21 @@ __device__ void write_result(const EngineArgs& a, int64_t job, const double* tot
     uint16_t* crow = a.o.counts + row * a.o.stride;
     for (int b = lane; b < a.o.stride; b += 32) crow[b] = b < k ? uint16_t(cnt[b]) : 0;
   }
+  if (a.o.mean && lane == 0) {
+    // RemainingDemand.mean() = sum(samples) / n (estimator.py:55-56) with
+    // CPython >= 3.12 sum(): Neumaier-compensated, in sample order
+    double f = tot[0], c = 0.0;
+    for (int w = 1; w < n; ++w) {
+      const double x = tot[w];
+      const double t = dadd(f, x);
+      c = fabs(f) >= fabs(x) ? dadd(c, dadd(dsub(f, t), x)) : dadd(c, dadd(dsub(x, t), f));
+      f = t;
+    }
+    if (c != 0.0 && isfinite(c)) f = dadd(f, c);
+    a.o.mean[row] = __ddiv_rn(f, small_int_to_double(n));
+  }
   if (lane == 0) {
+    if (a.o.worst) a.o.worst[row] = hi;
     if (a.o.lo) a.o.lo[row] = lo;
     if (a.o.width) a.o.width[row] = width;
     if (a.o.nbins) a.o.nbins[row] = k;

@@ -563,3 +563,56 @@ extern "C" int pdg_bucketize(const double* samples, int64_t rows, int32_t n, int
       samples, rows, n, k, lo, width, nbins, counts, stride);
   return launch_status("bucketize_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// K1c: SRPT-mean and LSTF keys over the queue (sched.py:216-224, 132-140);
+// elementwise, HBM-bound (5 x 8 B in, 16 B out per row)
+// ---------------------------------------------------------------------------
+namespace pdg {
+// order-preserving uint64 image of a float64 (negative keys included)
+__device__ __forceinline__ uint64_t orderable(double x) {
+  const uint64_t b = uint64_t(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void __launch_bounds__(256) policy_keys_kernel(
+    int policy, const double* __restrict__ mean, const double* __restrict__ worst,
+    const double* __restrict__ est_age, const double* __restrict__ age,
+    const double* __restrict__ deadline, double now, int64_t n,
+    const int32_t* __restrict__ row_idx, double* __restrict__ out_f64,
+    uint64_t* __restrict__ out_key) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t r = row_idx ? row_idx[i] : i;
+    double key;
+    if (policy == PDG_POLICY_SRPT_MEAN) {
+      key = dsub(mean[r], dsub(age[r], est_age[r]));
+    } else {
+      key = dsub(dsub(deadline[r], now), dsub(dadd(worst[r], est_age[r]), age[r]));
+    }
+    if (out_f64) out_f64[r] = key;
+    if (out_key) out_key[r] = orderable(key);
+  }
+}
+}  // namespace pdg
+
+extern "C" int pdg_policy_keys(int32_t policy, const double* mean, const double* worst,
+                               const double* est_age, const double* age,
+                               const double* deadline, double now, int64_t n,
+                               const int32_t* row_idx, double* out_key_f64, uint64_t* out_key,
+                               void* stream) {
+  using namespace pdg;
+  const bool srpt = policy == PDG_POLICY_SRPT_MEAN, lstf = policy == PDG_POLICY_LSTF;
+  if (n < 0 || !(srpt || lstf) || !est_age || !age || (srpt && !mean) ||
+      (lstf && (!worst || !deadline)) || (!out_key_f64 && !out_key)) {
+    set_error("pdg_policy_keys: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (n == 0) return PDG_OK;
+  int64_t blocks = (n + 255) / 256;
+  const int64_t cap = int64_t(sm_count()) * 8;
+  if (blocks > cap) blocks = cap;
+  policy_keys_kernel<<<unsigned(blocks), 256, 0, (cudaStream_t)stream>>>(
+      policy, mean, worst, est_age, age, deadline, now, n, row_idx, out_key_f64, out_key);
+  return launch_status("policy_keys_kernel");
+}

@@ -46,7 +46,8 @@ class OutC(C.Structure):
     _fields_ = [("samples", C.c_void_p), ("samples_stride", C.c_int64), ("lo", C.c_void_p),
                 ("width", C.c_void_p), ("nbins", C.c_void_p), ("nsamp", C.c_void_p),
                 ("counts", C.c_void_p), ("stride", C.c_int64), ("slot", C.c_void_p),
-                ("capped", C.c_void_p), ("flags", C.c_void_p)]
+                ("capped", C.c_void_p), ("flags", C.c_void_p), ("mean", C.c_void_p),
+                ("worst", C.c_void_p)]
 
 
 _JUMP = {}
@@ -123,11 +124,12 @@ class DemandEngine:
 
     def run(self, graph_idx, unit_idx, seeds, obs_unit=None, obs_val=None, *, n: int,
             bucket_count: int, visit_cap: int = WALK_VISIT_CAP, queue=None, slots=None,
-            samples: bool = False, stream=None):
+            samples: bool = False, mean: bool = False, stream=None):
         """Launch the engine on device-resident job arrays (torch tensors).
 
         Writes histogram rows into `queue` (HistQueue) at `slots` (default:
-        rows 0..N-1).  Returns dict(samples=[N,n] f64 or None, capped, flags).
+        rows 0..N-1), plus each row's worst case (max sample) and, with
+        mean=True, RemainingDemand.mean() for the SRPT-mean / LSTF keys.  Returns dict(samples=[N,n] f64 or None, capped, flags).
         """
         if n < 1:
             raise EstimationError(f"sample count must be >= 1, got {n}")
@@ -156,7 +158,8 @@ class DemandEngine:
                      _lib.ptr(obs_unit), _lib.ptr(obs_val))
         out = OutC(_lib.ptr(out_samples), n, _lib.ptr(queue.lo), _lib.ptr(queue.width),
                    _lib.ptr(queue.nbins), _lib.ptr(queue.nsamp), _lib.ptr(queue.counts),
-                   queue.stride, _lib.ptr(slots), _lib.ptr(capped), _lib.ptr(flags))
+                   queue.stride, _lib.ptr(slots), _lib.ptr(capped), _lib.ptr(flags),
+                   _lib.ptr(queue.mean) if mean else None, _lib.ptr(queue.worst))
         scratch = self._scratch_for(n, N)
         L = _lib.lib()
         _lib.check(L.pdg_mc_remaining_demand(

@@ -8,6 +8,8 @@ HBM layout (one row per queued application, row = queue slot):
     nbins, nsamp            : int32   [N]      bucket count k (1 = point mass), n
     counts                  : uint16  [N, S]   bucket counts, S = ceil(B/8)*8
     tiebreak                : int32   [N]      arrival-order position (sched.py:168)
+    mean, worst, deadline   : float64 [N]      RemainingDemand.mean() / worst_case /
+                                               deadline (SRPT-mean and LSTF keys)
 
 p_j = counts_j / n reproduces the reference's float64 probabilities exactly
 and the bucket values are rebuilt bit-exactly from (lo, width, est_age), so a
@@ -50,6 +52,10 @@ class HistQueue:
         self.nsamp = torch.ones(capacity, **i32)
         self.counts = torch.zeros(capacity, self.stride, dtype=torch.uint16, device=dev)
         self.tiebreak = torch.arange(capacity, **i32)
+        self.mean = torch.zeros(capacity, **f64)
+        self.worst = torch.zeros(capacity, **f64)
+        self.deadline = torch.zeros(capacity, **f64)
+        self.key_f64 = torch.zeros(capacity, **f64)
         self.key_f32 = torch.zeros(capacity, dtype=torch.float32, device=dev)
         self.flags = torch.zeros(capacity, dtype=torch.uint8, device=dev)
         self.keys = torch.zeros(capacity, dtype=torch.int64, device=dev)
@@ -106,6 +112,23 @@ class HistQueue:
             _lib.ptr(self.key_f32), _lib.ptr(self.flags), _lib.ptr(self.tiebreak),
             _lib.ptr(self.keys) if keys else None, _lib.ptr(rows), _lib.stream_ptr(stream)),
             "pdg_gittins_score_hist")
+
+    def score_policy(self, policy, now: float, n: Optional[int] = None, stream=None,
+                     rows: Optional[torch.Tensor] = None) -> None:
+        """K1c: SRPT-mean or LSTF keys (float64, bit-identical to
+        compute_priority, sched.py:216-224) into key_f64 and, order-preserving,
+        into keys; sort with order() (full 64-bit keys)."""
+        pv = getattr(policy, "value", policy)
+        code = {"srpt-mean": 1, "lstf": 2}.get(pv)
+        if code is None:
+            raise ValueError(f"score_policy: {pv!r} is not SRPT_MEAN or LSTF")
+        n = (self.n if n is None else int(n)) if rows is None else int(rows.numel())
+        L = _lib.lib()
+        _lib.check(L.pdg_policy_keys(
+            code, _lib.ptr(self.mean), _lib.ptr(self.worst), _lib.ptr(self.est_age),
+            _lib.ptr(self.age), _lib.ptr(self.deadline), float(now), n, _lib.ptr(rows),
+            _lib.ptr(self.key_f64), _lib.ptr(self.keys), _lib.stream_ptr(stream)),
+            "pdg_policy_keys")
 
     def order(self, n: Optional[int] = None, stream=None,
               arrival_ordered: bool = False) -> torch.Tensor:
