@@ -471,6 +471,7 @@ def run_ours(args):
         "e2e": e2e, "roofline": roofline, "k1_refresh": k1, "clocks": clk,
     }
     if world == 1 and not args.no_extra:
+        line["k1c_policy"] = bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b)
         del eng, q, w
         torch.cuda.empty_cache()
         line["config4_stream"] = bench_stream(dev)
@@ -487,6 +488,60 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# SRPT-mean / LSTF keys (K1c) and the engine's mean epilogue
+# ---------------------------------------------------------------------------
+
+def bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b, rows=1_000_000, reps=20):
+    import torch
+    from paper_2506_14851_b200.queue import HistQueue
+    from paper_2506_14851_b200.sched import Policy
+
+    def timed(fn, k):
+        ts = []
+        for _ in range(k):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.mean(ts))
+
+    run = lambda mean: eng.run(g_idx, u_idx, seeds, n=N_SAMP, bucket_count=b,  # noqa: E731
+                               visit_cap=VISIT_CAP, queue=q, mean=mean)
+    run(True)
+    base_ms, mean_ms = timed(lambda: run(False), 3), timed(lambda: run(True), 3)
+    hq = HistQueue(rows, 8)
+    rng = torch.Generator(device=dev).manual_seed(5)
+    for t in (hq.mean, hq.worst, hq.est_age, hq.age, hq.deadline):
+        t.uniform_(0, 1000, generator=rng)
+    hq.n = rows
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = {}
+    for pol in (Policy.SRPT_MEAN, Policy.LSTF):
+        hq.score_policy(pol, 500.0)
+
+        def one():
+            hq.score_policy(pol, 500.0)
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            ts.append(timed(one, 1))
+        ms = float(np.mean(ts))
+        nbytes = (4 if pol is Policy.SRPT_MEAN else 5) * 8 + 16
+        out[pol.value] = {"ms_per_launch": ms, "rows": rows, "apps_per_s": rows / (ms / 1e3),
+                          "roofline": {"bound": "hbm", "bytes_per_app": nbytes,
+                                       "achieved": nbytes * rows / (ms / 1e3) / 1e9,
+                                       "peak": measured_peaks()[0], "unit": "GB/s"}}
+        out[pol.value]["roofline"]["frac"] = (out[pol.value]["roofline"]["achieved"]
+                                              / out[pol.value]["roofline"]["peak"])
+    out["engine_mean_epilogue"] = {"engine_ms": base_ms, "engine_with_mean_ms": mean_ms,
+                                   "apps": n, "note": "RemainingDemand.mean() in CPython "
+                                   "sum() order (sequential, one lane per app)"}
+    return out
 
 
 # ---------------------------------------------------------------------------
