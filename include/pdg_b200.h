@@ -199,6 +199,32 @@ int pdg_policy_keys(int32_t policy, const double* mean, const double* worst,
                     uint64_t* out_key, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * K6  dispatch / preemption plan: the consumer of the
+ * priority keys.  Replaces the min()/max() scans of Simulator._dispatch and
+ * Simulator._preempt (simcore.py:512-516, 652-687) over _task_sort_key
+ * (simcore.py:339-344) on one PriorityRefresh (simcore.py:636-644): first the
+ * preemption swaps of every backend, then the dispatch fill of every backend.
+ * Task t: backend[t] in [0, n_backends), active[t] (1 = holds a slot),
+ * key[t] = the app's Priority.key (float64), app_rank[t] = position of the
+ * app's (arrival_time, app_instance_id) in arrival order, stage[t] /
+ * request[t] < 65536.  slots[b] <= 1024.  Events of backend b land in
+ * ev_task/ev_kind[b * ev_cap ...]: ev_count[b] preemption events (pairs:
+ * kind 1 = preempt, 2 = start), then ev_count[n_backends + b] dispatch starts
+ * (kind 2).  ev_cap >= 3 * max(slots) always suffices.  After the call,
+ * pdg_dispatch_status reports 0 = ok, 1 = a backend had more running tasks
+ * than slots, 2 = a plan needed more than 2 * slots waiting candidates.
+ * temp: pdg_dispatch_temp_bytes(n, n_backends) bytes of device scratch.
+ * ------------------------------------------------------------------------- */
+size_t pdg_dispatch_temp_bytes(int64_t n, int32_t n_backends);
+int pdg_dispatch_plan(const int32_t* backend, const uint8_t* active, const double* key,
+                      const uint32_t* app_rank, const int32_t* stage, const int32_t* request,
+                      int64_t n, const int32_t* slots, int32_t n_backends, double hysteresis,
+                      int32_t preempt, int32_t ev_cap, int32_t* ev_task, uint8_t* ev_kind,
+                      int32_t* ev_count, void* temp, size_t temp_bytes, void* stream);
+int pdg_dispatch_status(const void* temp, int64_t n, int32_t n_backends, int32_t* status_out,
+                        void* stream);
+
+/* ---------------------------------------------------------------------------
  * K4a  batched plan_prewarm (prewarm.py:42-96), bit-exact: one job per
  * (application, successor).  Job j's completion samples (absolute times, the
  * caller's completion_dist.samples) are pool[off[j] .. off[j]+len[j]).

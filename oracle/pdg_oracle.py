@@ -221,6 +221,51 @@ def lstf_key(samples: Sequence[float], attained: float, estimate_age: float,
 
 
 # ---------------------------------------------------------------------------
+# dispatch / preemption on one PriorityRefresh
+# (simcore.py:636-644 -> _preempt 652-687, _dispatch 512-516)
+# ---------------------------------------------------------------------------
+
+def plan_dispatch(backend, active, key, app_rank, stage, request, slots, hysteresis=1.5,
+                  preempt=True):
+    """Events [(kind, task)] (kind 1 = preempt, 2 = start) in the order the
+    simulator applies them: preemption swaps of every backend, then the
+    dispatch fill of every backend.  Task order = _task_sort_key
+    (simcore.py:339-344) with (arrival_time, app_instance_id) as app_rank."""
+    nb = len(slots)
+    tup = lambda t: (key[t], app_rank[t], stage[t], request[t])  # noqa: E731
+    queue = [[t for t in range(len(backend)) if backend[t] == b and not active[t]]
+             for b in range(nb)]
+    act = [[t for t in range(len(backend)) if backend[t] == b and active[t]]
+           for b in range(nb)]
+    ev = []
+    if preempt:
+        for b in range(nb):
+            if not queue[b]:
+                continue
+            changed = True
+            while changed:
+                changed = False
+                if not queue[b] or not act[b]:
+                    break
+                w = min(queue[b], key=tup)
+                x = max(act[b], key=tup)
+                if key[x] > key[w] * hysteresis and key[x] > key[w]:
+                    act[b].remove(x)
+                    queue[b].append(x)
+                    act[b].append(w)
+                    queue[b].remove(w)
+                    ev += [(1, x), (2, w)]
+                    changed = True
+    for b in range(nb):
+        while queue[b] and len(act[b]) < slots[b]:
+            w = min(queue[b], key=tup)
+            queue[b].remove(w)
+            act[b].append(w)
+            ev.append((2, w))
+    return ev
+
+
+# ---------------------------------------------------------------------------
 # a10: prewarm planner (prewarm.py:42-96)
 # ---------------------------------------------------------------------------
 
