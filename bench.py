@@ -472,6 +472,7 @@ def run_ours(args):
     }
     if world == 1 and not args.no_extra:
         line["k1c_policy"] = bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b)
+        line["k6_dispatch"] = bench_dispatch(dev)
         del eng, q, w
         torch.cuda.empty_cache()
         line["config4_stream"] = bench_stream(dev)
@@ -542,6 +543,57 @@ def bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b, rows=1_000_000, reps=20
                                    "apps": n, "note": "RemainingDemand.mean() in CPython "
                                    "sum() order (sequential, one lane per app)"}
     return out
+
+
+# ---------------------------------------------------------------------------
+# dispatch / preemption plan (K6)
+# ---------------------------------------------------------------------------
+
+def bench_dispatch(dev, n_tasks=1_000_000, slots=(64, 32, 32), reps=10, cpu_tasks=20_000):
+    """One PriorityRefresh's preemption + dispatch decisions over a 1M-task
+    table on 3 backends (device), and the reference's min()/max() scans
+    (oracle restatement of simcore.py:512-516, 652-687) on a bounded sample."""
+    import torch
+    from oracle import pdg_oracle as O
+    from paper_2506_14851_b200.dispatch import DispatchPlanner
+    rng = np.random.default_rng(11)
+
+    def table(n):
+        be = rng.integers(0, len(slots), n)
+        act = np.zeros(n, dtype=np.int64)
+        for b, s in enumerate(slots):
+            idx = np.flatnonzero(be == b)[:s]
+            act[idx] = 1
+        return {"backend": be, "active": act, "key": rng.lognormal(3, 2, n),
+                "app_rank": rng.permutation(n), "stage": rng.integers(0, 4, n),
+                "request": rng.integers(0, 3, n)}
+    t = table(n_tasks)
+    d = (torch.tensor(t["backend"], dtype=torch.int32, device=dev),
+         torch.tensor(t["active"], dtype=torch.uint8, device=dev),
+         torch.tensor(t["key"], dtype=torch.float64, device=dev),
+         torch.tensor(t["app_rank"], dtype=torch.int32, device=dev),
+         torch.tensor(t["stage"], dtype=torch.int32, device=dev),
+         torch.tensor(t["request"], dtype=torch.int32, device=dev))
+    pl = DispatchPlanner(device=str(dev))
+    ev = pl.plan(*d, list(slots))
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pl.plan(*d, list(slots))                  # includes the event read-back
+        ts.append((time.perf_counter() - t0) * 1e3)
+    c = table(cpu_tasks)
+    t0 = time.perf_counter()
+    O.plan_dispatch(c["backend"].tolist(), c["active"].tolist(), c["key"].tolist(),
+                    c["app_rank"].tolist(), c["stage"].tolist(), c["request"].tolist(),
+                    list(slots), 1.5)
+    cpu_ms = (time.perf_counter() - t0) * 1e3
+    return {"tasks": n_tasks, "backends": len(slots), "slots": list(slots),
+            "events": len(ev), "ms_per_plan_p50": float(np.median(ts)),
+            "tasks_per_s": n_tasks / (float(np.median(ts)) / 1e3),
+            "cpu_port_ms": cpu_ms, "cpu_sample_tasks": cpu_tasks,
+            "note": "wall clock incl. event read-back; the CPU port's min()/max() scans "
+                    "grow with tasks x slots"}
 
 
 # ---------------------------------------------------------------------------
