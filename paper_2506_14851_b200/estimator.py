@@ -90,8 +90,21 @@ class DemandEngine:
         _lib.lib()
         self.device = torch.device(device)
         self.bank = graphs if isinstance(graphs, GraphBank) else GraphBank(graphs, device=device)
-        b = self.bank
         self.jump = _jump_tensor(self.device)
+        self._rates = (float(prefill_rate), float(decode_rate))
+        self._bind()
+        self._scratch = None
+
+    def refresh(self, name: str, graph=None) -> None:
+        """Template refresh after profiling trials were recorded into graph
+        `name` (graphs.record_trial / pdgraph.record_trial): recompile that
+        graph's tables and re-bind the device pointers."""
+        self.bank.update(name, graph)
+        self._bind()
+
+    def _bind(self):
+        b = self.bank
+        prefill_rate, decode_rate = self._rates
         self.c_bank = GraphBankC(
             _lib.ptr(b.units), _lib.ptr(b.graph_base), _lib.ptr(b.graph_n),
             _lib.ptr(b.unit_capacity), _lib.ptr(b.vals), _lib.ptr(b.pool_off),
@@ -100,7 +113,6 @@ class DemandEngine:
             float(prefill_rate), float(decode_rate), _lib.ptr(b.succ_thr), int(b.max_units))
         self.max_unit_k = b.max_unit_k
         self.max_pairs = b.max_pairs
-        self._scratch = None
 
     # -- job marshalling ------------------------------------------------------
     def relevant_observation(self, name: str, current: str, observations) -> tuple[int, tuple]:

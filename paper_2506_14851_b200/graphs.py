@@ -160,6 +160,49 @@ def graph_from_kb(doc: dict) -> KBGraph:
     return KBGraph(doc["app_id"], doc["entry_unit"], units)
 
 
+class GraphError(ValueError):
+    """Mirror of pdgsim.errors.GraphError for KB graphs."""
+
+
+def record_trial(graph: KBGraph, trial: dict) -> KBGraph:
+    """Append one profiling trial (unit id -> KBRecord) to a KB graph, as
+    pdgraph.record_trial does (pdgraph.py:247-279): unknown units and
+    records not connected to the entry unit are rejected; each unit keeps
+    its last `capacity` records (FunctionalUnit.records is a capped deque,
+    pdgraph.py:148-160) and its branch frequencies are recomputed
+    (branch_probabilities, pdgraph.py:182-194).  Masks are left alone
+    (build_masks recomputes them, estimator.py:108-142).  Then call
+    GraphBank.update / DemandEngine.refresh."""
+    for uid in trial:
+        if uid not in graph.units:
+            raise GraphError(f"trial references unknown unit {uid!r}")
+    if graph.entry_unit not in trial:
+        raise GraphError(f"trial does not include the entry unit {graph.entry_unit!r}")
+    visited: set = set()
+    stack = [graph.entry_unit]
+    while stack:
+        uid = stack.pop()
+        if uid in visited or uid not in trial:
+            continue
+        visited.add(uid)
+        nxt = trial[uid].next_unit
+        if nxt is not None:
+            stack.append(nxt)
+    disconnected = set(trial) - visited
+    if disconnected:
+        raise GraphError(f"trial records disconnected from entry: {sorted(disconnected)}")
+    for uid in sorted(trial):
+        u = graph.units[uid]
+        u.records = (list(u.records) + [trial[uid]])[-u.capacity:]
+        counts: dict = {}
+        for r in u.records:
+            if r.next_unit is not None:
+                counts[r.next_unit] = counts.get(r.next_unit, 0) + 1
+        n = len(u.records)
+        u.successors = {k: c / n for k, c in sorted(counts.items())} if n else {}
+    return graph
+
+
 # ---------------------------------------------------------------------------
 # bucketing helpers (distributions.py:79-118), host side, exact float64
 # ---------------------------------------------------------------------------
@@ -204,115 +247,177 @@ def _masks(unit):
 # ---------------------------------------------------------------------------
 
 class GraphBank:
-    """Compiled device tables for a set of graphs (name -> graph)."""
+    """Compiled device tables for a set of graphs (name -> graph).
+
+    Each graph compiles to a self-contained segment (offsets local to the
+    segment); the bank is the concatenation of the segments with the
+    offsets rebased.  ``update(name)`` recompiles one graph after its
+    records changed (``record_trial``) and rebuilds the device tables from
+    the cached segments, so a profiling trial costs one graph's compile."""
 
     def __init__(self, graphs: dict, device: str = "cuda"):
         self.names = list(graphs)
         self.index = {nm: i for i, nm in enumerate(self.names)}
         self.unit_order = {}        # name -> [uid sorted]
+        self.empty_units = {}       # name -> [(uid, message)] (estimator.py:246-268)
+        self.graphs = graphs
+        self.device = device
+        self._segments = {nm: self._compile(nm, graphs[nm]) for nm in self.names}
+        self._place()
+
+    def update(self, name: str, graph=None) -> None:
+        """Recompile graph `name` (optionally replacing it) and rebuild the
+        device tables.  Pointers held by a DemandEngine must be re-bound
+        (DemandEngine.refresh does both)."""
+        if name not in self.index:
+            raise KeyError(name)
+        if graph is not None:
+            self.graphs[name] = graph
+        self.empty_units.pop(name, None)
+        self._segments[name] = self._compile(name, self.graphs[name])
+        self._place()
+
+    def _compile(self, nm, g) -> dict:
         vals: list = []
         units = []
         pools_off, pools_len = [], []
         succ_cum, succ_nxt = [], []
         conds, pairs = [], []
-        gbase, gn = [], []
 
         def push(xs) -> tuple[int, int]:
             off = len(vals)
             vals.extend(float(x) for x in xs)
             return off, len(xs)
 
-        self.empty_units = {}       # name -> [(uid, message)] (estimator.py:246-268)
-        for nm in self.names:
-            g = graphs[nm]
-            order = sorted(g.units)
-            self.unit_order[nm] = order
-            for uid in order:
-                u = g.units[uid]
-                if u.is_llm and (not list(u.input_dist.samples) or
-                                 not list(u.output_dist.samples)):
-                    self.empty_units.setdefault(nm, []).append(
-                        (uid, f"unit {uid!r} has no token-length samples"))
-                elif not u.is_llm and not list(u.duration_dist.samples):
-                    self.empty_units.setdefault(nm, []).append(
-                        (uid, f"unit {uid!r} has no duration samples"))
-            pos = {u: i for i, u in enumerate(order)}
-            gbase.append(len(units))
-            gn.append(len(order))
-            if len(order) > 32:
-                raise ValueError(f"graph {nm!r}: more than 32 units")
-            for uid in order:
-                u = g.units[uid]
-                d = np.zeros((), dtype=UNIT_DTYPE)
-                flags = _masks(u)
-                if u.is_llm:
-                    flags |= F_LLM
-                    a = list(u.input_dist.samples)
-                    b = list(u.output_dist.samples)
-                    d["a_off"], d["a_len"] = push(a)
-                    d["b_off"], d["b_len"] = push(b)
-                    d["pool_off"] = len(pools_off)
-                    bn = binning(a, u.bucket_count)
-                    if bn is not None:
-                        d["ib_lo"], d["ib_hi"], d["ib_k"] = bn
-                    if u.masks.output_own_input and len(u.records) > 0 and bn is not None:
-                        flags |= F_OWN
-                        groups: dict = {}
-                        for r in u.records:
-                            groups.setdefault(bucket_index(bn, r.input_len), []).append(
-                                r.output_len)
-                        for kb in range(bn[2]):
-                            xs = groups.get(kb, [])
-                            o, ln = push(xs) if xs else (0, 0)
-                            pools_off.append(o)
-                            pools_len.append(ln)
-                else:
-                    d["a_off"], d["a_len"] = push(list(u.duration_dist.samples))
-                d["flags"] = flags
-                succ = sorted(u.successors.items())
-                d["succ_off"] = len(succ_nxt)
-                d["succ_len"] = len(succ)
-                cum = np.cumsum([p for _, p in succ]) if succ else np.zeros(0)
-                succ_cum.extend(cum.tolist() + [0.0])
-                succ_nxt.extend([pos[s] for s, _ in succ] + [-1])
-                # K3 tables: joined records with every upstream (estimator.py:168-173)
-                d["cond_off"] = len(conds)
-                ups = [v for v in order if uid in g.units[v].successors]
-                for up_id in ups:
-                    up = g.units[up_id]
-                    c = np.zeros((), dtype=COND_DTYPE)
-                    c["up_local"] = pos[up_id]
-                    dists = [up.input_dist.samples, up.output_dist.samples,
-                             up.parallelism_dist.samples]
-                    bns = [binning(x, up.bucket_count) for x in dists]
-                    for j, bnj in enumerate(bns):
-                        if bnj is not None:
-                            c["lo"][j], c["hi"][j], c["k"][j] = bnj
-                            c["ok"][j] = 1
-                    mine = {}
+        order = sorted(g.units)
+        if len(order) > 32:
+            raise ValueError(f"graph {nm!r}: more than 32 units")
+        self.unit_order[nm] = order
+        for uid in order:
+            u = g.units[uid]
+            if u.is_llm and (not list(u.input_dist.samples) or
+                             not list(u.output_dist.samples)):
+                self.empty_units.setdefault(nm, []).append(
+                    (uid, f"unit {uid!r} has no token-length samples"))
+            elif not u.is_llm and not list(u.duration_dist.samples):
+                self.empty_units.setdefault(nm, []).append(
+                    (uid, f"unit {uid!r} has no duration samples"))
+        pos = {u: i for i, u in enumerate(order)}
+        for uid in order:
+            u = g.units[uid]
+            d = np.zeros((), dtype=UNIT_DTYPE)
+            flags = _masks(u)
+            if u.is_llm:
+                flags |= F_LLM
+                a = list(u.input_dist.samples)
+                b = list(u.output_dist.samples)
+                d["a_off"], d["a_len"] = push(a)
+                d["b_off"], d["b_len"] = push(b)
+                d["pool_off"] = len(pools_off)
+                bn = binning(a, u.bucket_count)
+                if bn is not None:
+                    d["ib_lo"], d["ib_hi"], d["ib_k"] = bn
+                if u.masks.output_own_input and len(u.records) > 0 and bn is not None:
+                    flags |= F_OWN
+                    groups: dict = {}
                     for r in u.records:
-                        mine[r.trial_id] = r
-                    c["pair_off"] = len(pairs)
-                    for ur in up.records:
-                        if ur.next_unit == uid and ur.trial_id in mine:
-                            p = np.zeros((), dtype=PAIR_DTYPE)
-                            for j, (bnj, v) in enumerate(zip(bns, (ur.input_len, ur.output_len,
-                                                                   float(ur.parallelism)))):
-                                p["bk"][j] = bucket_index(bnj, v) if bnj is not None else -1
-                            r = mine[ur.trial_id]
-                            p["in"], p["out"] = r.input_len, r.output_len
-                            pairs.append(p)
-                    c["pair_len"] = len(pairs) - int(c["pair_off"])
-                    conds.append(c)
-                d["cond_len"] = len(conds) - int(d["cond_off"])
-                units.append(d)
+                        groups.setdefault(bucket_index(bn, r.input_len), []).append(
+                            r.output_len)
+                    for kb in range(bn[2]):
+                        xs = groups.get(kb, [])
+                        o, ln = push(xs) if xs else (0, 0)
+                        pools_off.append(o)
+                        pools_len.append(ln)
+            else:
+                d["a_off"], d["a_len"] = push(list(u.duration_dist.samples))
+            d["flags"] = flags
+            succ = sorted(u.successors.items())
+            d["succ_off"] = len(succ_nxt)
+            d["succ_len"] = len(succ)
+            cum = np.cumsum([p for _, p in succ]) if succ else np.zeros(0)
+            succ_cum.extend(cum.tolist() + [0.0])
+            succ_nxt.extend([pos[s] for s, _ in succ] + [-1])
+            # K3 tables: joined records with every upstream (estimator.py:168-173)
+            d["cond_off"] = len(conds)
+            ups = [v for v in order if uid in g.units[v].successors]
+            for up_id in ups:
+                up = g.units[up_id]
+                c = np.zeros((), dtype=COND_DTYPE)
+                c["up_local"] = pos[up_id]
+                dists = [up.input_dist.samples, up.output_dist.samples,
+                         up.parallelism_dist.samples]
+                bns = [binning(x, up.bucket_count) for x in dists]
+                for j, bnj in enumerate(bns):
+                    if bnj is not None:
+                        c["lo"][j], c["hi"][j], c["k"][j] = bnj
+                        c["ok"][j] = 1
+                mine = {}
+                for r in u.records:
+                    mine[r.trial_id] = r
+                c["pair_off"] = len(pairs)
+                for ur in up.records:
+                    if ur.next_unit == uid and ur.trial_id in mine:
+                        pr = np.zeros((), dtype=PAIR_DTYPE)
+                        for j, (bnj, v) in enumerate(zip(bns, (ur.input_len, ur.output_len,
+                                                               float(ur.parallelism)))):
+                            pr["bk"][j] = bucket_index(bnj, v) if bnj is not None else -1
+                        r = mine[ur.trial_id]
+                        pr["in"], pr["out"] = r.input_len, r.output_len
+                        pairs.append(pr)
+                c["pair_len"] = len(pairs) - int(c["pair_off"])
+                conds.append(c)
+            d["cond_len"] = len(conds) - int(d["cond_off"])
+            units.append(d)
+        return {"units": np.array(units, dtype=UNIT_DTYPE) if units else
+                np.zeros(0, UNIT_DTYPE),
+                "vals": np.asarray(vals, dtype=np.float64),
+                "pools_off": np.asarray(pools_off, dtype=np.int64),
+                "pools_len": np.asarray(pools_len, dtype=np.int64),
+                "succ_cum": np.asarray(succ_cum, dtype=np.float64),
+                "succ_nxt": np.asarray(succ_nxt, dtype=np.int64),
+                "conds": np.array(conds, dtype=COND_DTYPE) if conds else
+                np.zeros(0, COND_DTYPE),
+                "pairs": np.array(pairs, dtype=PAIR_DTYPE) if pairs else
+                np.zeros(0, PAIR_DTYPE),
+                "caps": [getattr(g.units[uid], "capacity", 1000) for uid in order]}
 
-        self.graphs = graphs
-        caps = [getattr(graphs[nm].units[uid], "capacity", 1000)
-                for nm in self.names for uid in self.unit_order[nm]]
-        self._finish(device, np.array(units, dtype=UNIT_DTYPE) if units else
-                     np.zeros(0, UNIT_DTYPE), vals, gbase, gn, caps, pools_off, pools_len,
-                     succ_cum, succ_nxt, conds, pairs)
+    def _place(self) -> None:
+        """Concatenate the segments (rebasing their local offsets) and upload."""
+        units, vals, po, pl, sc, sn, cs, ps, caps = [], [], [], [], [], [], [], [], []
+        gbase, gn = [], []
+        nv = npool = nsucc = ncond = npair = nunit = 0
+        for nm in self.names:
+            sg = self._segments[nm]
+            u = sg["units"].copy()
+            llm = (u["flags"] & F_LLM) != 0
+            u["a_off"] += nv
+            u["b_off"] += np.where(llm, nv, 0).astype(u["b_off"].dtype)
+            u["pool_off"] += np.where(llm, npool, 0).astype(u["pool_off"].dtype)
+            u["succ_off"] += nsucc
+            u["cond_off"] += ncond
+            c = sg["conds"].copy()
+            c["pair_off"] += npair
+            units.append(u)
+            vals.append(sg["vals"])
+            po.append(np.where(sg["pools_len"] > 0, sg["pools_off"] + nv, 0))
+            pl.append(sg["pools_len"])
+            sc.append(sg["succ_cum"])
+            sn.append(sg["succ_nxt"])
+            cs.append(c)
+            ps.append(sg["pairs"])
+            caps.extend(sg["caps"])
+            gbase.append(nunit)
+            gn.append(len(u))
+            nv += len(sg["vals"])
+            npool += len(sg["pools_off"])
+            nsucc += len(sg["succ_nxt"])
+            ncond += len(c)
+            npair += len(sg["pairs"])
+            nunit += len(u)
+        cat = lambda xs, dt: np.concatenate(xs) if xs else np.zeros(0, dt)  # noqa: E731
+        self._finish(self.device, cat(units, UNIT_DTYPE), cat(vals, np.float64), gbase, gn,
+                     caps, cat(po, np.int64), cat(pl, np.int64), cat(sc, np.float64),
+                     cat(sn, np.int64), list(cat(cs, COND_DTYPE)), list(cat(ps, PAIR_DTYPE)))
 
     @classmethod
     def from_arrays(cls, *, units, vals, graph_base, graph_n, succ_cum, succ_nxt,
@@ -326,6 +431,7 @@ class GraphBank:
         self.index = {nm: i for i, nm in enumerate(self.names)}
         self.unit_order = unit_order or {}
         self.graphs = {}
+        self.device = device
         self._finish(device, units, vals, graph_base, graph_n, unit_capacity, [], [],
                      succ_cum, succ_nxt, [], [])
         return self
