@@ -137,6 +137,9 @@ typedef struct {
   double prefill_rate, decode_rate; /* RateProfile (pdgraph.py:282-291)     */
   const uint64_t* succ_thr;       /* ceil(succ_cum * 2^53): integer cum <= u */
   int32_t max_units;              /* max over graph_n                        */
+  const double* vals_div;         /* vals with LLM input pools / prefill_rate */
+                                  /* and output pools / decode_rate (exact  */
+                                  /* f64 divisions); durations as in vals   */
 } pdg_graph_bank;
 
 typedef struct {

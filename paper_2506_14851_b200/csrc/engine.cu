@@ -747,7 +747,26 @@ struct WalkState {
   uint16_t* osrt;
   double* kin;       // [max_pairs] K3 kept inputs / outputs (global scratch)
   double* kout;
+  double* kin_d;     // [max_pairs] the same divided by prefill / decode rate
+  double* kout_d;
 };
+
+// pool values as the stage time uses them: LLM inputs / prefill_rate, LLM
+// outputs / decode_rate (divided once, exactly as estimator.py:286 divides
+// each draw), durations unchanged -- the same offsets in a.b.vals_div
+__device__ __forceinline__ Pools pools_div(const EngineArgs& a, const UnitDesc& d, bool ov,
+                                           const Pools& ovd) {
+  Pools pl;
+  if ((d.flags & F_LLM) && ov) {
+    pl = ovd;
+  } else {
+    pl.A = a.b.vals_div + d.a_off;
+    pl.pa = d.a_len;
+    pl.B = a.b.vals_div + d.b_off;
+    pl.pb = d.b_len;
+  }
+  return pl;
+}
 
 // shared memory per warp: [counters | LLM staging] [tot] [mem] [bitsets of
 // max_units units]
@@ -903,7 +922,6 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
     else ws.ib[0] = uint16_t(lemire(g.pv, uint32_t(pl.pb), rej));
   }
   __syncwarp();
-  const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
   const bool hb = C > mA;
   // random(m): stage time + successor; the pool loads of the next word are
   // issued before the current word is finished
@@ -922,7 +940,7 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
       const uint64_t wd = pcg_out(st);
       const int v = few_succ ? sc.next3(wd) : sc.next(a, d, wd);
       const uint32_t w = ws.mem[k];
-      const double t = LLM ? dadd(__ddiv_rn(ca, pre), __ddiv_rn(cb, dec)) : ca;
+      const double t = LLM ? dadd(ca, cb) : ca;    // pools hold i/prefill, o/decode
       ws.tot[w] = dadd(ws.tot[w], t);
       arrive(ws, w, v, targets);
       k += 32;
@@ -946,7 +964,7 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
 // own-input LLM unit: outputs drawn per input bucket, buckets ascending,
 // walks in order within a bucket (estimator.py:275-283)
 __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& pl,
-                          const WalkState& ws, uint32_t m, Stream& g, unsigned& targets,
+                          const Pools& pd, const WalkState& ws, uint32_t m, Stream& g, unsigned& targets,
                           int lane) {
   const uint64_t* jt = a.b.jump;
   const unsigned lt = lanemask_lt();
@@ -955,7 +973,6 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& p
   const uint32_t per = (m + 31) >> 5;
   const uint32_t k0 = min(lane * per, m), k1 = min(k0 + per, m);
   const uint32_t c1 = pl.pa > 1 ? m : 0u;
-  const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
   bool rej = false;
   Cursor ca{g.s, 0xffffffffu, 0}, cb{g.s, 0xffffffffu, 0};
   const int K = d.ib_k;
@@ -966,8 +983,8 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& p
   __syncwarp();
   for (uint32_t k = k0; k < k1; ++k) {
     const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(ca, jt, g, k), uint32_t(pl.pa), rej) : 0u;
-    const double iv = pl.A[ia];
-    ws.tmp[k] = iv;
+    const double iv = pl.A[ia];                  // raw input picks the bucket
+    ws.tmp[k] = pd.A[ia];                        // i / prefill_rate
     const int bb = bucket_of(iv, d.ib_lo, d.ib_hi, K);
     ws.bkt[k] = uint16_t(bb);
     atomicAdd(&cnt[bb], 1u);
@@ -1019,11 +1036,11 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& p
     const uint32_t k = ws.osrt[j];
     const int bb = ws.bkt[k];
     const int pln = a.b.pool_len[d.pool_off + bb];
-    const double* pool = pln > 0 ? a.b.vals + a.b.pool_off[d.pool_off + bb] : pl.B;
+    const double* pool = pln > 0 ? a.b.vals_div + a.b.pool_off[d.pool_off + bb] : pd.B;
     const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
     const uint32_t pos = c1 + effo[bb] + (j - start[bb]);
     const uint32_t ob = P > 1 ? lemire(cursor_half(cb, jt, g, pos), P, rej) : 0u;
-    ws.tmp[k] = dadd(__ddiv_rn(ws.tmp[k], pre), __ddiv_rn(pool[ob], dec));
+    ws.tmp[k] = dadd(ws.tmp[k], pool[ob]);      // i/prefill + o/decode
   }
   if (__any_sync(kFull, rej)) return false;
   const uint32_t C = c1 + eff_total;
@@ -1074,6 +1091,8 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
   ws.osrt = ws.bkt + kSmemWalks;
   ws.kin = reinterpret_cast<double*>(gs + walk_gmem_bytes());
   ws.kout = ws.kin + a.max_pairs;
+  ws.kin_d = ws.kout + a.max_pairs;
+  ws.kout_d = ws.kin_d + a.max_pairs;
   for (;;) {
     int job = 0;
     if (lane == 0) job = atomicAdd(a.job_next, 1);
@@ -1094,6 +1113,22 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
     job_obs(a, job, obs_up, obs);
     const bool has_ov =
         condition(a, gbase, u0, obs_up, obs, ws.kin, ws.kout, ovp, conditioned, lane);
+    Pools ovd = ovp;                             // the override pools, divided
+    if (has_ov) {
+      const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
+      auto divide = [&](const double* p, int len, const double* buf, double* dbuf,
+                        double rate) -> const double* {
+        if (p >= buf && p < buf + a.max_pairs) {   // kept records: divide them
+          const int off = int(p - buf);
+          for (int i = lane; i < len; i += 32) dbuf[off + i] = __ddiv_rn(buf[off + i], rate);
+          return dbuf + off;
+        }
+        return a.b.vals_div + (p - a.b.vals);     // prior pool
+      };
+      ovd.A = divide(ovp.A, ovp.pa, ws.kin, ws.kin_d, pre);
+      ovd.B = divide(ovp.B, ovp.pb, ws.kout, ws.kout_d, dec);
+      __syncwarp();
+    }
     const LaneConst lc = lane_const(a.b.jump, g.inc, lane);
     if (lane < gn) {                             // stage the unit descriptors
       UnitCache c;
@@ -1127,14 +1162,14 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
         pending &= ~(1u << u);
         const UnitDesc d = ws.uc[u].d;
         const bool ov = has_ov && u == u0;
-        const Pools pl = pools_for(a, d, ov, ovp);
+        const Pools pd = pools_div(a, d, ov, ovd);
         unsigned targets = 0;
         if (!(d.flags & F_LLM))
-          ok = visit_strided<false>(a, d, succ_of(ws.uc[u]), pl, ws, m, g, lc, targets, lane);
+          ok = visit_strided<false>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, lc, targets, lane);
         else if ((d.flags & F_OWN) && !ov)
-          ok = visit_own(a, d, pl, ws, m, g, targets, lane);
+          ok = visit_own(a, d, pools_for(a, d, ov, ovp), pd, ws, m, g, targets, lane);
         else
-          ok = visit_strided<true>(a, d, succ_of(ws.uc[u]), pl, ws, m, g, lc, targets, lane);
+          ok = visit_strided<true>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, lc, targets, lane);
         pending |= __reduce_or_sync(kFull, targets);
       }
     }
@@ -1170,7 +1205,8 @@ static size_t walk_scratch(int n) {
 }
 
 static size_t scratch_per_warp(int n, int max_pairs) {
-  return (walk_scratch(n) + align16(size_t(max_pairs) * 16) + 64 + 255) & ~size_t(255);
+  // kept-pool buffers kin/kout, plus their rate-divided copies (walk kernel)
+  return (walk_scratch(n) + align16(size_t(max_pairs) * 32) + 64 + 255) & ~size_t(255);
 }
 
 // scratch = per-warp regions + 256 B (serial counter) + one int per job
@@ -1189,6 +1225,10 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
       n_samples > (1 << 19) || visit_cap < 0 || bucket_count < 1 || bucket_count > 1024 ||
       max_unit_k < 0 || max_unit_k > 1024 || max_pairs < 0) {
     set_error("pdg_mc_remaining_demand: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (n_samples <= kSmemWalks && !bank->vals_div) {
+    set_error("pdg_mc_remaining_demand: graph bank without vals_div");
     return PDG_EINVAL;
   }
   if (out->counts && out->stride < bucket_count) {

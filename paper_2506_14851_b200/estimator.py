@@ -34,7 +34,8 @@ class GraphBankC(C.Structure):
                 ("pool_off", C.c_void_p), ("pool_len", C.c_void_p),
                 ("succ_cum", C.c_void_p), ("succ_nxt", C.c_void_p), ("conds", C.c_void_p),
                 ("pairs", C.c_void_p), ("jump", C.c_void_p), ("prefill_rate", C.c_double),
-                ("decode_rate", C.c_double), ("succ_thr", C.c_void_p), ("max_units", C.c_int32)]
+                ("decode_rate", C.c_double), ("succ_thr", C.c_void_p), ("max_units", C.c_int32),
+                ("vals_div", C.c_void_p)]
 
 
 class JobsC(C.Structure):
@@ -105,12 +106,22 @@ class DemandEngine:
     def _bind(self):
         b = self.bank
         prefill_rate, decode_rate = self._rates
+        # pool values divided by their rate once (i/prefill, o/decode: the
+        # reference's own per-draw divisions, estimator.py:286, so exact)
+        # (tensor / tensor: torch turns division by a scalar into a
+        # multiplication by its reciprocal, which is not the same rounding)
+        k = b.vals_kind
+        pre = torch.full_like(b.vals, prefill_rate)
+        dec = torch.full_like(b.vals, decode_rate)
+        self.vals_div = torch.where(k == 1, b.vals / pre, torch.where(k == 2, b.vals / dec,
+                                                                      b.vals))
         self.c_bank = GraphBankC(
             _lib.ptr(b.units), _lib.ptr(b.graph_base), _lib.ptr(b.graph_n),
             _lib.ptr(b.unit_capacity), _lib.ptr(b.vals), _lib.ptr(b.pool_off),
             _lib.ptr(b.pool_len), _lib.ptr(b.succ_cum), _lib.ptr(b.succ_nxt),
             _lib.ptr(b.conds), _lib.ptr(b.pairs), _lib.ptr(self.jump),
-            float(prefill_rate), float(decode_rate), _lib.ptr(b.succ_thr), int(b.max_units))
+            float(prefill_rate), float(decode_rate), _lib.ptr(b.succ_thr), int(b.max_units),
+            _lib.ptr(self.vals_div))
         self.max_unit_k = b.max_unit_k
         self.max_pairs = b.max_pairs
 

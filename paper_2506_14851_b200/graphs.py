@@ -279,14 +279,16 @@ class GraphBank:
 
     def _compile(self, nm, g) -> dict:
         vals: list = []
+        kinds: list = []            # 0 duration, 1 input (/prefill), 2 output (/decode)
         units = []
         pools_off, pools_len = [], []
         succ_cum, succ_nxt = [], []
         conds, pairs = [], []
 
-        def push(xs) -> tuple[int, int]:
+        def push(xs, kind=0) -> tuple[int, int]:
             off = len(vals)
             vals.extend(float(x) for x in xs)
+            kinds.extend([kind] * len(xs))
             return off, len(xs)
 
         order = sorted(g.units)
@@ -311,8 +313,8 @@ class GraphBank:
                 flags |= F_LLM
                 a = list(u.input_dist.samples)
                 b = list(u.output_dist.samples)
-                d["a_off"], d["a_len"] = push(a)
-                d["b_off"], d["b_len"] = push(b)
+                d["a_off"], d["a_len"] = push(a, 1)
+                d["b_off"], d["b_len"] = push(b, 2)
                 d["pool_off"] = len(pools_off)
                 bn = binning(a, u.bucket_count)
                 if bn is not None:
@@ -325,7 +327,7 @@ class GraphBank:
                             r.output_len)
                     for kb in range(bn[2]):
                         xs = groups.get(kb, [])
-                        o, ln = push(xs) if xs else (0, 0)
+                        o, ln = push(xs, 2) if xs else (0, 0)
                         pools_off.append(o)
                         pools_len.append(ln)
             else:
@@ -371,6 +373,7 @@ class GraphBank:
         return {"units": np.array(units, dtype=UNIT_DTYPE) if units else
                 np.zeros(0, UNIT_DTYPE),
                 "vals": np.asarray(vals, dtype=np.float64),
+                "kinds": np.asarray(kinds, dtype=np.int8),
                 "pools_off": np.asarray(pools_off, dtype=np.int64),
                 "pools_len": np.asarray(pools_len, dtype=np.int64),
                 "succ_cum": np.asarray(succ_cum, dtype=np.float64),
@@ -384,6 +387,7 @@ class GraphBank:
     def _place(self) -> None:
         """Concatenate the segments (rebasing their local offsets) and upload."""
         units, vals, po, pl, sc, sn, cs, ps, caps = [], [], [], [], [], [], [], [], []
+        kinds = []
         gbase, gn = [], []
         nv = npool = nsucc = ncond = npair = nunit = 0
         for nm in self.names:
@@ -399,6 +403,7 @@ class GraphBank:
             c["pair_off"] += npair
             units.append(u)
             vals.append(sg["vals"])
+            kinds.append(sg["kinds"])
             po.append(np.where(sg["pools_len"] > 0, sg["pools_off"] + nv, 0))
             pl.append(sg["pools_len"])
             sc.append(sg["succ_cum"])
@@ -415,6 +420,7 @@ class GraphBank:
             npair += len(sg["pairs"])
             nunit += len(u)
         cat = lambda xs, dt: np.concatenate(xs) if xs else np.zeros(0, dt)  # noqa: E731
+        self.host_kinds = cat(kinds, np.int8)
         self._finish(self.device, cat(units, UNIT_DTYPE), cat(vals, np.float64), gbase, gn,
                      caps, cat(po, np.int64), cat(pl, np.int64), cat(sc, np.float64),
                      cat(sn, np.int64), list(cat(cs, COND_DTYPE)), list(cat(ps, PAIR_DTYPE)))
@@ -432,6 +438,7 @@ class GraphBank:
         self.unit_order = unit_order or {}
         self.graphs = {}
         self.device = device
+        self.host_kinds = np.zeros(len(vals), dtype=np.int8)
         self._finish(device, units, vals, graph_base, graph_n, unit_capacity, [], [],
                      succ_cum, succ_nxt, [], [])
         return self
@@ -451,6 +458,9 @@ class GraphBank:
         self.n_units = len(units)
         self.units = t(units.view(np.uint8).reshape(-1), np.uint8)
         self.vals = t(vals, np.float64)
+        kinds = getattr(self, "host_kinds", None)
+        self.vals_kind = t(kinds if kinds is not None and len(kinds) == len(vals)
+                           else np.zeros(len(vals), np.int8), np.int8)
         self.graph_base = t(gbase, np.int32)
         self.graph_n = t(gn, np.int32)
         self.unit_capacity = t(caps, np.int32)
