@@ -962,38 +962,71 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
 }
 
 // own-input LLM unit: outputs drawn per input bucket, buckets ascending,
-// walks in order within a bucket (estimator.py:275-283)
-__device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& pl,
-                          const Pools& pd, const WalkState& ws, uint32_t m, Stream& g, unsigned& targets,
-                          int lane) {
-  const uint64_t* jt = a.b.jump;
+// walks in order within a bucket (estimator.py:275-283).  The segment is
+// [A halves | B halves in (bucket, rank) order | uniforms]; lanes decode it
+// strided like visit_strided, in three phases: the A words (input draws,
+// their buckets and bucket counts), a counting sort that maps each B half to
+// its member, the B words, then the uniforms.  The half shared by the last A
+// word and the first B draw, and numpy's buffered half, are placed by lane 0.
+__device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab& sc,
+                          const Pools& pl, const Pools& pd, const WalkState& ws, uint32_t m,
+                          Stream& g, const LaneConst& lc, unsigned& targets, int lane) {
   const unsigned lt = lanemask_lt();
-  SuccTab sc;
-  sc.load(a, d);
-  const uint32_t per = (m + 31) >> 5;
-  const uint32_t k0 = min(lane * per, m), k1 = min(k0 + per, m);
-  const uint32_t c1 = pl.pa > 1 ? m : 0u;
-  bool rej = false;
-  Cursor ca{g.s, 0xffffffffu, 0}, cb{g.s, 0xffffffffu, 0};
   const int K = d.ib_k;
   uint32_t* cnt = ws.cnt;
   uint32_t* start = ws.cnt + a.max_unit_k;
   uint32_t* effo = ws.cnt + 2 * a.max_unit_k;
+  uint16_t* effl = ws.osrt;                       // B position -> member rank
+  const uint32_t mA = pl.pa > 1 ? m : 0u;
+  const uint32_t pin = g.pend ? 1u : 0u;
+  const uint32_t wA = mA ? (mA - pin + 1) >> 1 : 0u;
+  // bucket_index of an input draw (distributions.py:107-118), bucket width hoisted
+  const double blo = d.ib_lo, bhi = d.ib_hi;
+  const double bw = __ddiv_rn(dsub(bhi, blo), small_int_to_double(K));
+  auto bucket = [&](double v) -> int {
+    if (bhi == blo || v <= blo) return 0;
+    if (v >= bhi) return K - 1;
+    const int i = __double2int_rz(__ddiv_rn(dsub(v, blo), bw));
+    return i < K - 1 ? i : K - 1;
+  };
+  bool rej = false;
+  auto a_draw = [&](uint32_t r, uint32_t h) {
+    const uint32_t ia = lemire(h, uint32_t(pl.pa), rej);
+    ws.tmp[r] = pd.A[ia];                         // i / prefill_rate
+    const int bb = bucket(pl.A[ia]);              // the raw input picks the bucket
+    ws.bkt[r] = uint16_t(bb);
+    atomicAdd(&cnt[bb], 1u);
+  };
   for (int b = lane; b < K; b += 32) cnt[b] = 0;
   __syncwarp();
-  for (uint32_t k = k0; k < k1; ++k) {
-    const uint32_t ia = pl.pa > 1 ? lemire(cursor_half(ca, jt, g, k), uint32_t(pl.pa), rej) : 0u;
-    const double iv = pl.A[ia];                  // raw input picks the bucket
-    ws.tmp[k] = pd.A[ia];                        // i / prefill_rate
-    const int bb = bucket_of(iv, d.ib_lo, d.ib_hi, K);
-    ws.bkt[k] = uint16_t(bb);
-    atomicAdd(&cnt[bb], 1u);
+  const ulonglong2 ap =
+      __ldg(reinterpret_cast<const ulonglong2*>(a.b.jump) + 2 * (2048 + lane));
+  U128 st = add128(mul128(g.s, U128{ap.x, ap.y}), lc.cl);   // one stride before word lane
+  uint32_t pend_hi = 0;
+  uint32_t q = lane;
+  for (; q < wA; q += 32) {                       // phase A: input draws
+    st = pcg_stride32(st, lc.c32);
+    const uint64_t wd = pcg_out(st);
+    const uint32_t R = 2u * q + pin;
+    a_draw(R, uint32_t(wd));
+    if (R + 1 < mA) a_draw(R + 1, uint32_t(wd >> 32));
+    else pend_hi = uint32_t(wd >> 32);            // half mA: first B draw or leftover
+  }
+  if (mA && pin && lane == 0) a_draw(0, g.pv);
+  if (!mA) {                                      // single-value input pool
+    const int bb = bucket(pl.A[0]);
+    for (uint32_t k = lane; k < m; k += 32) {
+      ws.tmp[k] = pd.A[0];
+      ws.bkt[k] = uint16_t(bb);
+    }
+    if (lane == 0) cnt[bb] = m;
   }
   __syncwarp();
+  // bucket layout: all members by bucket (start), drawing members (effo)
   const int perb = (K + 31) >> 5;
   uint32_t la = 0, le = 0;
-  for (int q = 0; q < perb; ++q) {
-    const int bb = lane * perb + q;
+  for (int t = 0; t < perb; ++t) {
+    const int bb = lane * perb + t;
     if (bb < K) {
       const int pln = a.b.pool_len[d.pool_off + bb];
       const int P = pln > 0 ? pln : pl.pb;
@@ -1005,8 +1038,8 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& p
   const uint32_t eff_total = __shfl_sync(kFull, ie_incl, 31);
   uint32_t ra = ia_incl - la, re = ie_incl - le;
   __syncwarp();
-  for (int q = 0; q < perb; ++q) {
-    const int bb = lane * perb + q;
+  for (int t = 0; t < perb; ++t) {
+    const int bb = lane * perb + t;
     if (bb < K) {
       const int pln = a.b.pool_len[d.pool_off + bb];
       const int P = pln > 0 ? pln : pl.pb;
@@ -1019,7 +1052,9 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& p
     }
   }
   __syncwarp();
-  for (uint32_t base = 0; base < m; base += 32) {   // stable counting sort by bucket
+  // stable counting sort by bucket: drawing members get their B position,
+  // members of single-value pools take value 0 now
+  for (uint32_t base = 0; base < m; base += 32) {
     const uint32_t k = base + lane;
     const bool valid = k < m;
     const int bb = valid ? int(ws.bkt[k]) : (0x10000 + lane);
@@ -1029,35 +1064,62 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const Pools& p
     __syncwarp();
     if (valid && (__ffs(peers) - 1) == lane) cnt[bb] = dest + __popc(peers);
     __syncwarp();
-    if (valid) ws.osrt[dest + __popc(peers & lt)] = uint16_t(k);
+    if (valid) {
+      const int pln = a.b.pool_len[d.pool_off + bb];
+      if ((pln > 0 ? pln : pl.pb) > 1) {
+        effl[effo[bb] + dest + __popc(peers & lt) - start[bb]] = uint16_t(k);
+      } else {
+        const double* pool = pln > 0 ? a.b.vals_div + a.b.pool_off[d.pool_off + bb] : pd.B;
+        ws.tmp[k] = dadd(ws.tmp[k], pool[0]);
+      }
+    }
   }
   __syncwarp();
-  for (uint32_t j = k0; j < k1; ++j) {
-    const uint32_t k = ws.osrt[j];
+  const uint32_t C = mA + eff_total;
+  const uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
+  auto b_draw = [&](uint32_t j, uint32_t h) {
+    const uint32_t k = effl[j];
     const int bb = ws.bkt[k];
     const int pln = a.b.pool_len[d.pool_off + bb];
     const double* pool = pln > 0 ? a.b.vals_div + a.b.pool_off[d.pool_off + bb] : pd.B;
     const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
-    const uint32_t pos = c1 + effo[bb] + (j - start[bb]);
-    const uint32_t ob = P > 1 ? lemire(cursor_half(cb, jt, g, pos), P, rej) : 0u;
-    ws.tmp[k] = dadd(ws.tmp[k], pool[ob]);      // i/prefill + o/decode
+    ws.tmp[k] = dadd(ws.tmp[k], pool[lemire(h, P, rej)]);   // + o / decode_rate
+  };
+  const uint32_t sh = __shfl_sync(kFull, pend_hi, (wA - 1) & 31u);
+  for (; q < wb; q += 32) {                       // phase B: output draws
+    st = pcg_stride32(st, lc.c32);
+    const uint64_t wd = pcg_out(st);
+    const uint32_t R = 2u * q + pin;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t r = R + t, h = t ? uint32_t(wd >> 32) : uint32_t(wd);
+      if (r < C) b_draw(r - mA, h);
+      else pend_hi = h;
+    }
+  }
+  if (eff_total && lane == 0) {                   // B draw 0 on a half decoded earlier
+    if (!mA && pin) b_draw(0, g.pv);
+    else if (mA && ((mA - pin) & 1u)) b_draw(0, sh);
   }
   if (__any_sync(kFull, rej)) return false;
-  const uint32_t C = c1 + eff_total;
-  const uint32_t F = C == 0 ? 0u : C - (g.pend ? 1u : 0u);
-  const uint32_t words = (F + 1) >> 1;
-  close_group(g, C, ca, cb);
   __syncwarp();
-  Cursor cd{g.s, 0xffffffffu, 0};
-  for (uint32_t k = k0; k < k1; ++k) {
-    const uint64_t uw = cursor_word(cd, jt, g.inc, words + k);
+  const uint32_t W = wb + m;
+  for (; q < W; q += 32) {                        // random(m): successor + total
+    st = pcg_stride32(st, lc.c32);
+    const uint32_t k = q - wb;
+    const int v = sc.ns <= 3 ? sc.next3(pcg_out(st)) : sc.next(a, d, pcg_out(st));
     const uint32_t w = ws.mem[k];
-    arrive(ws, w, sc.next(a, d, uw), targets);
     ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
+    arrive(ws, w, v, targets);
   }
-  const unsigned last_lane = (m - 1) / per;
-  g.s.lo = __shfl_sync(kFull, cd.st.lo, last_lane);
-  g.s.hi = __shfl_sync(kFull, cd.st.hi, last_lane);
+  const unsigned last = (W - 1) & 31u;
+  g.s.lo = __shfl_sync(kFull, st.lo, last);
+  g.s.hi = __shfl_sync(kFull, st.hi, last);
+  const uint32_t pv = __shfl_sync(kFull, pend_hi, (wb - 1) & 31u);
+  if (C) {
+    g.pend = ((pin + C) & 1u) != 0;
+    if (g.pend) g.pv = pv;
+  }
   __syncwarp();
   return true;
 }
@@ -1167,7 +1229,8 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
         if (!(d.flags & F_LLM))
           ok = visit_strided<false>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, lc, targets, lane);
         else if ((d.flags & F_OWN) && !ov)
-          ok = visit_own(a, d, pools_for(a, d, ov, ovp), pd, ws, m, g, targets, lane);
+          ok = visit_own(a, d, succ_of(ws.uc[u]), pools_for(a, d, ov, ovp), pd, ws, m, g, lc,
+                         targets, lane);
         else
           ok = visit_strided<true>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, lc, targets, lane);
         pending |= __reduce_or_sync(kFull, targets);
