@@ -108,6 +108,18 @@ int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
               int32_t begin_bit, void* temp, size_t temp_bytes, void* stream);
 
 
+/* K5b  incremental order after re-scoring rows[0..m) (distinct): the previous
+ * order (sorted_*_in, produced by pdg_order with begin_bit 0 or by this call)
+ * minus those rows, merged with their new keys (keys[] holds every row's
+ * packed key).  Same result as a full pdg_order (keys are unique).  mark: a
+ * caller-owned zeroed uint8[n] (left zeroed).  temp:
+ * pdg_order_update_temp_bytes(n, m) bytes. */
+size_t pdg_order_update_temp_bytes(int64_t n, int64_t m);
+int pdg_order_update(const uint64_t* keys, const uint64_t* sorted_keys_in,
+                     const uint32_t* sorted_slots_in, int64_t n, const int32_t* rows, int64_t m,
+                     uint8_t* mark, uint64_t* sorted_keys_out, uint32_t* sorted_slots_out,
+                     void* temp, size_t temp_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * K2 + K3 + a4  demand engine.
  * Replaces pdgsim.estimator.monte_carlo_remaining_demand (estimator.py:305-362)

@@ -42,7 +42,12 @@ class RefinementStream:
         self._temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
         self.order_keys = torch.empty(self.n, dtype=torch.int64, device=dev)
         self.order_slots = torch.empty(self.n, dtype=torch.int32, device=dev)
+        self._keys2 = torch.empty_like(self.order_keys)
+        self._slots2 = torch.empty_like(self.order_slots)
+        self._mark = torch.zeros(self.n, dtype=torch.uint8, device=dev)
         self._slots = torch.arange(self.n, dtype=torch.int32, device=dev)
+        self._utemp = None
+        self._ordered = False          # order_* hold the order of the current keys
 
     def process(self, app: torch.Tensor, next_unit: torch.Tensor, seed: torch.Tensor,
                 obs_unit: Optional[torch.Tensor] = None, obs_val: Optional[torch.Tensor] = None,
@@ -65,15 +70,34 @@ class RefinementStream:
             self.q.est_age.index_copy_(0, app.long(), attained)
             self.q.age.index_copy_(0, app.long(), attained)
         self.q.score(self.penalty, rows=app, stream=stream)
-        if resort:
+        if resort and self._ordered:
+            self._update_order(app, stream)     # K5b: merge the batch into the order
+        elif resort:
             self.order(stream)
+        else:
+            self._ordered = False
 
     def order(self, stream=None) -> torch.Tensor:
-        """Global order of the whole queue (stable 32-bit key sort; queue rows
-        are in arrival order)."""
+        """Global order of the whole queue: full sort of the packed
+        (key, arrival position) words."""
         L = _lib.lib()
         _lib.check(L.pdg_order(_lib.ptr(self.q.keys), _lib.ptr(self.order_keys),
-                               _lib.ptr(self._slots), _lib.ptr(self.order_slots), self.n, 32,
+                               _lib.ptr(self._slots), _lib.ptr(self.order_slots), self.n, 0,
                                _lib.ptr(self._temp), self._temp.numel(),
                                _lib.stream_ptr(stream)), "pdg_order")
+        self._ordered = True
         return self.order_slots
+
+    def _update_order(self, rows: torch.Tensor, stream=None) -> None:
+        L = _lib.lib()
+        m = int(rows.numel())
+        need = int(L.pdg_order_update_temp_bytes(self.n, m))
+        if self._utemp is None or self._utemp.numel() < need:
+            self._utemp = torch.empty(need, dtype=torch.uint8, device=self.order_keys.device)
+        _lib.check(L.pdg_order_update(
+            _lib.ptr(self.q.keys), _lib.ptr(self.order_keys), _lib.ptr(self.order_slots), self.n,
+            _lib.ptr(rows), m, _lib.ptr(self._mark), _lib.ptr(self._keys2),
+            _lib.ptr(self._slots2), _lib.ptr(self._utemp), self._utemp.numel(),
+            _lib.stream_ptr(stream)), "pdg_order_update")
+        self.order_keys, self._keys2 = self._keys2, self.order_keys
+        self.order_slots, self._slots2 = self._slots2, self.order_slots

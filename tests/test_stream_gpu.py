@@ -45,8 +45,10 @@ def test_event_stream_parity(kb_graphs):
         st.process(t(ev["app"][sl], torch.int32), t(ev["next"][sl], torch.int32),
                    t(ev["seed"][sl], torch.int64), obs_unit[sl],
                    t(ev["obs"][sl], torch.float64), t(np.full(500, 3.0), torch.float64))
-    order = st.order().cpu().numpy()
+    inc = st.order_slots.clone()                         # K5b: merged batch by batch
+    order = st.order().cpu().numpy()                     # K5: full re-sort
     torch.cuda.synchronize()
+    np.testing.assert_array_equal(inc.cpu().numpy(), order)
     keys = hq.key_f32[:n].cpu().numpy()
     assert sorted(order.tolist()) == list(range(n))
     assert np.all(np.diff(keys[order]) >= 0)

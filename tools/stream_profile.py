@@ -45,6 +45,7 @@ def main():
          for k, v in (("app", ev["app"]), ("next", ev["next"]), ("comp", ev["completed"]),
                       ("obs", ev["obs"]), ("seed", ev["seed"]))}
     att = torch.full((n_events,), 5.0, dtype=torch.float64, device=dev)
+    st.order()
     T = {"engine": [], "k1": [], "sort": []}
     for i in range(n_events // batch):
         sl = slice(i * batch, (i + 1) * batch)
@@ -60,7 +61,7 @@ def main():
         hq.age.index_copy_(0, app.long(), att[sl])
         hq.score(2.0, rows=app)
         ev_[2].record()
-        st.order()
+        st._update_order(app)
         ev_[3].record()
         torch.cuda.synchronize()
         if i >= 2:
