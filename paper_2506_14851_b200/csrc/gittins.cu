@@ -446,7 +446,9 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
   if (blocks > cap) blocks = cap;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t maxb = rows->stride;   // buckets per row are bounded by the stride
-  if (maxb == 256) {
+  // lane-per-row tiles pay off once every SM has tiles to stream; small
+  // (incremental) batches take the warp-per-row kernel's lower latency
+  if (maxb == 256 && n >= int64_t(sm_count()) * 32 * 4) {
     const size_t smem = size_t(kRowWarps) * kTileU4 * sizeof(uint4);
     static bool attr = false;
     if (!attr) {
