@@ -749,6 +749,7 @@ struct WalkState {
   double* kout;
   double* kin_d;     // [max_pairs] the same divided by prefill / decode rate
   double* kout_d;
+  U128* cl;          // [32] per-lane stride constant K_l * inc (shared memory)
 };
 
 // pool values as the stage time uses them: LLM inputs / prefill_rate, LLM
@@ -776,7 +777,7 @@ __host__ __device__ inline size_t walk_union_bytes(int counters) {
 }
 __host__ __device__ inline size_t walk_smem_bytes(int counters, int units) {
   return walk_union_bytes(counters) + size_t(kSmemWalks) * 10 + size_t(units) * kWalkWords * 4 +
-         size_t(units) * 112;
+         size_t(units) * 112 + 32 * sizeof(U128);
 }
 // global scratch per warp: [own-input arrays] [K3 pairs]
 __host__ __device__ inline size_t walk_gmem_bytes() {
@@ -895,7 +896,7 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
   const uint32_t W = wb + m;
   const ulonglong2 ap =
       __ldg(reinterpret_cast<const ulonglong2*>(a.b.jump) + 2 * (2048 + lane));
-  U128 st = add128(mul128(g.s, U128{ap.x, ap.y}), lc.cl);   // one stride before word lane
+  U128 st = add128(mul128(g.s, U128{ap.x, ap.y}), ws.cl[lane]);   // one stride before word lane
   bool rej = false;
   uint32_t pend_hi = 0;
   uint32_t q = lane;
@@ -1001,7 +1002,7 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
   __syncwarp();
   const ulonglong2 ap =
       __ldg(reinterpret_cast<const ulonglong2*>(a.b.jump) + 2 * (2048 + lane));
-  U128 st = add128(mul128(g.s, U128{ap.x, ap.y}), lc.cl);   // one stride before word lane
+  U128 st = add128(mul128(g.s, U128{ap.x, ap.y}), ws.cl[lane]);   // one stride before word lane
   uint32_t pend_hi = 0;
   uint32_t q = lane;
   for (; q < wA; q += 32) {                       // phase A: input draws
@@ -1148,6 +1149,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
   ws.mem = reinterpret_cast<uint16_t*>(ws.tot + kSmemWalks);
   ws.bits = reinterpret_cast<uint32_t*>(ws.mem + kSmemWalks);
   ws.uc = reinterpret_cast<UnitCache*>(ws.bits + a.b.max_units * kWalkWords);
+  ws.cl = reinterpret_cast<U128*>(ws.uc + a.b.max_units);
   ws.tmp = reinterpret_cast<double*>(gs);
   ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + kSmemWalks);
   ws.osrt = ws.bkt + kSmemWalks;
@@ -1192,6 +1194,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
       __syncwarp();
     }
     const LaneConst lc = lane_const(a.b.jump, g.inc, lane);
+    ws.cl[lane] = lc.cl;                         // reloaded once per visit
     if (lane < gn) {                             // stage the unit descriptors
       UnitCache c;
       c.d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + lane];
