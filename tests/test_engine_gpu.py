@@ -143,12 +143,12 @@ def test_random_graphs_vs_oracle(engine, kb_graphs):
         assert got[i][1] == want.capped
 
 
-def _rejecting_seed(P, n, steps):
+def _rejecting_seed(P, n, steps, window=200):
     """A seed whose stream hits a Lemire rejection inside the u32 halves the
     single-unit self-loop walk consumes (n walks, `steps` visits each)."""
     thr = (2**32 - P) % P
     per_step = n // 2 + (n % 2) + n       # words per step (halves region first)
-    for seed in range(200):
+    for seed in range(window):
         raw = np.random.default_rng(seed).bit_generator.random_raw(per_step * steps)
         for t in range(steps):
             base = t * per_step
@@ -160,13 +160,14 @@ def _rejecting_seed(P, n, steps):
     return None
 
 
-def test_lemire_rejection_replayed_exactly():
+@pytest.mark.parametrize("n", [4000, 512, 96])      # mc_engine_kernel / mc_walk_kernel
+def test_lemire_rejection_replayed_exactly(n):
     """numpy rejects a bounded draw with probability < P/2^32; the engine's
-    warp vote must detect it and replay the visit sequentially."""
+    warp vote must detect it and replay the application sequentially."""
     from paper_2506_14851_b200.estimator import DemandEngine
     from paper_2506_14851_b200.graphs import graph_from_kb
     P = max(range(900, 1001), key=lambda p: (2**32 - p) % p)
-    n, steps = 4000, 64
+    steps = 64
     rng = np.random.default_rng(5)
     durs = rng.uniform(1.0, 2.0, P)
     doc = {"app_id": "rej", "entry_unit": "a", "units": [{
@@ -174,7 +175,7 @@ def test_lemire_rejection_replayed_exactly():
         "capacity": 1000, "bucket_count": 10,
         "records": [{"trial_id": t, "duration": float(durs[t]), "next_unit": "a"}
                     for t in range(P)]}]}
-    seed = _rejecting_seed(P, n, steps)
+    seed = _rejecting_seed(P, n, steps, window=200 if n >= 4000 else 6000)
     if seed is None:
         pytest.skip("no rejecting seed found in the scan window")
     # the scan assumes a pure halves/doubles layout without earlier rejections;
