@@ -271,7 +271,16 @@ typedef struct {
   const int32_t* succ_nxt;    /* local unit index of each successor            */
   const double* succ_p;       /* branch probability (pdgraph.py:182-194)       */
   const int32_t* unit_type;   /* [U] warm-content backend type, -1 = none      */
+  const int32_t* win_idx;     /* optional [U, n_windows]: pdg_prewarm_window_index */
+                              /* of the windows passed to pdg_prewarm_need       */
 } pdg_prewarm_tables;
+
+/* lower_bound(svc_sorted[u], windows[k]) for every unit and window: lets
+ * pdg_prewarm_need skip its per-application searches (a sample below W_k can
+ * still complete at now + W_k after rounding; the kernel walks those back). */
+int pdg_prewarm_window_index(const pdg_prewarm_tables* tables, int32_t n_units,
+                             const double* windows, int32_t n_windows, int32_t* out,
+                             void* stream);
 
 int pdg_prewarm_need(const pdg_prewarm_tables* tables, const int32_t* graph,
                      const int32_t* unit, const double* now, int64_t n,

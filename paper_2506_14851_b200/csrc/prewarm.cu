@@ -141,6 +141,8 @@ struct NeedArgs {
   int64_t n;
   float* need;                  // [N, T, K] optional
   double* agg;                  // [T, K] optional, sum over applications
+  const int32_t* win_idx;       // [U, K] optional: lower_bound(svc[u], W_k)
+  int stage_n;                  // service samples staged per warp (0 with win_idx)
 };
 
 // first index i in the ascending array with now + s[i] >= x  (exact f64)
@@ -162,10 +164,12 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
   extern __shared__ double nsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int TK = a.n_types * a.n_windows;
-  double* stage = nsm + size_t(wib) * kNeedStage;
-  double* wagg = nsm + size_t(kNeedWarps) * kNeedStage + size_t(wib) * TK;
-  if (a.agg)
-    for (int i = lane; i < TK; i += 32) wagg[i] = 0.0;
+  double* stage = nsm + size_t(wib) * a.stage_n;
+  double* cagg = nsm + size_t(kNeedWarps) * a.stage_n;   // [T][K] of this CTA
+  if (a.agg) {
+    for (int i = threadIdx.x; i < TK; i += blockDim.x) cagg[i] = 0.0;
+    __syncthreads();
+  }
   const int64_t gw = int64_t(blockIdx.x) * kNeedWarps + wib;
   const int64_t nw = int64_t(gridDim.x) * kNeedWarps;
   const int kwin = lane < a.n_windows ? lane : -1;
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
     const int n = a.svc_len[u];
     const double* gsrc = a.svc_sorted + a.svc_off[u];
     const double* s = gsrc;
-    if (n <= kNeedStage) {                           // coalesced stage, then LDS searches
+    if (n <= a.stage_n) {                            // coalesced stage, then LDS searches
       for (int i = lane; i < n; i += 32) stage[i] = gsrc[i];
       __syncwarp();
       s = stage;
@@ -194,8 +198,17 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
     float pneed = 0.f;                               // P(completion < now + W_k)
     if (kwin >= 0 && m > 0) {
       const double x = dadd(now, wk);
-      const int cnt_ge = (n - base) - lower_bound_abs(s + base, n - base, now, x);
-      pneed = 1.f - __fdiv_rn(float(cnt_ge), float(m));
+      int j;
+      if (a.win_idx) {
+        // samples >= W_k complete at >= now + W_k (rounding is monotone); a
+        // sample just below W_k can round up onto it: walk back over those
+        j = a.win_idx[int64_t(u) * a.n_windows + kwin];
+        while (j > 0 && dadd(now, s[j - 1]) >= x) --j;
+        j = j > base ? j : base;
+      } else {
+        j = base + lower_bound_abs(s + base, n - base, now, x);
+      }
+      pneed = 1.f - __fdiv_rn(float(n - j), float(m));
     }
     // up to 4 successors; successors of equal type are merged first
     const int so = a.succ_off[u];
@@ -213,31 +226,26 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
     if (t3 >= 0 && t3 == t1) { f1 += f3; t3 = -1; }
     if (t3 >= 0 && t3 == t2) { f2 += f3; t3 = -1; }
     if (kwin >= 0) {
-      if (a.need) {                                  // dense row: zeros, then the <= 4 types
+      if (a.need) {                                  // dense row, each element once
         float* row = a.need + app * int64_t(TK) + kwin;
-        for (int t = 0; t < a.n_types; ++t) __stcs(row + t * a.n_windows, 0.f);
-        if (t0 >= 0) __stcs(row + t0 * a.n_windows, f0);
-        if (t1 >= 0) __stcs(row + t1 * a.n_windows, f1);
-        if (t2 >= 0) __stcs(row + t2 * a.n_windows, f2);
-        if (t3 >= 0) __stcs(row + t3 * a.n_windows, f3);
+        for (int t = 0; t < a.n_types; ++t) {
+          const float v = t == t0 ? f0 : t == t1 ? f1 : t == t2 ? f2 : t == t3 ? f3 : 0.f;
+          __stcs(row + t * a.n_windows, v);
+        }
       }
       if (a.agg) {
-        if (t0 >= 0) wagg[t0 * a.n_windows + kwin] += f0;
-        if (t1 >= 0) wagg[t1 * a.n_windows + kwin] += f1;
-        if (t2 >= 0) wagg[t2 * a.n_windows + kwin] += f2;
-        if (t3 >= 0) wagg[t3 * a.n_windows + kwin] += f3;
+        if (t0 >= 0) atomicAdd(cagg + t0 * a.n_windows + kwin, double(f0));
+        if (t1 >= 0) atomicAdd(cagg + t1 * a.n_windows + kwin, double(f1));
+        if (t2 >= 0) atomicAdd(cagg + t2 * a.n_windows + kwin, double(f2));
+        if (t3 >= 0) atomicAdd(cagg + t3 * a.n_windows + kwin, double(f3));
       }
     }
     __syncwarp();
   }
   if (a.agg) {
     __syncthreads();
-    for (int i = threadIdx.x; i < TK; i += blockDim.x) {
-      double acc = 0.0;
-      for (int q = 0; q < kNeedWarps; ++q)
-        acc += nsm[size_t(kNeedWarps) * kNeedStage + size_t(q) * TK + i];
-      if (acc != 0.0) atomicAdd(a.agg + i, acc);
-    }
+    for (int i = threadIdx.x; i < TK; i += blockDim.x)
+      if (cagg[i] != 0.0) atomicAdd(a.agg + i, cagg[i]);
   }
 }
 
@@ -265,6 +273,41 @@ extern "C" int pdg_plan_prewarm(const double* pool, const int32_t* off, const in
   return launch_status("prewarm_plan_kernel");
 }
 
+__global__ void window_index_kernel(const double* __restrict__ svc, const int32_t* __restrict__ off,
+                                    const int32_t* __restrict__ len, int32_t n_units,
+                                    const double* __restrict__ windows, int32_t k,
+                                    int32_t* __restrict__ out) {
+  const int64_t total = int64_t(n_units) * k;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int u = int(i / k), w = int(i % k);
+    const double* s = svc + off[u];
+    const double x = windows[w];
+    int lo = 0, hi = len[u];
+    while (lo < hi) {                                // first s >= W_k
+      const int mid = (lo + hi) >> 1;
+      if (s[mid] >= x) hi = mid; else lo = mid + 1;
+    }
+    out[i] = lo;
+  }
+}
+
+extern "C" int pdg_prewarm_window_index(const pdg_prewarm_tables* t, int32_t n_units,
+                                        const double* windows, int32_t n_windows,
+                                        int32_t* out, void* stream) {
+  if (!t || n_units < 0 || n_windows < 1 || n_windows > 32 || !windows || !out) {
+    set_error("pdg_prewarm_window_index: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (n_units == 0) return PDG_OK;
+  int64_t blocks = (int64_t(n_units) * n_windows + 255) / 256;
+  const int64_t cap = int64_t(sm_count()) * 8;
+  if (blocks > cap) blocks = cap;
+  window_index_kernel<<<unsigned(blocks), 256, 0, (cudaStream_t)stream>>>(
+      t->svc_sorted, t->svc_off, t->svc_len, n_units, windows, n_windows, out);
+  return launch_status("window_index_kernel");
+}
+
 extern "C" int pdg_prewarm_need(const pdg_prewarm_tables* t, const int32_t* graph,
                                 const int32_t* unit, const double* now, int64_t n,
                                 const double* windows, int32_t n_windows, int32_t n_types,
@@ -277,9 +320,9 @@ extern "C" int pdg_prewarm_need(const pdg_prewarm_tables* t, const int32_t* grap
   if (n == 0) return PDG_OK;
   NeedArgs a{t->svc_sorted, t->svc_off, t->svc_len, t->graph_base, t->succ_off, t->succ_len,
              t->succ_nxt, t->succ_p, t->unit_type, graph, unit, now, windows, n_types,
-             n_windows, n, need, agg};
-  const size_t smem = sizeof(double) * size_t(kNeedWarps) *
-                      (kNeedStage + (agg ? size_t(n_types) * n_windows : 0));
+             n_windows, n, need, agg, t->win_idx, t->win_idx ? 0 : kNeedStage};
+  const size_t smem = sizeof(double) * (size_t(kNeedWarps) * a.stage_n +
+                                        (agg ? size_t(n_types) * n_windows : 0));
   cudaError_t e = cudaFuncSetAttribute(prewarm_need_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(prewarm_need_kernel)");

@@ -101,7 +101,7 @@ def plan_prewarm(completion_dist, p_s: float, t_p: float, knob: float, now: floa
 class PrewarmTablesC(C.Structure):
     _fields_ = [(nm, C.c_void_p) for nm in ("svc_sorted", "svc_off", "svc_len", "graph_base",
                                             "succ_off", "succ_len", "succ_nxt", "succ_p",
-                                            "unit_type")]
+                                            "unit_type", "win_idx")]
 
 
 class PrewarmTables:
@@ -124,7 +124,10 @@ class PrewarmTables:
                       succ_off=t(succ_off, np.int32), succ_len=t(succ_len, np.int32),
                       succ_nxt=t(succ_nxt, np.int32), succ_p=t(succ_p, np.float64),
                       unit_type=t(unit_type, np.int32))
-        self.c = PrewarmTablesC(*[_lib.ptr(self.t[nm]) for nm, _ in PrewarmTablesC._fields_])
+        self.c = PrewarmTablesC(*[_lib.ptr(self.t[nm]) if nm in self.t else None
+                                  for nm, _ in PrewarmTablesC._fields_])
+        self.n_units = int(np.asarray(svc_len).size)
+        self._win = None            # (windows, index) cache for pdg_prewarm_window_index
 
     @classmethod
     def from_graphs(cls, graphs: dict, prefill_rate=10000.0, decode_rate=50.0, device="cuda"):
@@ -162,12 +165,26 @@ class PrewarmTables:
         tb.type_ids = types
         return tb
 
+    def _window_index(self, windows, stream=None):
+        if self._win is None or not torch.equal(self._win[0], windows):
+            idx = torch.empty(max(self.n_units, 1) * int(windows.numel()), dtype=torch.int32,
+                              device=self.device)
+            self.c.win_idx = None
+            _lib.check(_lib.lib().pdg_prewarm_window_index(
+                C.byref(self.c), self.n_units, _lib.ptr(windows), int(windows.numel()),
+                _lib.ptr(idx), _lib.stream_ptr(stream)), "pdg_prewarm_window_index")
+            self._win = (windows.clone(), idx)
+        return self._win[1]
+
     def need(self, graph_idx, unit_idx, now, windows, *, dense=True, aggregate=True,
-             out=None, stream=None):
-        """need[N, T, K] float32 (dense) and/or agg[T, K] float64 over the queue."""
+             out=None, window_index=True, stream=None):
+        """need[N, T, K] float32 (dense) and/or agg[T, K] float64 over the queue.
+        window_index: per-(unit, window) lower bounds computed once per window
+        grid instead of a binary search per application."""
         n = int(graph_idx.numel())
         K = int(windows.numel())
         dev = self.device
+        self.c.win_idx = _lib.ptr(self._window_index(windows, stream)) if window_index else None
         need = out if out is not None else (
             torch.empty((n, self.n_types, K), dtype=torch.float32, device=dev) if dense else None)
         agg = torch.zeros((self.n_types, K), dtype=torch.float64, device=dev) if aggregate else None

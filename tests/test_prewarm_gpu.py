@@ -79,9 +79,18 @@ def test_need_grid_vs_oracle(kb_graphs):
     g = torch.tensor([j[0] for j in jobs], dtype=torch.int32, device="cuda")
     u = torch.tensor([j[1] for j in jobs], dtype=torch.int32, device="cuda")
     nowv = rng.uniform(0, 50, len(jobs))
+    nowv[::3] = rng.uniform(1e6, 1e9, len(nowv[::3]))   # completion times that round
     now = torch.tensor(nowv, dtype=torch.float64, device="cuda")
     win = np.sort(rng.uniform(0, 400, 32))
-    need, agg = tb.need(g, u, now, torch.tensor(win, dtype=torch.float64, device="cuda"))
+    win[:8] = np.sort(np.concatenate([graphs["code-gen"].units[x].duration_dist.samples[:2]
+                                      for x in sorted(graphs["code-gen"].units)
+                                      if not graphs["code-gen"].units[x].is_llm] +
+                                     [np.array(win[:8])]))[:8]   # windows on sample values
+    win = np.sort(win)
+    wt = torch.tensor(win, dtype=torch.float64, device="cuda")
+    need, agg = tb.need(g, u, now, wt)                          # window-index path
+    need2, agg2 = tb.need(g, u, now, wt, window_index=False)    # per-app search path
+    np.testing.assert_array_equal(need.cpu().numpy(), need2.cpu().numpy())
     need = need.cpu().numpy()
     T = tb.n_types
     tot = np.zeros((T, 32))
