@@ -473,6 +473,7 @@ def run_ours(args):
     if world == 1 and not args.no_extra:
         line["k1c_policy"] = bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b)
         line["k6_dispatch"] = bench_dispatch(dev)
+        line["masks"] = bench_masks(dev)
         del eng, q, w
         torch.cuda.empty_cache()
         line["config4_stream"] = bench_stream(dev)
@@ -543,6 +544,39 @@ def bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b, rows=1_000_000, reps=20
                                    "apps": n, "note": "RemainingDemand.mean() in CPython "
                                    "sum() order (sequential, one lane per app)"}
     return out
+
+
+# ---------------------------------------------------------------------------
+# correlation masks (estimator.py:62-142)
+# ---------------------------------------------------------------------------
+
+def bench_masks(dev, copies=256, cpu_copies=2):
+    """build_masks over `copies` x the 8 reference archetype graphs of the
+    golden set (one pdg_pearson_flags launch incl. host gather), and the
+    oracle (the reference's own arithmetic) on a bounded sample."""
+    import copy
+    import gzip
+
+    from oracle import pdg_oracle as O
+    from paper_2506_14851_b200.graphs import build_masks, graph_from_kb
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "graphs.json.gz"), "rt") as fh:
+        docs = json.load(fh)
+    base = {k: docs[k] for k in STREAM_TEMPLATES}
+    graphs = {f"{k}#{i}": graph_from_kb(copy.deepcopy(v)) for i in range(copies)
+              for k, v in base.items()}
+    build_masks(graphs)
+    t0 = time.perf_counter()
+    res = build_masks(graphs)
+    gpu_ms = (time.perf_counter() - t0) * 1e3
+    n_jobs = sum(len(m) for g in res.values() for m in g.values())
+    t0 = time.perf_counter()
+    for _ in range(cpu_copies):
+        for v in base.values():
+            O.build_masks(O.graph_from_kb(v))
+    cpu_ms = (time.perf_counter() - t0) * 1e3 / cpu_copies * copies
+    return {"graphs": len(graphs), "pearson_jobs": n_jobs, "ms": gpu_ms,
+            "cpu_port_ms_extrapolated": cpu_ms,
+            "note": "wall clock incl. the host-side join of records (Python) and the copy back"}
 
 
 # ---------------------------------------------------------------------------

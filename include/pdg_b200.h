@@ -287,6 +287,18 @@ int pdg_prewarm_need(const pdg_prewarm_tables* tables, const int32_t* graph,
                      const double* windows, int32_t n_windows, int32_t n_types,
                      float* need, double* agg, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Correlation masks: estimator.pearson (estimator.py:
+ * 62-81) for a batch of (x, y) pairs laid out at x/y[off[j] .. off[j]+len[j]);
+ * rho[j] = NaN where the reference raises (fewer than 2 points, constant
+ * input), flag[j] = |rho| > threshold as _flag / build_masks set the mask
+ * (estimator.py:97-142).  Sums follow CPython sum(); squares are d*d (the
+ * reference's d**2 goes through libm pow, up to one ulp apart).
+ * ------------------------------------------------------------------------- */
+int pdg_pearson_flags(const double* x, const double* y, const int32_t* off, const int32_t* len,
+                      int64_t n_jobs, double threshold, double* rho, uint8_t* flag,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -266,6 +266,69 @@ def plan_dispatch(backend, active, key, app_rank, stage, request, slots, hystere
 
 
 # ---------------------------------------------------------------------------
+# correlation masks (estimator.py:62-142)
+# ---------------------------------------------------------------------------
+
+MASK_NAMES = ("input_upstream_input", "input_upstream_output", "output_upstream_output",
+              "output_own_input", "parallelism_upstream_parallelism")
+
+
+def pearson(x: Sequence[float], y: Sequence[float]) -> Optional[float]:
+    """estimator.pearson (62-81) in the reference's own float operations
+    (CPython sum(), ** 2, math.sqrt); None where it raises."""
+    if len(x) != len(y) or len(x) < 2:
+        return None
+    n = len(x)
+    mx = py_sum(x) / n
+    my = py_sum(y) / n
+    sxx = py_sum([(a - mx) ** 2 for a in x])
+    syy = py_sum([(b - my) ** 2 for b in y])
+    if sxx == 0 or syy == 0:
+        return None
+    sxy = py_sum([(a - mx) * (b - my) for a, b in zip(x, y)])
+    return max(-1.0, min(1.0, sxy / math.sqrt(sxx * syy)))
+
+
+def mask_jobs(g: "OGraph"):
+    """The (unit, mask, xs, ys) pairs build_masks correlates (estimator.py:
+    108-142): joined (upstream record, unit record) pairs on trial_id, in
+    upstream order (sorted ids) then record order (_joined_pairs, 84-95)."""
+    jobs = []
+    for uid in sorted(g.units):
+        u = g.units[uid]
+        ups = [v for v in sorted(g.units) if any(r.next_unit == uid for r in g.units[v].records)]
+        own = ([r.output_len for r in u.records], [r.input_len for r in u.records])
+        if not ups:
+            jobs.append((uid, "output_own_input") + own)
+            continue
+        by_trial = {r.trial_id: r for r in u.records}
+        pairs = [(ur, by_trial[ur.trial_id]) for v in ups for ur in g.units[v].records
+                 if ur.next_unit == uid and ur.trial_id in by_trial]
+        up_in = [p[0].input_len for p in pairs]
+        up_out = [p[0].output_len for p in pairs]
+        up_par = [float(p[0].parallelism) for p in pairs]
+        my_in = [p[1].input_len for p in pairs]
+        my_out = [p[1].output_len for p in pairs]
+        my_par = [float(p[1].parallelism) for p in pairs]
+        jobs += [(uid, "input_upstream_input", my_in, up_in),
+                 (uid, "input_upstream_output", my_in, up_out),
+                 (uid, "output_upstream_output", my_out, up_out),
+                 (uid, "output_own_input") + own,
+                 (uid, "parallelism_upstream_parallelism", my_par, up_par)]
+    return jobs
+
+
+def build_masks(g: "OGraph", threshold: float = 0.5) -> dict:
+    """uid -> {mask: bool} as estimator.build_masks sets them (_flag, 97-105:
+    fewer than 2 points or an undefined correlation -> False)."""
+    out = {uid: {k: False for k in MASK_NAMES} for uid in g.units}
+    for uid, name, xs, ys in mask_jobs(g):
+        r = pearson(xs, ys)
+        out[uid][name] = r is not None and abs(r) > threshold
+    return out
+
+
+# ---------------------------------------------------------------------------
 # a10: prewarm planner (prewarm.py:42-96)
 # ---------------------------------------------------------------------------
 

@@ -203,6 +203,83 @@ def record_trial(graph: KBGraph, trial: dict) -> KBGraph:
     return graph
 
 
+MASK_NAMES = ("input_upstream_input", "input_upstream_output", "output_upstream_output",
+              "output_own_input", "parallelism_upstream_parallelism")
+
+
+def _mask_jobs(graph):
+    """(unit, mask, xs, ys) correlated by build_masks (estimator.py:108-142):
+    a unit without upstreams only gets output_own_input; otherwise the
+    (upstream record, unit record) pairs joined on trial_id, upstreams in
+    sorted order (_joined_pairs, estimator.py:84-95)."""
+    jobs = []
+    for uid in sorted(graph.units):
+        u = graph.units[uid]
+        ups = [v for v in sorted(graph.units)
+               if any(r.next_unit == uid for r in graph.units[v].records)]
+        own = ([r.output_len for r in u.records], [r.input_len for r in u.records])
+        if not ups:
+            jobs.append((uid, "output_own_input") + own)
+            continue
+        by_trial = {r.trial_id: r for r in u.records}
+        pairs = [(ur, by_trial[ur.trial_id]) for v in ups for ur in graph.units[v].records
+                 if ur.next_unit == uid and ur.trial_id in by_trial]
+        up_in = [p[0].input_len for p in pairs]
+        up_out = [p[0].output_len for p in pairs]
+        my_in = [p[1].input_len for p in pairs]
+        my_out = [p[1].output_len for p in pairs]
+        jobs += [(uid, "input_upstream_input", my_in, up_in),
+                 (uid, "input_upstream_output", my_in, up_out),
+                 (uid, "output_upstream_output", my_out, up_out),
+                 (uid, "output_own_input") + own,
+                 (uid, "parallelism_upstream_parallelism",
+                  [float(p[1].parallelism) for p in pairs],
+                  [float(p[0].parallelism) for p in pairs])]
+    return jobs
+
+
+def build_masks(graphs, threshold: float = 0.5, device: str = "cuda"):
+    """estimator.build_masks (estimator.py:108-142) for a set of graphs in one
+    launch (pdg_pearson_flags): sets every unit's correlation masks in place
+    and returns {name: {unit: {mask: rho or None}}}."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    if not isinstance(graphs, dict):
+        graphs = {"g": graphs}
+    jobs, xs, ys, off, ln = [], [], [], [], []
+    for nm, g in graphs.items():
+        for uid, mask, x, y in _mask_jobs(g):
+            jobs.append((nm, uid, mask))
+            off.append(len(xs))
+            ln.append(len(x) if len(x) == len(y) else 0)
+            xs.extend(x)
+            ys.extend(y)
+    dev = torch.device(device)
+    t = lambda a, dt: torch.tensor(a if len(a) else [0], dtype=dt, device=dev)  # noqa: E731
+    X, Y, O, N = t(xs, torch.float64), t(ys, torch.float64), t(off, torch.int32), \
+        t(ln, torch.int32)
+    rho = torch.empty(max(len(jobs), 1), dtype=torch.float64, device=dev)
+    flag = torch.empty(max(len(jobs), 1), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib().pdg_pearson_flags(_lib.ptr(X), _lib.ptr(Y), _lib.ptr(O), _lib.ptr(N),
+                                            len(jobs), C.c_double(threshold), _lib.ptr(rho),
+                                            _lib.ptr(flag), _lib.stream_ptr()),
+               "pdg_pearson_flags")
+    rho_h, flag_h = rho.cpu().numpy(), flag.cpu().numpy()
+    out: dict = {}
+    for nm, g in graphs.items():
+        for uid, u in g.units.items():
+            for k in MASK_NAMES:
+                setattr(u.masks, k, False)
+    for i, (nm, uid, mask) in enumerate(jobs):
+        setattr(graphs[nm].units[uid].masks, mask, bool(flag_h[i]))
+        r = float(rho_h[i])
+        out.setdefault(nm, {}).setdefault(uid, {})[mask] = None if r != r else r
+    return out
+
+
 # ---------------------------------------------------------------------------
 # bucketing helpers (distributions.py:79-118), host side, exact float64
 # ---------------------------------------------------------------------------
