@@ -238,10 +238,11 @@ def _mask_jobs(graph):
     return jobs
 
 
-def build_masks(graphs, threshold: float = 0.5, device: str = "cuda"):
+def build_masks(graphs, threshold: float = 0.5, device: str = "cuda", timing=None):
     """estimator.build_masks (estimator.py:108-142) for a set of graphs in one
     launch (pdg_pearson_flags): sets every unit's correlation masks in place
-    and returns {name: {unit: {mask: rho or None}}}."""
+    and returns {name: {unit: {mask: rho or None}}}.  timing (dict, optional)
+    receives the kernel time in ms (CUDA events)."""
     import ctypes as C
 
     import torch
@@ -263,10 +264,17 @@ def build_masks(graphs, threshold: float = 0.5, device: str = "cuda"):
         t(ln, torch.int32)
     rho = torch.empty(max(len(jobs), 1), dtype=torch.float64, device=dev)
     flag = torch.empty(max(len(jobs), 1), dtype=torch.uint8, device=dev)
+    if timing is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     _lib.check(_lib.lib().pdg_pearson_flags(_lib.ptr(X), _lib.ptr(Y), _lib.ptr(O), _lib.ptr(N),
                                             len(jobs), C.c_double(threshold), _lib.ptr(rho),
                                             _lib.ptr(flag), _lib.stream_ptr()),
                "pdg_pearson_flags")
+    if timing is not None:
+        e1.record()
+        e1.synchronize()
+        timing["kernel_ms"] = e0.elapsed_time(e1)
     rho_h, flag_h = rho.cpu().numpy(), flag.cpu().numpy()
     out: dict = {}
     for nm, g in graphs.items():
