@@ -5,22 +5,22 @@
 // ApplicationInstance.set_remaining's bucketing (sched.py:170-181,
 // distributions.py:79-105).  Output samples are bit-identical to the
 // reference for the same (graph, current unit, observations, n, seed): the
-// kernel evaluates the reference's numpy PCG64 stream *by position*.
+// kernels evaluate the reference's numpy PCG64 stream *by position*.
 //
-// Mapping: one warp per application.  The reference walk is vectorised per
-// (step, unit): at each outer step the occupied-unit set is frozen, units are
-// visited in ascending index order, and every walk sitting on the unit *at
-// that moment* draws
+// The reference walk is vectorised per (step, unit): at each outer step the
+// occupied-unit set is frozen, units are visited in ascending index order,
+// and every walk sitting on the unit *at that moment* draws
 //   choice(A, m) [, choice(B, m) | per-input-bucket choice(pool_b, m_b)],
 //   then random(m)                                 (estimator.py:343-353)
-// so each draw's position in the stream is (group base) + (rank of the walk
-// among the unit's members).  Per step the warp compacts the still-active
-// walks (index order kept); per unit visit it compacts that unit's members
-// into a list whose position IS the rank, and lane l takes a contiguous block
-// of ranks.  Its stream positions are then consecutive inside each draw
-// group: one PCG64 jump per group to the block start (pcg64.cuh), then single
-// LCG steps (a 64-bit word serves two 32-bit bounded draws).  A member's
-// bounded draws, its uniform and its commit happen in one loop iteration.
+// so each draw's position in the stream is (visit base) + (rank of the walk
+// among the unit's members).  One warp per application in both kernels:
+//
+//   mc_walk_kernel (n <= 512, the production path; design at its definition
+//     below): walk membership as per-unit bitsets in shared memory, the
+//     visit's stream segment decoded lane-strided (lane l reads words l,
+//     l+32, ..., one multiply-add per 32-word stride).
+//   mc_engine_kernel (512 < n): active-walk and member compaction per visit,
+//     lane-contiguous rank blocks, one PCG64 jump per lane and draw group.
 //
 // numpy's Lemire rejection (probability < P/2^32 per draw) shifts every later
 // position.  A warp vote detects it; the application is then abandoned by the
