@@ -273,6 +273,9 @@ typedef struct {
   const int32_t* unit_type;   /* [U] warm-content backend type, -1 = none      */
   const int32_t* win_idx;     /* optional [U, n_windows]: pdg_prewarm_window_index */
                               /* of the windows passed to pdg_prewarm_need       */
+  const int32_t* unit_rec;    /* optional [U, 12], 16-B aligned: svc_off, svc_len, */
+                              /* backend type of successors 0..3 (-1 = none),     */
+                              /* float bits of (float)p_s of successors 0..3, 0, 0 */
 } pdg_prewarm_tables;
 
 /* lower_bound(svc_sorted[u], windows[k]) for every unit and window: lets

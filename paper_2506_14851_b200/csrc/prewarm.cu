@@ -143,6 +143,7 @@ struct NeedArgs {
   double* agg;                  // [T, K] optional, sum over applications
   const int32_t* win_idx;       // [U, K] optional: lower_bound(svc[u], W_k)
   int stage_n;                  // service samples staged per warp (0 with win_idx)
+  const int4* unit_rec;         // [U, 3] optional packed unit record (see header)
 };
 
 // first index i in the ascending array with now + s[i] >= x  (exact f64)
@@ -178,8 +179,15 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
     const int gbase = a.graph_base[a.graph[app]];
     const int u = gbase + a.unit[app];
     const double now = a.now[app];
-    const int n = a.svc_len[u];
-    const double* gsrc = a.svc_sorted + a.svc_off[u];
+    // one 48-byte record per unit when available (fewer dependent loads)
+    int4 r0 = make_int4(0, 0, 0, 0), r1 = r0, r2 = r0;
+    if (a.unit_rec) {
+      r0 = a.unit_rec[3 * int64_t(u)];
+      r1 = a.unit_rec[3 * int64_t(u) + 1];
+      r2 = a.unit_rec[3 * int64_t(u) + 2];
+    }
+    const int n = a.unit_rec ? r0.y : a.svc_len[u];
+    const double* gsrc = a.svc_sorted + (a.unit_rec ? r0.x : a.svc_off[u]);
     const double* s = gsrc;
     if (n <= a.stage_n) {                            // coalesced stage, then LDS searches
       for (int i = lane; i < n; i += 32) stage[i] = gsrc[i];
@@ -211,22 +219,41 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
       pneed = 1.f - __fdiv_rn(float(n - j), float(m));
     }
     // up to 4 successors; successors of equal type are merged first
-    const int so = a.succ_off[u];
-    const int ns = a.succ_len[u] < 4 ? a.succ_len[u] : 4;
     int t0 = -1, t1 = -1, t2 = -1, t3 = -1;
     float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
-    if (ns > 0) { t0 = a.unit_type[gbase + a.succ_nxt[so]];     f0 = float(a.succ_p[so]) * pneed; }
-    if (ns > 1) { t1 = a.unit_type[gbase + a.succ_nxt[so + 1]]; f1 = float(a.succ_p[so + 1]) * pneed; }
-    if (ns > 2) { t2 = a.unit_type[gbase + a.succ_nxt[so + 2]]; f2 = float(a.succ_p[so + 2]) * pneed; }
-    if (ns > 3) { t3 = a.unit_type[gbase + a.succ_nxt[so + 3]]; f3 = float(a.succ_p[so + 3]) * pneed; }
+    if (a.unit_rec) {                                // types -1 beyond the successors
+      t0 = r0.z; t1 = r0.w; t2 = r1.x; t3 = r1.y;
+      f0 = __int_as_float(r1.z) * pneed;
+      f1 = __int_as_float(r1.w) * pneed;
+      f2 = __int_as_float(r2.x) * pneed;
+      f3 = __int_as_float(r2.y) * pneed;
+    } else {
+      const int so = a.succ_off[u];
+      const int ns = a.succ_len[u] < 4 ? a.succ_len[u] : 4;
+      if (ns > 0) { t0 = a.unit_type[gbase + a.succ_nxt[so]];     f0 = float(a.succ_p[so]) * pneed; }
+      if (ns > 1) { t1 = a.unit_type[gbase + a.succ_nxt[so + 1]]; f1 = float(a.succ_p[so + 1]) * pneed; }
+      if (ns > 2) { t2 = a.unit_type[gbase + a.succ_nxt[so + 2]]; f2 = float(a.succ_p[so + 2]) * pneed; }
+      if (ns > 3) { t3 = a.unit_type[gbase + a.succ_nxt[so + 3]]; f3 = float(a.succ_p[so + 3]) * pneed; }
+    }
     if (t1 >= 0 && t1 == t0) { f0 += f1; t1 = -1; }
     if (t2 >= 0 && t2 == t0) { f0 += f2; t2 = -1; }
     if (t2 >= 0 && t2 == t1) { f1 += f2; t2 = -1; }
     if (t3 >= 0 && t3 == t0) { f0 += f3; t3 = -1; }
     if (t3 >= 0 && t3 == t1) { f1 += f3; t3 = -1; }
     if (t3 >= 0 && t3 == t2) { f2 += f3; t3 = -1; }
+    if (a.need && (TK & 3) == 0) {                   // dense row: 16-B zero stores ...
+      float4* row4 = reinterpret_cast<float4*>(a.need + app * int64_t(TK));
+      for (int i = lane; i < (TK >> 2); i += 32) __stcs(row4 + i, make_float4(0.f, 0.f, 0.f, 0.f));
+      __syncwarp();                                  // ... ordered before the values
+    }
     if (kwin >= 0) {
-      if (a.need) {                                  // dense row, each element once
+      if (a.need && (TK & 3) == 0) {                 // the <= 4 non-zero types
+        float* row = a.need + app * int64_t(TK) + kwin;
+        if (t0 >= 0) __stcs(row + t0 * a.n_windows, f0);
+        if (t1 >= 0) __stcs(row + t1 * a.n_windows, f1);
+        if (t2 >= 0) __stcs(row + t2 * a.n_windows, f2);
+        if (t3 >= 0) __stcs(row + t3 * a.n_windows, f3);
+      } else if (a.need) {                           // dense row, each element once
         float* row = a.need + app * int64_t(TK) + kwin;
         for (int t = 0; t < a.n_types; ++t) {
           const float v = t == t0 ? f0 : t == t1 ? f1 : t == t2 ? f2 : t == t3 ? f3 : 0.f;
@@ -320,7 +347,8 @@ extern "C" int pdg_prewarm_need(const pdg_prewarm_tables* t, const int32_t* grap
   if (n == 0) return PDG_OK;
   NeedArgs a{t->svc_sorted, t->svc_off, t->svc_len, t->graph_base, t->succ_off, t->succ_len,
              t->succ_nxt, t->succ_p, t->unit_type, graph, unit, now, windows, n_types,
-             n_windows, n, need, agg, t->win_idx, t->win_idx ? 0 : kNeedStage};
+             n_windows, n, need, agg, t->win_idx, t->win_idx ? 0 : kNeedStage,
+             reinterpret_cast<const int4*>(t->unit_rec)};
   const size_t smem = sizeof(double) * (size_t(kNeedWarps) * a.stage_n +
                                         (agg ? size_t(n_types) * n_windows : 0));
   cudaError_t e = cudaFuncSetAttribute(prewarm_need_kernel,

@@ -101,7 +101,7 @@ def plan_prewarm(completion_dist, p_s: float, t_p: float, knob: float, now: floa
 class PrewarmTablesC(C.Structure):
     _fields_ = [(nm, C.c_void_p) for nm in ("svc_sorted", "svc_off", "svc_len", "graph_base",
                                             "succ_off", "succ_len", "succ_nxt", "succ_p",
-                                            "unit_type", "win_idx")]
+                                            "unit_type", "win_idx", "unit_rec")]
 
 
 class PrewarmTables:
@@ -124,6 +124,26 @@ class PrewarmTables:
                       succ_off=t(succ_off, np.int32), succ_len=t(succ_len, np.int32),
                       succ_nxt=t(succ_nxt, np.int32), succ_p=t(succ_p, np.float64),
                       unit_type=t(unit_type, np.int32))
+        # one 48-byte record per unit for the need kernel: (svc_off, svc_len,
+        # successor backend types x4, float(p_s) bits x4, 0, 0)
+        soff_a, slen_a = np.asarray(svc_off, np.int64), np.asarray(svc_len, np.int64)
+        so_a, sl_a = np.asarray(succ_off, np.int64), np.asarray(succ_len, np.int64)
+        nx_a, p_a = np.asarray(succ_nxt, np.int64), np.asarray(succ_p, np.float64)
+        ut_a, gb_a = np.asarray(unit_type, np.int64), np.asarray(graph_base, np.int64)
+        U = soff_a.size
+        rec = np.zeros((max(U, 1), 12), dtype=np.int32)
+        gof = np.zeros(U, dtype=np.int64)                  # graph base of each unit
+        for g in range(gb_a.size):
+            gof[gb_a[g]:(gb_a[g + 1] if g + 1 < gb_a.size else U)] = gb_a[g]
+        rec[:U, 0], rec[:U, 1] = soff_a, slen_a
+        rec[:U, 2:6] = -1
+        for i in range(4):
+            has = sl_a > i
+            idx = np.where(has, so_a + i, 0)
+            rec[:U, 2 + i] = np.where(has, ut_a[gof + nx_a[idx]] if nx_a.size else -1, -1)
+            pf = np.where(has, p_a[idx] if p_a.size else 0.0, 0.0).astype(np.float32)
+            rec[:U, 6 + i] = pf.view(np.int32)
+        self.t["unit_rec"] = t(rec.reshape(-1), np.int32)
         self.c = PrewarmTablesC(*[_lib.ptr(self.t[nm]) if nm in self.t else None
                                   for nm, _ in PrewarmTablesC._fields_])
         self.n_units = int(np.asarray(svc_len).size)
@@ -177,7 +197,7 @@ class PrewarmTables:
         return self._win[1]
 
     def need(self, graph_idx, unit_idx, now, windows, *, dense=True, aggregate=True,
-             out=None, window_index=True, stream=None):
+             out=None, window_index=True, unit_records=True, stream=None):
         """need[N, T, K] float32 (dense) and/or agg[T, K] float64 over the queue.
         window_index: per-(unit, window) lower bounds computed once per window
         grid instead of a binary search per application."""
@@ -185,6 +205,7 @@ class PrewarmTables:
         K = int(windows.numel())
         dev = self.device
         self.c.win_idx = _lib.ptr(self._window_index(windows, stream)) if window_index else None
+        self.c.unit_rec = _lib.ptr(self.t["unit_rec"]) if unit_records else None
         need = out if out is not None else (
             torch.empty((n, self.n_types, K), dtype=torch.float32, device=dev) if dense else None)
         agg = torch.zeros((self.n_types, K), dtype=torch.float64, device=dev) if aggregate else None

@@ -89,7 +89,8 @@ def test_need_grid_vs_oracle(kb_graphs):
     win = np.sort(win)
     wt = torch.tensor(win, dtype=torch.float64, device="cuda")
     need, agg = tb.need(g, u, now, wt)                          # window-index path
-    need2, agg2 = tb.need(g, u, now, wt, window_index=False)    # per-app search path
+    need2, agg2 = tb.need(g, u, now, wt, window_index=False,    # per-app search path
+                          unit_records=False)
     np.testing.assert_array_equal(need.cpu().numpy(), need2.cpu().numpy())
     need = need.cpu().numpy()
     T = tb.n_types
