@@ -749,7 +749,6 @@ struct WalkState {
   double* kout;
   double* kin_d;     // [max_pairs] the same divided by prefill / decode rate
   double* kout_d;
-  U128* cl;          // [32] per-lane stride constant K_l * inc (shared memory)
 };
 
 // pool values as the stage time uses them: LLM inputs / prefill_rate, LLM
@@ -777,7 +776,7 @@ __host__ __device__ inline size_t walk_union_bytes(int counters) {
 }
 __host__ __device__ inline size_t walk_smem_bytes(int counters, int units) {
   return walk_union_bytes(counters) + size_t(kSmemWalks) * 10 + size_t(units) * kWalkWords * 4 +
-         size_t(units) * 112 + 32 * sizeof(U128);
+         size_t(units) * 112;
 }
 // global scratch per warp: [own-input arrays] [K3 pairs]
 __host__ __device__ inline size_t walk_gmem_bytes() {
@@ -871,6 +870,15 @@ struct LaneConst {
   U128 c32;    // G_32 * inc
 };
 
+// Lane l decodes the words of the application's stream whose absolute
+// position is l mod 32, whatever visit they belong to: its chain state `st`
+// is the state of the last such word it decoded, so every visit simply
+// continues the chain one 32-word stride at a time.  P = words consumed.
+struct LaneStream {
+  U128 st;
+  uint32_t P;
+};
+
 __device__ __forceinline__ LaneConst lane_const(const uint64_t* jt, const U128& inc, int lane) {
   const ulonglong2* l2 = reinterpret_cast<const ulonglong2*>(jt) + 2 * 2048;
   const ulonglong2 k = __ldg(l2 + 2 * lane + 1), g32 = __ldg(l2 + 2 * 32 + 1);
@@ -887,19 +895,18 @@ __device__ __forceinline__ LaneConst lane_const(const uint64_t* jt, const U128& 
 template <bool LLM>
 __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const SuccTab& sc,
                               const Pools& pl, const WalkState& ws, uint32_t m, Stream& g,
-                              const LaneConst& lc, unsigned& targets, int lane) {
+                              LaneStream& ls, const LaneConst& lc, unsigned& targets,
+                              int lane) {
   constexpr bool llm = LLM;
   const uint32_t mA = pl.pa > 1 ? m : 0u;
   const uint32_t C = mA + ((llm && pl.pb > 1) ? m : 0u);
   const uint32_t pin = g.pend ? 1u : 0u;
   const uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
   const uint32_t W = wb + m;
-  const ulonglong2 ap =
-      __ldg(reinterpret_cast<const ulonglong2*>(a.b.jump) + 2 * (2048 + lane));
-  U128 st = add128(mul128(g.s, U128{ap.x, ap.y}), ws.cl[lane]);   // one stride before word lane
+  U128 st = ls.st;                                // one stride before word q
   bool rej = false;
   uint32_t pend_hi = 0;
-  uint32_t q = lane;
+  uint32_t q = (uint32_t(lane) - ls.P) & 31u;
   for (; q < wb; q += 32) {                       // bounded halves -> draw indices
     st = pcg_stride32(st, lc.c32);
     const uint64_t wd = pcg_out(st);
@@ -950,10 +957,9 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
   if (sc.ns <= 3) uniforms(std::true_type{});
   else uniforms(std::false_type{});
   if (__any_sync(kFull, rej)) return false;
-  const unsigned last = (W - 1) & 31u;            // it decoded word W - 1
-  g.s.lo = __shfl_sync(kFull, st.lo, last);
-  g.s.hi = __shfl_sync(kFull, st.hi, last);
-  const uint32_t pv = __shfl_sync(kFull, pend_hi, (wb - 1) & 31u);
+  ls.st = st;
+  const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
+  ls.P += W;
   if (C) {
     g.pend = ((pin + C) & 1u) != 0;
     if (g.pend) g.pv = pv;
@@ -971,7 +977,8 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
 // word and the first B draw, and numpy's buffered half, are placed by lane 0.
 __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab& sc,
                           const Pools& pl, const Pools& pd, const WalkState& ws, uint32_t m,
-                          Stream& g, const LaneConst& lc, unsigned& targets, int lane) {
+                          Stream& g, LaneStream& ls, const LaneConst& lc, unsigned& targets,
+                          int lane) {
   const unsigned lt = lanemask_lt();
   const int K = d.ib_k;
   uint32_t* cnt = ws.cnt;
@@ -1000,11 +1007,9 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
   };
   for (int b = lane; b < K; b += 32) cnt[b] = 0;
   __syncwarp();
-  const ulonglong2 ap =
-      __ldg(reinterpret_cast<const ulonglong2*>(a.b.jump) + 2 * (2048 + lane));
-  U128 st = add128(mul128(g.s, U128{ap.x, ap.y}), ws.cl[lane]);   // one stride before word lane
+  U128 st = ls.st;                                // one stride before word q
   uint32_t pend_hi = 0;
-  uint32_t q = lane;
+  uint32_t q = (uint32_t(lane) - ls.P) & 31u;
   for (; q < wA; q += 32) {                       // phase A: input draws
     st = pcg_stride32(st, lc.c32);
     const uint64_t wd = pcg_out(st);
@@ -1086,7 +1091,7 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
     const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
     ws.tmp[k] = dadd(ws.tmp[k], pool[lemire(h, P, rej)]);   // + o / decode_rate
   };
-  const uint32_t sh = __shfl_sync(kFull, pend_hi, (wA - 1) & 31u);
+  const uint32_t sh = __shfl_sync(kFull, pend_hi, (ls.P + wA - 1) & 31u);
   for (; q < wb; q += 32) {                       // phase B: output draws
     st = pcg_stride32(st, lc.c32);
     const uint64_t wd = pcg_out(st);
@@ -1113,10 +1118,9 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
     ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
     arrive(ws, w, v, targets);
   }
-  const unsigned last = (W - 1) & 31u;
-  g.s.lo = __shfl_sync(kFull, st.lo, last);
-  g.s.hi = __shfl_sync(kFull, st.hi, last);
-  const uint32_t pv = __shfl_sync(kFull, pend_hi, (wb - 1) & 31u);
+  ls.st = st;
+  const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
+  ls.P += W;
   if (C) {
     g.pend = ((pin + C) & 1u) != 0;
     if (g.pend) g.pv = pv;
@@ -1149,7 +1153,6 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
   ws.mem = reinterpret_cast<uint16_t*>(ws.tot + kSmemWalks);
   ws.bits = reinterpret_cast<uint32_t*>(ws.mem + kSmemWalks);
   ws.uc = reinterpret_cast<UnitCache*>(ws.bits + a.b.max_units * kWalkWords);
-  ws.cl = reinterpret_cast<U128*>(ws.uc + a.b.max_units);
   ws.tmp = reinterpret_cast<double*>(gs);
   ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + kSmemWalks);
   ws.osrt = ws.bkt + kSmemWalks;
@@ -1194,7 +1197,13 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
       __syncwarp();
     }
     const LaneConst lc = lane_const(a.b.jump, g.inc, lane);
-    ws.cl[lane] = lc.cl;                         // reloaded once per visit
+    LaneStream ls;                               // lane l: words l, l+32, ... of the stream
+    {
+      const ulonglong2 ap =
+          __ldg(reinterpret_cast<const ulonglong2*>(a.b.jump) + 2 * (2048 + lane));
+      ls.st = add128(mul128(g.s, U128{ap.x, ap.y}), lc.cl);   // one stride before word lane
+      ls.P = 0;
+    }
     if (lane < gn) {                             // stage the unit descriptors
       UnitCache c;
       c.d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + lane];
@@ -1230,12 +1239,14 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
         const Pools pd = pools_div(a, d, ov, ovd);
         unsigned targets = 0;
         if (!(d.flags & F_LLM))
-          ok = visit_strided<false>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, lc, targets, lane);
+          ok = visit_strided<false>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, ls, lc, targets,
+                                    lane);
         else if ((d.flags & F_OWN) && !ov)
-          ok = visit_own(a, d, succ_of(ws.uc[u]), pools_for(a, d, ov, ovp), pd, ws, m, g, lc,
-                         targets, lane);
+          ok = visit_own(a, d, succ_of(ws.uc[u]), pools_for(a, d, ov, ovp), pd, ws, m, g, ls,
+                         lc, targets, lane);
         else
-          ok = visit_strided<true>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, lc, targets, lane);
+          ok = visit_strided<true>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, ls, lc, targets,
+                                   lane);
         pending |= __reduce_or_sync(kFull, targets);
       }
     }
