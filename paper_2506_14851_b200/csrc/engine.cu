@@ -31,8 +31,17 @@
 #include "common.cuh"
 #include "pcg64.cuh"
 
+#ifndef PDG_UNROLL_B
+#define PDG_UNROLL_B 1       // unroll of the bounded-word decode loop
+#endif
+#ifndef PDG_UNROLL_U
+#define PDG_UNROLL_U 2       // unroll of the uniform-word loop
+#endif
+
 namespace pdg {
 
+constexpr int kUnrollB = PDG_UNROLL_B;
+constexpr int kUnrollU = PDG_UNROLL_U;
 constexpr int kWarps = 4;            // apps per CTA
 constexpr int kSmemWalks = 512;      // walks kept in shared memory per warp
 
@@ -907,6 +916,7 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
   bool rej = false;
   uint32_t pend_hi = 0;
   uint32_t q = (uint32_t(lane) - ls.P) & 31u;
+#pragma unroll kUnrollB
   for (; q < wb; q += 32) {                       // bounded halves -> draw indices
     st = pcg_stride32(st, lc.c32);
     const uint64_t wd = pcg_out(st);
@@ -940,6 +950,7 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
   double xa = pl.A[min(uint32_t(ws.ia[k]), la)], xb = 0.0;
   if (LLM) xb = pl.B[min(uint32_t(ws.ib[k]), lb)];
   auto uniforms = [&](auto few_succ) {
+#pragma unroll kUnrollU
     for (; q < W; q += 32) {
       const double ca = xa, cb = xb;
       xa = pl.A[min(uint32_t(ws.ia[k + 32]), la)];
