@@ -474,6 +474,7 @@ def run_ours(args):
         line["k1c_policy"] = bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b)
         line["k6_dispatch"] = bench_dispatch(dev)
         line["masks"] = bench_masks(dev)
+        line["config1_refresh_latency"] = bench_refresh_latency()
         del eng, q, w
         torch.cuda.empty_cache()
         line["config4_stream"] = bench_stream(dev)
@@ -543,6 +544,33 @@ def bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b, rows=1_000_000, reps=20
     out["engine_mean_epilogue"] = {"engine_ms": base_ms, "engine_with_mean_ms": mean_ms,
                                    "apps": n, "note": "RemainingDemand.mean() in CPython "
                                    "sum() order (sequential, one lane per app)"}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# config 1: the paper's "policy runtime" (refresh_priorities elapsed_ns,
+# sched.py:269-310) at scheduler-sized batches, drop-in vs the reference
+# ---------------------------------------------------------------------------
+
+def bench_refresh_latency():
+    try:
+        from tools.refresh_latency import apps
+        from tests.dispatch_hook import import_pdgsim
+        pdgsim = import_pdgsim()
+        from pdgsim import sched as ref
+    except ImportError as e:
+        return {"unavailable": f"reference pdgsim not importable: {e}"}
+    from paper_2506_14851_b200 import sched as ours
+    rng = np.random.default_rng(0)
+    out = {"note": "median RefreshResult.elapsed_ns over 300 forced refreshes; the reference "
+                   "timed on this host's CPU, ours through the drop-in (host arrays in/out)"}
+    for m, b in ((47, 64), (1000, 10)):
+        live = apps(pdgsim, m, b, rng)
+        for name, fn in (("ours", ours.refresh_priorities), ("reference", ref.refresh_priorities)):
+            for _ in range(30):
+                fn(live, 0.0, 1.0, force=True)
+            ts = [fn(live, 0.0, 1.0, force=True).elapsed_ns for _ in range(300)]
+            out[f"{name}_apps{m}_bins{b}_p50_us"] = float(np.median(ts)) / 1e3
     return out
 
 

@@ -43,6 +43,7 @@ _SIG = {
     "pdg_abi_version": (C.c_int, []),
     "pdg_device_info": (C.c_int, [_P, _P, _P]),
     "pdg_gittins_rank_f64": (C.c_int, [_P, _P, _P, _I64, _I32, _P, _P]),
+    "pdg_gittins_rank_f64_host": (C.c_int, [_P, _P, _P, _I64, _I32, _P, _P]),
     "pdg_gittins_score_hist": (C.c_int, [C.POINTER(HistRows), _P, _I64, _D, _P, _P, _P, _P, _P,
                                                   _P]),
     "pdg_bucketize": (C.c_int, [_P, _I64, _I32, _I32, _P, _P, _P, _P, _I64, _P]),

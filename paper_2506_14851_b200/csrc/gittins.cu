@@ -17,6 +17,7 @@
 //        in float64 at the alive boundary, scans in int32 (S, T exact) and
 //        float32 (P); HBM-bound, 128-bit loads of 8 counts per lane.
 #include <cub/cub.cuh>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -420,6 +421,63 @@ extern "C" int pdg_gittins_rank_f64(const double* values, const double* probs,
   gittins_f64_kernel<<<unsigned(blocks), threads, 0, (cudaStream_t)stream>>>(
       values, probs, ages, n_rows, n_bins, out_rank);
   return launch_status("gittins_f64_kernel");
+}
+
+// Host-buffer form for scheduler-sized batches (the drop-in refresh): one
+// packed upload into a pinned staging area, the kernel, one download, all on
+// the caller's stream inside the library -- no per-call allocation.
+namespace {
+struct HostStage {
+  double* h = nullptr;     // pinned host
+  double* d = nullptr;     // device
+  size_t cap = 0;          // doubles
+};
+thread_local HostStage g_stage;
+}  // namespace
+
+extern "C" int pdg_gittins_rank_f64_host(const double* values, const double* probs,
+                                         const double* ages, int64_t n_rows, int32_t n_bins,
+                                         double* out_rank, void* stream) {
+  using namespace pdg;
+  if (n_rows < 0 || n_bins <= 0 || (n_rows > 0 && (!values || !probs || !ages || !out_rank))) {
+    set_error("pdg_gittins_rank_f64_host: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (n_rows == 0) return PDG_OK;
+  const size_t nb = size_t(n_rows) * size_t(n_bins);
+  const size_t need = 2 * nb + 2 * size_t(n_rows);
+  HostStage& st = g_stage;
+  if (need > st.cap) {
+    size_t cap = 4096;
+    while (cap < need) cap <<= 1;
+    if (st.h) cudaFreeHost(st.h);
+    if (st.d) cudaFree(st.d);
+    st.h = nullptr;
+    st.d = nullptr;
+    st.cap = 0;
+    cudaError_t e = cudaMallocHost(&st.h, cap * sizeof(double));
+    if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_f64_host cudaMallocHost");
+    e = cudaMalloc(&st.d, cap * sizeof(double));
+    if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_f64_host cudaMalloc");
+    st.cap = cap;
+  }
+  std::memcpy(st.h, values, nb * sizeof(double));
+  std::memcpy(st.h + nb, probs, nb * sizeof(double));
+  std::memcpy(st.h + 2 * nb, ages, size_t(n_rows) * sizeof(double));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t in = 2 * nb + size_t(n_rows);
+  cudaError_t e = cudaMemcpyAsync(st.d, st.h, in * sizeof(double), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_f64_host upload");
+  int rc = pdg_gittins_rank_f64(st.d, st.d + nb, st.d + 2 * nb, n_rows, n_bins, st.d + in,
+                                stream);
+  if (rc != PDG_OK) return rc;
+  e = cudaMemcpyAsync(st.h + in, st.d + in, size_t(n_rows) * sizeof(double),
+                      cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_f64_host download");
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_f64_host sync");
+  std::memcpy(out_rank, st.h + in, size_t(n_rows) * sizeof(double));
+  return PDG_OK;
 }
 
 extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* age,

@@ -72,10 +72,12 @@ class RefreshResult:
 # ---------------------------------------------------------------------------
 
 def gittins_rank_batch(values, probs, ages) -> np.ndarray:
-    """Gittins ranks of N aligned support rows; NaN marks exhausted rows."""
-    v = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
-    p = np.ascontiguousarray(np.asarray(probs, dtype=np.float64))
-    a = np.ascontiguousarray(np.asarray(ages, dtype=np.float64))
+    """Gittins ranks of N aligned support rows; NaN marks exhausted rows.
+    Host arrays go straight to the C ABI (pdg_gittins_rank_f64_host: one
+    staged upload, the K1a kernel, one download)."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    p = np.ascontiguousarray(probs, dtype=np.float64)
+    a = np.ascontiguousarray(ages, dtype=np.float64)
     if v.ndim != 2 or p.shape != v.shape or a.shape != (v.shape[0],):
         raise ValueError(f"shape mismatch: values {v.shape}, probs {p.shape}, ages {a.shape}")
     n, b = v.shape
@@ -83,16 +85,11 @@ def gittins_rank_batch(values, probs, ages) -> np.ndarray:
         return np.empty(0)
     if b == 0:       # no support at all: every row is exhausted
         return np.full(n, np.nan)
-    L = _lib.lib()
-    dev = torch.device("cuda")
-    tv = torch.from_numpy(v).to(dev, non_blocking=True)
-    tp = torch.from_numpy(p).to(dev, non_blocking=True)
-    ta = torch.from_numpy(a).to(dev, non_blocking=True)
-    out = torch.empty(n, dtype=torch.float64, device=dev)
-    _lib.check(L.pdg_gittins_rank_f64(_lib.ptr(tv), _lib.ptr(tp), _lib.ptr(ta), n, b,
-                                      _lib.ptr(out), _lib.stream_ptr()),
-               "pdg_gittins_rank_f64")
-    return out.cpu().numpy()
+    out = np.empty(n)
+    _lib.check(_lib.lib().pdg_gittins_rank_f64_host(
+        v.ctypes.data, p.ctypes.data, a.ctypes.data, n, b, out.ctypes.data, None),
+        "pdg_gittins_rank_f64_host")
+    return out
 
 
 def gittins_rank_points(values: Sequence[float], probs: Sequence[float],
@@ -238,15 +235,20 @@ def refresh_priorities(live: Iterable, now: float, bucket_period: float,
         rest = [a for a in due if a.remaining is None]
         if gapps:
             m = len(gapps)
-            width = max(a.bucket_width for a in gapps)
-            vals = np.zeros((m, width))
-            prbs = np.zeros((m, width))
-            for i, a in enumerate(gapps):     # ragged rows: pad with last value, 0 mass
-                k = a.bucket_width
-                vals[i, :k] = a.shifted_values
-                prbs[i, :k] = a.bucket_probs
-                if k < width:
-                    vals[i, k:] = vals[i, k - 1]
+            width0 = gapps[0].bucket_width
+            if all(a.bucket_width == width0 for a in gapps):   # sched.py:276-281
+                vals = np.concatenate([a.shifted_values for a in gapps]).reshape(m, width0)
+                prbs = np.concatenate([a.bucket_probs for a in gapps]).reshape(m, width0)
+            else:
+                width = max(a.bucket_width for a in gapps)
+                vals = np.zeros((m, width))
+                prbs = np.zeros((m, width))
+                for i, a in enumerate(gapps):     # ragged rows: pad with last value, 0 mass
+                    k = a.bucket_width
+                    vals[i, :k] = a.shifted_values
+                    prbs[i, :k] = a.bucket_probs
+                    if k < width:
+                        vals[i, k:] = vals[i, k - 1]
             ages = np.fromiter((a.attained_service for a in gapps), float, m)
             ranks = gittins_rank_batch(vals, prbs, ages)
             nan = np.isnan(ranks)
