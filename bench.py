@@ -475,6 +475,7 @@ def run_ours(args):
         line["k6_dispatch"] = bench_dispatch(dev)
         line["masks"] = bench_masks(dev)
         line["config1_refresh_latency"] = bench_refresh_latency()
+        line["k1_refresh_1m"] = bench_k1_large(dev)
         del eng, q, w
         torch.cuda.empty_cache()
         line["config4_stream"] = bench_stream(dev)
@@ -545,6 +546,45 @@ def bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b, rows=1_000_000, reps=20
                                    "apps": n, "note": "RemainingDemand.mean() in CPython "
                                    "sum() order (sequential, one lane per app)"}
     return out
+
+
+# ---------------------------------------------------------------------------
+# K1b periodic refresh of a 1M-row resident queue (no re-estimation)
+# ---------------------------------------------------------------------------
+
+def bench_k1_large(dev, n=1_000_000, reps=20):
+    import torch
+    from paper_2506_14851_b200.queue import HistQueue
+    q = HistQueue(n, N_BINS)
+    g = torch.Generator(device=dev).manual_seed(1)
+    q.counts.copy_((torch.rand((n, N_BINS), device=dev, generator=g) * 5).to(torch.uint16))
+    q.nsamp.fill_(N_SAMP)
+    q.nbins.fill_(N_BINS)
+    q.lo.uniform_(0, 100, generator=g)
+    q.width.uniform_(0.1, 2, generator=g)
+    q.est_age.uniform_(0, 10, generator=g)
+    q.age.copy_(q.est_age + torch.rand(n, device=dev, dtype=torch.float64, generator=g) * 200)
+    q.n = n
+    for _ in range(3):
+        q.score(PENALTY)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        q.score(PENALTY)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    nbytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
+    ach = nbytes * n / (ms / 1e3) / 1e9
+    peak = measured_peaks()[0]
+    return {"kernel": "gittins_rows_kernel", "rows": n, "ms_per_launch": ms,
+            "apps_per_s": n / (ms / 1e3),
+            "roofline": {"bound": "hbm", "bytes_per_app": nbytes, "achieved": ach,
+                         "peak": peak, "unit": "GB/s", "frac": ach / peak}}
 
 
 # ---------------------------------------------------------------------------
