@@ -40,3 +40,34 @@ def test_no_cpu_fallback():
     from paper_2506_14851_b200._lib import PdgDeviceError
     with pytest.raises(PdgDeviceError):
         sched.gittins_rank_batch(np.ones((1, 2)), np.full((1, 2), 0.5), np.zeros(1))
+
+
+def test_invalid_arguments_rejected_before_any_device_work():
+    """Argument validation happens on the host, before any CUDA call: every
+    entry point returns PDG_EINVAL (1) with a message, no exception crosses
+    the ABI."""
+    import ctypes as C
+
+    from paper_2506_14851_b200 import _build, _lib
+    _build.build()
+    L = _lib.load()
+    EINVAL = 1
+    null = None
+    assert L.pdg_gittins_rank_f64(null, null, null, -1, 4, null, null) == EINVAL
+    assert L.pdg_gittins_rank_f64_host(null, null, null, 3, 0, null, null) == EINVAL
+    assert L.pdg_policy_keys(7, null, null, null, null, null, C.c_double(0.0), 10, null, null,
+                             null, null) == EINVAL
+    assert L.pdg_policy_keys(2, null, null, null, null, null, C.c_double(0.0), 10, null, null,
+                             null, null) == EINVAL
+    assert L.pdg_dispatch_plan(null, null, null, null, null, null, -1, null, 1,
+                               C.c_double(1.5), 1, 3, null, null, null, null, 0, null) == EINVAL
+    assert L.pdg_order(null, null, null, null, 5, 16, null, 0, null) == EINVAL
+    assert L.pdg_order_update(null, null, null, 4, null, 9, null, null, null, null, 0,
+                              null) == EINVAL
+    assert L.pdg_pearson_flags(null, null, null, null, -2, C.c_double(0.5), null, null,
+                               null) == EINVAL
+    assert L.pdg_prewarm_window_index(null, 1, null, 4, null, null) == EINVAL
+    assert L.pdg_mc_remaining_demand(null, null, 1, 512, 64, 64, 0, 0, null, null, 0,
+                                     null) == EINVAL
+    msg = L.pdg_last_error()
+    assert msg and b"pdg_mc_remaining_demand" in msg
