@@ -213,3 +213,49 @@ def test_visit_cap_zero_and_empty_units(kb_graphs):
     g2 = graph_from_kb(doc)
     with pytest.raises(EstimationError, match="no duration samples"):
         E.monte_carlo_remaining_demand(g2, "a", [], Env, n=8, seed=1)
+
+
+def _wide_graph_doc(rng, n_units=32):
+    """32 units (the per-graph maximum), up to 6 successors per unit (the
+    > 3 successor path), single-sample pools, LLM and duration units."""
+    ids = [f"u{i:02d}" for i in range(n_units)]
+    units = []
+    for i, uid in enumerate(ids):
+        llm = i % 3 == 0
+        n_rec = 1 if i % 7 == 5 else int(rng.integers(20, 60))
+        succ = rng.choice(n_units, size=int(rng.integers(1, 7)), replace=False)
+        recs = []
+        for t in range(n_rec):
+            nxt = None if rng.random() < 0.25 else ids[int(rng.choice(succ))]
+            r = {"trial_id": t, "next_unit": nxt}
+            if llm:
+                r.update(input_len=float(rng.integers(10, 3000)),
+                         output_len=float(rng.integers(5, 900)), parallelism=1)
+            else:
+                r["duration"] = float(rng.lognormal(1, 1))
+            recs.append(r)
+        kind = {"kind": "llm-inference", "model_id": "m"} if llm else \
+            {"kind": "docker-exec", "image_id": f"i{i}"}
+        units.append({"unit_id": uid, "backend": kind, "capacity": 1000, "bucket_count": 10,
+                      "records": recs})
+    return {"app_id": "wide", "entry_unit": ids[0], "units": units}
+
+
+def test_wide_graph_32_units_many_successors():
+    from paper_2506_14851_b200.estimator import DemandEngine
+    from paper_2506_14851_b200.graphs import graph_from_kb
+    rng = np.random.default_rng(31)
+    doc = _wide_graph_doc(rng)
+    eng = DemandEngine({"wide": graph_from_kb(doc)})
+    og = O.graph_from_kb(doc)
+    assert max(len(u.succ) for u in og.units.values()) > 3
+    cases = []
+    for uid in sorted(og.units)[::3]:
+        for n in (1, 37, 300, 512):
+            cases.append({"graph": "wide", "current": uid, "obs": [], "n": n,
+                          "seed": int(rng.integers(0, 2**62)), "visit_cap": 64})
+    got = run_cases(eng, cases)
+    for i, c in enumerate(cases):
+        want = O.mc_remaining_demand(og, c["current"], [], c["n"], c["seed"], c["visit_cap"])
+        np.testing.assert_array_equal(got[i][0], want.samples, err_msg=str(c))
+        assert got[i][1] == want.capped
