@@ -16,6 +16,7 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass
 from enum import Enum
+from itertools import repeat
 from typing import Iterable, NamedTuple, Optional, Sequence
 
 import numpy as np
@@ -231,8 +232,9 @@ def refresh_priorities(live: Iterable, now: float, bucket_period: float,
     start = time.perf_counter_ns()
     rest = due
     if _pv(policy) == "gittins" and due:
-        gapps = [a for a in due if a.remaining is not None]
-        rest = [a for a in due if a.remaining is None]
+        gapps, rest = [], []
+        for a in due:
+            (gapps if a.remaining is not None else rest).append(a)
         if gapps:
             m = len(gapps)
             width0 = gapps[0].bucket_width
@@ -257,8 +259,9 @@ def refresh_priorities(live: Iterable, now: float, bucket_period: float,
                 for a, flagged in zip(gapps, nan.tolist()):
                     if flagged:
                         a.overrun_flagged = True
-            for a, key in zip(gapps, ranks.tolist()):
-                priorities[a.app_instance_id] = Priority(policy, key, a.tiebreak)
+            priorities = dict(zip([a.app_instance_id for a in gapps],
+                                  map(Priority, repeat(policy, m), ranks.tolist(),
+                                      [a.tiebreak for a in gapps])))
     for a in rest:
         priorities[a.app_instance_id] = compute_priority(
             policy, a, now, tenant_service, overrun_penalty_factor)
