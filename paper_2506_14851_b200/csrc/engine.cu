@@ -957,7 +957,13 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
       if (LLM) xb = pl.B[min(uint32_t(ws.ib[k + 32]), lb)];
       st = pcg_stride32(st, lc.c32);
       const uint64_t wd = pcg_out(st);
-      const int v = few_succ ? sc.next3(wd) : sc.next(a, d, wd);
+      // successor decided by as many threshold compares as the unit has
+      constexpr int NS = decltype(few_succ)::value;
+      const uint64_t kk = wd >> 11;
+      const int v = NS == 0 ? sc.n0
+                  : NS == 1 ? (kk < sc.t0 ? sc.n0 : sc.n1)
+                  : NS == 2 ? (kk < sc.t0 ? sc.n0 : kk < sc.t1 ? sc.n1 : sc.n2)
+                  : NS == 3 ? sc.next3(wd) : sc.next(a, d, wd);
       const uint32_t w = ws.mem[k];
       const double t = LLM ? dadd(ca, cb) : ca;    // pools hold i/prefill, o/decode
       ws.tot[w] = dadd(ws.tot[w], t);
@@ -965,8 +971,13 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
       k += 32;
     }
   };
-  if (sc.ns <= 3) uniforms(std::true_type{});
-  else uniforms(std::false_type{});
+  switch (sc.ns) {
+    case 0: uniforms(std::integral_constant<int, 0>{}); break;
+    case 1: uniforms(std::integral_constant<int, 1>{}); break;
+    case 2: uniforms(std::integral_constant<int, 2>{}); break;
+    case 3: uniforms(std::integral_constant<int, 3>{}); break;
+    default: uniforms(std::integral_constant<int, 4>{}); break;
+  }
   if (__any_sync(kFull, rej)) return false;
   ls.st = st;
   const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
