@@ -158,7 +158,16 @@ typedef struct {
   const double* vals_div;         /* vals with LLM input pools / prefill_rate */
                                   /* and output pools / decode_rate (exact  */
                                   /* f64 divisions); durations as in vals   */
+  int32_t features;               /* PDG_BANK_FEATURES_VALID | OR of the    */
+                                  /* PDG_BANK_HAS_* kinds the bank holds;   */
+                                  /* a speed hint only (0: assume all)      */
 } pdg_graph_bank;
+enum {
+  PDG_BANK_HAS_LLM = 1,           /* LLM units (input/output pools)         */
+  PDG_BANK_HAS_OWN_INPUT = 2,     /* output_own_input pools                 */
+  PDG_BANK_HAS_CONDITIONS = 4,    /* K3 masks (estimator.py:299)            */
+  PDG_BANK_FEATURES_VALID = 0x40000000
+};
 
 typedef struct {
   const int32_t* graph;           /* [N] graph index in the bank                      */

@@ -26,7 +26,7 @@ int sm_count() {
 
 extern "C" const char* pdg_last_error(void) { return pdg::g_err; }
 
-extern "C" int pdg_abi_version(void) { return 2; }
+extern "C" int pdg_abi_version(void) { return 3; }
 
 extern "C" int pdg_device_info(int* sms, int* major, int* minor) {
   int dev = 0;

@@ -1159,7 +1159,21 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
 #endif
 constexpr int kWalkWarps = PDG_WALK_WARPS;
 
-__global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel(EngineArgs a) {
+#ifndef PDG_WALK_MINB_LEAN
+#define PDG_WALK_MINB_LEAN 6 // the same for banks without LLM / own-input / K3 units
+#endif
+
+// FEAT: the unit kinds the bank holds (F_LLM, F_OWN, F_ANYMASK bits; the
+// host reads them from pdg_graph_bank.features).  Paths for kinds a bank does
+// not hold are compiled out -- their registers otherwise cost the plain
+// duration walk a resident CTA per SM.  A job that needs a compiled-out path
+// anyway (features understated by the caller) is handed to mc_serial_kernel,
+// so FEAT only ever affects speed.
+template <int FEAT>
+__global__ void __launch_bounds__(kWalkWarps * 32,
+                                  FEAT == 0 ? PDG_WALK_MINB_LEAN : PDG_WALK_MINB)
+mc_walk_kernel(EngineArgs a) {
+  constexpr bool kLLM = FEAT & F_LLM, kOwn = FEAT & F_OWN, kCond = FEAT & F_ANYMASK;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;
@@ -1200,10 +1214,16 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
     int obs_up;
     double obs[3];
     job_obs(a, job, obs_up, obs);
-    const bool has_ov =
+    if (!kCond && obs_up >= 0 &&
+        (reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u0].flags & F_ANYMASK)) {
+      if (lane == 0) a.serial_list[atomicAdd(a.serial_count, 1)] = int32_t(job);
+      __syncwarp();
+      continue;                                  // K3 compiled out: serial path
+    }
+    const bool has_ov = kCond &&
         condition(a, gbase, u0, obs_up, obs, ws.kin, ws.kout, ovp, conditioned, lane);
     Pools ovd = ovp;                             // the override pools, divided
-    if (has_ov) {
+    if (kCond && has_ov) {
       const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
       auto divide = [&](const double* p, int len, const double* buf, double* dbuf,
                         double rate) -> const double* {
@@ -1263,9 +1283,11 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PDG_WALK_MINB) mc_walk_kernel
         if (!(d.flags & F_LLM))
           ok = visit_strided<false>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, ls, lc, targets,
                                     lane);
+        else if (!kLLM)
+          ok = false;                            // compiled out: serial path
         else if ((d.flags & F_OWN) && !ov)
-          ok = visit_own(a, d, succ_of(ws.uc[u]), pools_for(a, d, ov, ovp), pd, ws, m, g, ls,
-                         lc, targets, lane);
+          ok = kOwn && visit_own(a, d, succ_of(ws.uc[u]), pools_for(a, d, ov, ovp), pd, ws, m,
+                                 g, ls, lc, targets, lane);
         else
           ok = visit_strided<true>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, ls, lc, targets,
                                    lane);
@@ -1385,9 +1407,19 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   };
   if (sm) {
     const int mu = bank->max_units < 1 ? 1 : bank->max_units;
-    if (int r = launch(mc_walk_kernel, kWalkWarps,
-                       size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu)))
-      return r;
+    // unit kinds present (pdg_graph_bank.features; VALID bit clear: assume all)
+    int feat = (bank->features & PDG_BANK_FEATURES_VALID) ? (bank->features & 7) : 7;
+    if (!jobs->obs_unit) feat &= ~F_ANYMASK;     // no observations: no K3
+    const size_t smem = size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu);
+    int r = PDG_OK;
+    switch (feat) {
+      case 0: r = launch(mc_walk_kernel<0>, kWalkWarps, smem); break;
+      case 1: r = launch(mc_walk_kernel<1>, kWalkWarps, smem); break;
+      case 4: r = launch(mc_walk_kernel<4>, kWalkWarps, smem); break;
+      case 5: r = launch(mc_walk_kernel<5>, kWalkWarps, smem); break;
+      default: r = launch(mc_walk_kernel<7>, kWalkWarps, smem); break;
+    }
+    if (r) return r;
   } else if (small_idx(n_samples)) {
     if (int r = launch(mc_engine_kernel<uint16_t>, kWarps, size_t(kWarps) * cnt_bytes)) return r;
   } else {

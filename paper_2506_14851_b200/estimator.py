@@ -35,7 +35,7 @@ class GraphBankC(C.Structure):
                 ("succ_cum", C.c_void_p), ("succ_nxt", C.c_void_p), ("conds", C.c_void_p),
                 ("pairs", C.c_void_p), ("jump", C.c_void_p), ("prefill_rate", C.c_double),
                 ("decode_rate", C.c_double), ("succ_thr", C.c_void_p), ("max_units", C.c_int32),
-                ("vals_div", C.c_void_p)]
+                ("vals_div", C.c_void_p), ("features", C.c_int32)]
 
 
 class JobsC(C.Structure):
@@ -121,7 +121,7 @@ class DemandEngine:
             _lib.ptr(b.pool_len), _lib.ptr(b.succ_cum), _lib.ptr(b.succ_nxt),
             _lib.ptr(b.conds), _lib.ptr(b.pairs), _lib.ptr(self.jump),
             float(prefill_rate), float(decode_rate), _lib.ptr(b.succ_thr), int(b.max_units),
-            _lib.ptr(self.vals_div))
+            _lib.ptr(self.vals_div), int(b.features))
         self.max_unit_k = b.max_unit_k
         self.max_pairs = b.max_pairs
 

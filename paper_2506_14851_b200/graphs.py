@@ -35,6 +35,7 @@ import numpy as np
 F_LLM = 1
 F_OWN = 2            # output_own_input mask with records (estimator.py:255)
 F_ANYMASK = 4        # masks.any() (estimator.py:299)
+FEATURES_VALID = 0x40000000   # pdg_graph_bank.features: the kind bits are set
 F_IUI = 8            # input_upstream_input
 F_IUO = 16           # input_upstream_output
 F_OUO = 32           # output_upstream_output
@@ -558,6 +559,11 @@ class GraphBank:
         self.succ_thr = t(np.ceil(cum * 2.0 ** 53).astype(np.uint64).view(np.int64), np.int64)
         self.succ_nxt = t(succ_nxt, np.int32)
         self.max_units = int(np.max(gn)) if len(gn) else 1
+        # unit kinds present (pdg_graph_bank.features: the engine compiles out
+        # the paths of absent kinds)
+        kinds_present = int(np.bitwise_or.reduce(units["flags"] & (F_LLM | F_OWN | F_ANYMASK))
+                            if len(units) else 0)
+        self.features = FEATURES_VALID | kinds_present
         ca = np.array(conds, dtype=COND_DTYPE) if len(conds) else np.zeros(1, COND_DTYPE)
         pa = np.array(pairs, dtype=PAIR_DTYPE) if len(pairs) else np.zeros(1, PAIR_DTYPE)
         self.host_conds = ca

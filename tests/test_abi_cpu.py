@@ -22,7 +22,7 @@ def test_library_exports_header_symbols():
     for name in declared_symbols():
         assert hasattr(L, name), name
     assert set(declared_symbols()) == set(_lib.EXPORTS)
-    assert L.pdg_abi_version() == 2
+    assert L.pdg_abi_version() == 3
 
 
 def test_sm100a_cubin_in_library():

@@ -78,6 +78,26 @@ def test_golden_mc_cases_bit_exact(engine, mc_cases, mc_full):
             np.testing.assert_array_equal(s, mc_full[c["full"]])
 
 
+@pytest.mark.parametrize("kinds", [0, 1, 5])
+def test_understated_bank_features_stay_exact(engine, mc_cases, kinds):
+    """pdg_graph_bank.features is a speed hint: a walk kernel compiled
+    without the LLM / own-input / K3 paths hands the jobs that need them to
+    the serial kernel, so the golden cases stay bit-exact."""
+    from paper_2506_14851_b200.graphs import FEATURES_VALID
+    saved = engine.c_bank.features
+    engine.c_bank.features = FEATURES_VALID | kinds
+    try:
+        cases = mc_cases["cases"]
+        got = run_cases(engine, cases)
+    finally:
+        engine.c_bank.features = saved
+    for i, c in enumerate(cases):
+        s, capped, flags, _ = got[i]
+        assert _sha(s) == c["sha256"], (kinds, i, c["graph"], c["current"], c["n"])
+        assert capped == c["capped"], i
+        assert bool(flags & 1) == c["conditioned"], i
+
+
 def test_config1_all_mc_calls_bit_exact(engine, config1_golden):
     """Every Monte Carlo call of the config-1 simulation (3.5k calls, with
     online-refinement observations) reproduced in one batched launch."""
