@@ -779,13 +779,14 @@ __device__ __forceinline__ Pools pools_div(const EngineArgs& a, const UnitDesc& 
 
 // shared memory per warp: [counters | LLM staging] [tot] [mem] [bitsets of
 // max_units units]
-__host__ __device__ inline size_t walk_union_bytes(int counters) {
-  const size_t c = size_t(counters) * 4, s = size_t(kSmemWalks) * 4;
+// (banks without LLM units stage no B draws: the staging area is ia only)
+__host__ __device__ inline size_t walk_union_bytes(int counters, bool llm = true) {
+  const size_t c = size_t(counters) * 4, s = size_t(kSmemWalks) * (llm ? 4 : 2);
   return align16(c > s ? c : s);
 }
-__host__ __device__ inline size_t walk_smem_bytes(int counters, int units) {
-  return walk_union_bytes(counters) + size_t(kSmemWalks) * 10 + size_t(units) * kWalkWords * 4 +
-         size_t(units) * 112;
+__host__ __device__ inline size_t walk_smem_bytes(int counters, int units, bool llm = true) {
+  return walk_union_bytes(counters, llm) + size_t(kSmemWalks) * 10 +
+         size_t(units) * kWalkWords * 4 + size_t(units) * 112;
 }
 // global scratch per warp: [own-input arrays] [K3 pairs]
 __host__ __device__ inline size_t walk_gmem_bytes() {
@@ -1160,7 +1161,7 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
 constexpr int kWalkWarps = PDG_WALK_WARPS;
 
 #ifndef PDG_WALK_MINB_LEAN
-#define PDG_WALK_MINB_LEAN 6 // the same for banks without LLM / own-input / K3 units
+#define PDG_WALK_MINB_LEAN 7 // the same for banks without LLM / own-input / K3 units
 #endif
 
 // FEAT: the unit kinds the bank holds (F_LLM, F_OWN, F_ANYMASK bits; the
@@ -1177,7 +1178,7 @@ mc_walk_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;
-  unsigned char* sb = smem + walk_smem_bytes(a.counters, a.b.max_units) * wib;
+  unsigned char* sb = smem + walk_smem_bytes(a.counters, a.b.max_units, kLLM) * wib;
   const int64_t gwarp = int64_t(blockIdx.x) * kWalkWarps + wib;
   unsigned char* gs =
       reinterpret_cast<unsigned char*>(a.scratch) + size_t(gwarp) * a.scratch_per_warp;
@@ -1185,7 +1186,7 @@ mc_walk_kernel(EngineArgs a) {
   ws.cnt = reinterpret_cast<uint32_t*>(sb);
   ws.ia = reinterpret_cast<uint16_t*>(sb);
   ws.ib = ws.ia + kSmemWalks;
-  ws.tot = reinterpret_cast<double*>(sb + walk_union_bytes(a.counters));
+  ws.tot = reinterpret_cast<double*>(sb + walk_union_bytes(a.counters, kLLM));
   ws.mem = reinterpret_cast<uint16_t*>(ws.tot + kSmemWalks);
   ws.bits = reinterpret_cast<uint32_t*>(ws.mem + kSmemWalks);
   ws.uc = reinterpret_cast<UnitCache*>(ws.bits + a.b.max_units * kWalkWords);
@@ -1411,11 +1412,12 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
     int feat = (bank->features & PDG_BANK_FEATURES_VALID) ? (bank->features & 7) : 7;
     if (!jobs->obs_unit) feat &= ~F_ANYMASK;     // no observations: no K3
     const size_t smem = size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu);
+    const size_t smem_plain = size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu, false);
     int r = PDG_OK;
     switch (feat) {
-      case 0: r = launch(mc_walk_kernel<0>, kWalkWarps, smem); break;
+      case 0: r = launch(mc_walk_kernel<0>, kWalkWarps, smem_plain); break;
       case 1: r = launch(mc_walk_kernel<1>, kWalkWarps, smem); break;
-      case 4: r = launch(mc_walk_kernel<4>, kWalkWarps, smem); break;
+      case 4: r = launch(mc_walk_kernel<4>, kWalkWarps, smem_plain); break;
       case 5: r = launch(mc_walk_kernel<5>, kWalkWarps, smem); break;
       default: r = launch(mc_walk_kernel<7>, kWalkWarps, smem); break;
     }
