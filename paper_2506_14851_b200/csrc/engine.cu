@@ -750,7 +750,7 @@ struct WalkState {
   uint32_t* cnt;     // [counters] histogram / own-input bucket counters
   uint16_t* ia;      // [kSmemWalks] staged A-draw index per rank (over cnt)
   uint16_t* ib;      // [kSmemWalks] staged B-draw index per rank
-  struct UnitCache* uc;  // [max_units] the application's unit descriptors
+  void* uc;          // [max_units] the application's unit descriptors (UnitCacheOf)
   double* tmp;       // own-input path (global scratch)
   uint16_t* bkt;
   uint16_t* osrt;
@@ -786,7 +786,7 @@ __host__ __device__ inline size_t walk_union_bytes(int counters, bool llm = true
 }
 __host__ __device__ inline size_t walk_smem_bytes(int counters, int units, bool llm = true) {
   return walk_union_bytes(counters, llm) + size_t(kSmemWalks) * 10 +
-         size_t(units) * kWalkWords * 4 + size_t(units) * 112;
+         size_t(units) * kWalkWords * 4 + size_t(units) * (llm ? 112 : 48);
 }
 // global scratch per warp: [own-input arrays] [K3 pairs]
 __host__ __device__ inline size_t walk_gmem_bytes() {
@@ -833,7 +833,37 @@ struct __align__(16) UnitCache {
 };
 static_assert(sizeof(UnitCache) == 112, "unit cache layout");
 
-__device__ __forceinline__ SuccTab succ_of(const UnitCache& c) {
+// the same for banks without LLM units: only what a duration visit reads
+struct __align__(16) UnitCacheLean {
+  uint64_t t0, t1, t2;
+  int32_t a_off, a_len, succ_off;
+  int16_t flags, ns;
+  int8_t n[4];
+};
+static_assert(sizeof(UnitCacheLean) == 48, "lean unit cache layout");
+
+template <bool LLM>
+struct UnitCacheOf { using type = UnitCache; };
+template <>
+struct UnitCacheOf<false> { using type = UnitCacheLean; };
+
+__host__ __device__ constexpr size_t unit_cache_bytes(bool llm) {
+  return llm ? sizeof(UnitCache) : sizeof(UnitCacheLean);
+}
+
+__device__ __forceinline__ UnitDesc desc_of(const UnitCache& c) { return c.d; }
+__device__ __forceinline__ UnitDesc desc_of(const UnitCacheLean& c) {
+  UnitDesc d{};
+  d.flags = c.flags;
+  d.a_off = c.a_off;
+  d.a_len = c.a_len;
+  d.succ_off = c.succ_off;
+  d.succ_len = c.ns;
+  return d;
+}
+
+template <typename Cache>
+__device__ __forceinline__ SuccTab succ_of(const Cache& c) {
   SuccTab s;
   s.t0 = c.t0;
   s.t1 = c.t1;
@@ -1189,7 +1219,9 @@ mc_walk_kernel(EngineArgs a) {
   ws.tot = reinterpret_cast<double*>(sb + walk_union_bytes(a.counters, kLLM));
   ws.mem = reinterpret_cast<uint16_t*>(ws.tot + kSmemWalks);
   ws.bits = reinterpret_cast<uint32_t*>(ws.mem + kSmemWalks);
-  ws.uc = reinterpret_cast<UnitCache*>(ws.bits + a.b.max_units * kWalkWords);
+  using Cache = typename UnitCacheOf<kLLM>::type;
+  Cache* const uc = reinterpret_cast<Cache*>(ws.bits + a.b.max_units * kWalkWords);
+  ws.uc = uc;
   ws.tmp = reinterpret_cast<double*>(gs);
   ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + kSmemWalks);
   ws.osrt = ws.bkt + kSmemWalks;
@@ -1248,9 +1280,17 @@ mc_walk_kernel(EngineArgs a) {
       ls.P = 0;
     }
     if (lane < gn) {                             // stage the unit descriptors
-      UnitCache c;
-      c.d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + lane];
-      const SuccTab t = [&] { SuccTab x; x.load(a, c.d); return x; }();
+      Cache c;
+      const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + lane];
+      if constexpr (kLLM) {
+        c.d = d;
+      } else {
+        c.a_off = d.a_off;
+        c.a_len = d.a_len;
+        c.succ_off = d.succ_off;
+        c.flags = int16_t(d.flags);
+      }
+      const SuccTab t = [&] { SuccTab x; x.load(a, d); return x; }();
       c.t0 = t.t0;
       c.t1 = t.t1;
       c.t2 = t.t2;
@@ -1259,7 +1299,7 @@ mc_walk_kernel(EngineArgs a) {
       c.n[1] = int8_t(t.n1);
       c.n[2] = int8_t(t.n2);
       c.n[3] = int8_t(t.n3);
-      ws.uc[lane] = c;
+      uc[lane] = c;
     }
     for (int i = lane; i < gn * kWalkWords; i += 32) {
       const int u = i / kWalkWords, wi = i - u * kWalkWords;
@@ -1277,20 +1317,20 @@ mc_walk_kernel(EngineArgs a) {
         occ &= occ - 1;
         const uint32_t m = take_members(ws, u, lane);
         pending &= ~(1u << u);
-        const UnitDesc d = ws.uc[u].d;
+        const UnitDesc d = desc_of(uc[u]);
         const bool ov = has_ov && u == u0;
         const Pools pd = pools_div(a, d, ov, ovd);
         unsigned targets = 0;
         if (!(d.flags & F_LLM))
-          ok = visit_strided<false>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, ls, lc, targets,
+          ok = visit_strided<false>(a, d, succ_of(uc[u]), pd, ws, m, g, ls, lc, targets,
                                     lane);
         else if (!kLLM)
           ok = false;                            // compiled out: serial path
         else if ((d.flags & F_OWN) && !ov)
-          ok = kOwn && visit_own(a, d, succ_of(ws.uc[u]), pools_for(a, d, ov, ovp), pd, ws, m,
+          ok = kOwn && visit_own(a, d, succ_of(uc[u]), pools_for(a, d, ov, ovp), pd, ws, m,
                                  g, ls, lc, targets, lane);
         else
-          ok = visit_strided<true>(a, d, succ_of(ws.uc[u]), pd, ws, m, g, ls, lc, targets,
+          ok = visit_strided<true>(a, d, succ_of(uc[u]), pd, ws, m, g, ls, lc, targets,
                                    lane);
         pending |= __reduce_or_sync(kFull, targets);
       }
