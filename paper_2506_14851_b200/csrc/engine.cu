@@ -455,6 +455,7 @@ __device__ void write_result(const EngineArgs& a, int64_t job, const double* tot
   const int n = a.n;
   int capped = 0;
   double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+#pragma unroll 1
   for (int w = lane; w < n; w += 32) {
     if (cur) capped += cur[w] >= 0;
     const double sv = tot[w];
@@ -472,8 +473,10 @@ __device__ void write_result(const EngineArgs& a, int64_t job, const double* tot
   double width = 0.0;
   if (lo == hi) k = 1;
   else width = __ddiv_rn(dsub(hi, lo), small_int_to_double(k));
+#pragma unroll 1
   for (int b = lane; b < k; b += 32) cnt[b] = 0;
   __syncwarp();
+#pragma unroll 1
   for (int w = lane; w < n; w += 32) {
     int idx = 0;
     if (k > 1) {
@@ -485,12 +488,14 @@ __device__ void write_result(const EngineArgs& a, int64_t job, const double* tot
   __syncwarp();
   if (a.o.counts) {
     uint16_t* crow = a.o.counts + row * a.o.stride;
+#pragma unroll 1
     for (int b = lane; b < a.o.stride; b += 32) crow[b] = b < k ? uint16_t(cnt[b]) : 0;
   }
   if (a.o.mean && lane == 0) {
     // RemainingDemand.mean() = sum(samples) / n (estimator.py:55-56) with
     // CPython >= 3.12 sum(): Neumaier-compensated, in sample order
     double f = tot[0], c = 0.0;
+#pragma unroll 1
     for (int w = 1; w < n; ++w) {
       const double x = tot[w];
       const double t = dadd(f, x);
