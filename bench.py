@@ -544,7 +544,9 @@ def bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b, rows=1_000_000, reps=20
                                               / out[pol.value]["roofline"]["peak"])
     out["engine_mean_epilogue"] = {"engine_ms": base_ms, "engine_with_mean_ms": mean_ms,
                                    "apps": n, "note": "RemainingDemand.mean() in CPython "
-                                   "sum() order (sequential, one lane per app)"}
+                                   "sum() order: the running sum and the compensation are sequential "
+                                   "float64 chains (lane 0), the compensation terms are formed "
+                                   "across the warp"}
     return out
 
 

@@ -449,9 +449,69 @@ __device__ bool visit_unit(const EngineArgs& a, int gbase, int u, const Pools& o
 // ---------------------------------------------------------------------------
 // shared epilogue: samples out, capped count, bucketing (distributions.py:79-105)
 // ---------------------------------------------------------------------------
-__device__ void write_result(const EngineArgs& a, int64_t job, const double* tot,
+// RemainingDemand.mean() = sum(samples) / n (estimator.py:55-56) with CPython
+// >= 3.12 sum(): Neumaier-compensated, in sample order.  Both running sums are
+// sequential float64 chains; with a buffer `sb` of n doubles the warp splits
+// the work: lane 0 runs the sum chain (partial sums -> sb), all lanes form the
+// compensation terms, lane 0 runs the compensation chain (same operations in
+// the same order, so the same bits).  tot is overwritten in that case.
+__device__ double neumaier_mean(double* tot, int n, double* sb, int lane) {
+  double f = 0.0;
+  if (!sb) {                                     // one lane, one pass
+    if (lane == 0) {
+      double c = 0.0;
+      f = tot[0];
+#pragma unroll 1
+      for (int w = 1; w < n; ++w) {
+        const double x = tot[w];
+        const double t = dadd(f, x);
+        c = fabs(f) >= fabs(x) ? dadd(c, dadd(dsub(f, t), x)) : dadd(c, dadd(dsub(x, t), f));
+        f = t;
+      }
+      if (c != 0.0 && isfinite(c)) f = dadd(f, c);
+    }
+    return f;
+  }
+  if (lane == 0) {                               // pairs: 16-byte loads / stores
+    const double2* t2 = reinterpret_cast<const double2*>(tot);
+    double2* s2 = reinterpret_cast<double2*>(sb);
+    f = tot[0];
+    sb[0] = f;
+    if (n > 1) sb[1] = f = dadd(f, tot[1]);
+#pragma unroll 4
+    for (int i = 1; i < n / 2; ++i) {
+      const double2 y = t2[i];
+      const double f0 = dadd(f, y.x);
+      f = dadd(f0, y.y);
+      s2[i] = make_double2(f0, f);
+    }
+    if ((n & 1) && n > 1) sb[n - 1] = f = dadd(f, tot[n - 1]);
+  }
+  __syncwarp();
+  for (int w = lane + 1; w < n; w += 32) {       // compensation term of sample w
+    const double p = sb[w - 1], t = sb[w], x = tot[w];
+    tot[w] = fabs(p) >= fabs(x) ? dadd(dsub(p, t), x) : dadd(dsub(x, t), p);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const double2* e2 = reinterpret_cast<const double2*>(tot);
+    double c = 0.0;
+    if (n > 1) c = dadd(c, tot[1]);
+#pragma unroll 4
+    for (int i = 1; i < n / 2; ++i) {
+      const double2 e = e2[i];
+      c = dadd(dadd(c, e.x), e.y);
+    }
+    if ((n & 1) && n > 1) c = dadd(c, tot[n - 1]);
+    if (c != 0.0 && isfinite(c)) f = dadd(f, c);
+  }
+  return f;
+}
+
+__device__ void write_result(const EngineArgs& a, int64_t job, double* tot,
                              const int8_t* cur, uint32_t* cnt, bool conditioned, bool has_ov,
-                             bool replayed, int lane, int capped_walks = -1) {
+                             bool replayed, int lane, int capped_walks = -1,
+                             double* mean_buf = nullptr) {
   const int n = a.n;
   int capped = 0;
   double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
@@ -491,19 +551,9 @@ __device__ void write_result(const EngineArgs& a, int64_t job, const double* tot
 #pragma unroll 1
     for (int b = lane; b < a.o.stride; b += 32) crow[b] = b < k ? uint16_t(cnt[b]) : 0;
   }
-  if (a.o.mean && lane == 0) {
-    // RemainingDemand.mean() = sum(samples) / n (estimator.py:55-56) with
-    // CPython >= 3.12 sum(): Neumaier-compensated, in sample order
-    double f = tot[0], c = 0.0;
-#pragma unroll 1
-    for (int w = 1; w < n; ++w) {
-      const double x = tot[w];
-      const double t = dadd(f, x);
-      c = fabs(f) >= fabs(x) ? dadd(c, dadd(dsub(f, t), x)) : dadd(c, dadd(dsub(x, t), f));
-      f = t;
-    }
-    if (c != 0.0 && isfinite(c)) f = dadd(f, c);
-    a.o.mean[row] = __ddiv_rn(f, small_int_to_double(n));
+  if (a.o.mean) {
+    const double f = neumaier_mean(tot, n, mean_buf, lane);
+    if (lane == 0) a.o.mean[row] = __ddiv_rn(f, small_int_to_double(n));
   }
   if (lane == 0) {
     if (a.o.worst) a.o.worst[row] = hi;
@@ -1348,7 +1398,8 @@ mc_walk_kernel(EngineArgs a) {
     int capped = 0;
     for (int i = lane; i < gn * kWalkWords; i += 32) capped += __popc(ws.bits[i]);
     capped = warp_sum(capped);
-    write_result(a, job, ws.tot, nullptr, ws.cnt, conditioned, has_ov, false, lane, capped);
+    write_result(a, job, ws.tot, nullptr, ws.cnt, conditioned, has_ov, false, lane, capped,
+                 ws.tmp);
   }
 }
 
