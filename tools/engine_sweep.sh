@@ -4,11 +4,11 @@
 set -u
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
-SRC="paper_2506_14851_b200/csrc"
-: > gpurun_out/sweep.txt
+SRC="${SWEEP_SRC:-paper_2506_14851_b200/csrc}"
+[ -n "${SWEEP_APPEND:-}" ] || : > gpurun_out/sweep.txt
 i=0
 for flags in "$@"; do
-  out=/tmp/pdg_var_$i.so
+  out=/tmp/pdg_var_${SWEEP_TAG:-}$i.so
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr \
     -Xcompiler -fPIC -shared -cudart static -I include $flags -o $out \
     $SRC/abi.cu $SRC/gittins.cu $SRC/engine.cu $SRC/prewarm.cu $SRC/dispatch.cu $SRC/masks.cu > /tmp/nvcc_$i.log 2>&1 || { echo "build failed: $flags" >> gpurun_out/sweep.txt; cat /tmp/nvcc_$i.log >> gpurun_out/sweep.txt; i=$((i+1)); continue; }
