@@ -19,6 +19,9 @@
 //     "> now" conditioning of plan_prewarm).  One warp per application, one
 //     lane per window; the sorted service pools make each survival a binary
 //     search.  Output need[N, T, K] (float32) is the HBM-bound part.
+//     prewarm_need_batched_kernel is the production form (packed unit
+//     records + window index): two consecutive applications per warp with
+//     their load chains interleaved, per-warp aggregates without atomics.
 #include "common.cuh"
 
 namespace pdg {
@@ -276,6 +279,142 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
   }
 }
 
+// The same computation for the common layout (packed unit records, window
+// index, dense rows of 4k floats), NB applications per warp at a time: the
+// per-application chain of dependent loads (job -> graph base -> unit record
+// -> window index / samples) is issued for all NB applications before any of
+// them is consumed, so NB chains are in flight per warp instead of one.
+#ifndef PDG_NEED_CONSEC
+#define PDG_NEED_CONSEC 1
+#endif
+#ifndef PDG_NEED_STCS
+#define PDG_NEED_STCS 1
+#endif
+template <typename T>
+__device__ __forceinline__ void need_st(T* p, T v) {
+#if PDG_NEED_STCS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_batched_kernel(NeedArgs a) {
+  extern __shared__ double nsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int TK = a.n_types * a.n_windows, K = a.n_windows;
+  // per warp [T][K] aggregate: lane k owns column k, so plain read-add-write
+  double* cagg = nsm + size_t(wib) * TK;
+  if (a.agg) {
+    for (int i = lane; i < TK; i += 32) cagg[i] = 0.0;
+    __syncwarp();
+  }
+  const int64_t gw = int64_t(blockIdx.x) * kNeedWarps + wib;
+  const int64_t nw = int64_t(gridDim.x) * kNeedWarps;
+  const int kwin = lane < K ? lane : -1;
+  const double wk = kwin >= 0 ? a.windows[kwin] : 0.0;
+  // warp-consecutive applications: a warp's rows form one contiguous run
+  for (int64_t app0 = PDG_NEED_CONSEC ? gw * NB : gw; app0 < a.n; app0 += NB * nw) {
+    int64_t app[NB];
+    int g[NB], un[NB], u[NB], j[NB];
+    double now[NB], s0[NB], sj[NB];
+    int4 r0[NB], r1[NB], r2[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      app[b] = PDG_NEED_CONSEC ? app0 + b : app0 + b * nw;
+      const int64_t q = app[b] < a.n ? app[b] : app0;
+      g[b] = __ldg(a.graph + q);
+      un[b] = __ldg(a.unit + q);
+      now[b] = __ldg(a.now + q);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) u[b] = __ldg(a.graph_base + g[b]) + un[b];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      r0[b] = __ldg(a.unit_rec + 3 * int64_t(u[b]));
+      r1[b] = __ldg(a.unit_rec + 3 * int64_t(u[b]) + 1);
+      r2[b] = __ldg(a.unit_rec + 3 * int64_t(u[b]) + 2);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const double* s = a.svc_sorted + r0[b].x;
+      s0[b] = r0[b].y > 0 ? __ldg(s) : 0.0;
+      j[b] = kwin >= 0 ? __ldg(a.win_idx + int64_t(u[b]) * K + kwin) : 0;
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      sj[b] = j[b] > 0 ? __ldg(a.svc_sorted + r0[b].x + j[b] - 1) : 0.0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (app[b] >= a.n) break;                      // warp-uniform
+      const int n = r0[b].y;
+      const double* s = a.svc_sorted + r0[b].x;
+      const double nw_ = now[b];
+      int first_live = 0;
+      if (n > 0 && !(dadd(nw_, s0[b]) > nw_))
+        first_live = lower_bound_abs(s, n, nw_, __longlong_as_double(
+            __double_as_longlong(nw_) + 1));         // smallest value > now
+      const int live = n - first_live;
+      const int base = live > 0 ? first_live : 0;
+      const int m = live > 0 ? live : n;
+      float pneed = 0.f;
+      if (kwin >= 0 && m > 0) {
+        const double x = dadd(nw_, wk);
+        int jj = j[b];
+        if (jj > 0 && dadd(nw_, sj[b]) >= x) {       // rounding walk-back (rare)
+          --jj;
+          while (jj > 0 && dadd(nw_, s[jj - 1]) >= x) --jj;
+        }
+        jj = jj > base ? jj : base;
+        pneed = 1.f - __fdiv_rn(float(n - jj), float(m));
+      }
+      int t0 = r0[b].z, t1 = r0[b].w, t2 = r1[b].x, t3 = r1[b].y;
+      float f0 = __int_as_float(r1[b].z) * pneed;
+      float f1 = __int_as_float(r1[b].w) * pneed;
+      float f2 = __int_as_float(r2[b].x) * pneed;
+      float f3 = __int_as_float(r2[b].y) * pneed;
+      if (t1 >= 0 && t1 == t0) { f0 += f1; t1 = -1; }
+      if (t2 >= 0 && t2 == t0) { f0 += f2; t2 = -1; }
+      if (t2 >= 0 && t2 == t1) { f1 += f2; t2 = -1; }
+      if (t3 >= 0 && t3 == t0) { f0 += f3; t3 = -1; }
+      if (t3 >= 0 && t3 == t1) { f1 += f3; t3 = -1; }
+      if (t3 >= 0 && t3 == t2) { f2 += f3; t3 = -1; }
+      float4* row4 = reinterpret_cast<float4*>(a.need + app[b] * int64_t(TK));
+#pragma unroll 4
+      for (int i = lane; i < (TK >> 2); i += 32) need_st(row4 + i, make_float4(0.f, 0.f, 0.f, 0.f));
+      __syncwarp();
+      if (kwin >= 0) {
+        float* row = a.need + app[b] * int64_t(TK) + kwin;
+        if (t0 >= 0) need_st(row + t0 * K, f0);
+        if (t1 >= 0) need_st(row + t1 * K, f1);
+        if (t2 >= 0) need_st(row + t2 * K, f2);
+        if (t3 >= 0) need_st(row + t3 * K, f3);
+        if (a.agg) {
+          double* c = cagg + kwin;
+          if (t0 >= 0) c[t0 * K] += double(f0);
+          if (t1 >= 0) c[t1 * K] += double(f1);
+          if (t2 >= 0) c[t2 * K] += double(f2);
+          if (t3 >= 0) c[t3 * K] += double(f3);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (a.agg) {                                       // warps -> CTA -> global
+    __syncthreads();
+    for (int i = threadIdx.x; i < TK; i += blockDim.x) {
+      double v = 0.0;
+      for (int w = 0; w < kNeedWarps; ++w) v += nsm[size_t(w) * TK + i];
+      if (v != 0.0) atomicAdd(a.agg + i, v);
+    }
+  }
+}
+
+#ifndef PDG_NEED_BATCH
+#define PDG_NEED_BATCH 2
+#endif
+
 }  // namespace pdg
 
 using namespace pdg;
@@ -349,6 +488,20 @@ extern "C" int pdg_prewarm_need(const pdg_prewarm_tables* t, const int32_t* grap
              t->succ_nxt, t->succ_p, t->unit_type, graph, unit, now, windows, n_types,
              n_windows, n, need, agg, t->win_idx, t->win_idx ? 0 : kNeedStage,
              reinterpret_cast<const int4*>(t->unit_rec)};
+  if (t->unit_rec && t->win_idx && need && ((n_types * n_windows) & 3) == 0) {
+    auto kern = prewarm_need_batched_kernel<PDG_NEED_BATCH>;
+    const size_t smem = agg ? sizeof(double) * size_t(kNeedWarps) * n_types * n_windows : 0;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(prewarm_need_batched)");
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNeedWarps * 32, smem);
+    int64_t blocks = (n + kNeedWarps * PDG_NEED_BATCH - 1) / (kNeedWarps * PDG_NEED_BATCH);
+    const int64_t cap = int64_t(sm_count()) * (per_sm > 0 ? per_sm : 1);
+    if (blocks > cap) blocks = cap;
+    kern<<<unsigned(blocks), kNeedWarps * 32, smem, (cudaStream_t)stream>>>(a);
+    return launch_status("prewarm_need_batched_kernel");
+  }
   const size_t smem = sizeof(double) * (size_t(kNeedWarps) * a.stage_n +
                                         (agg ? size_t(n_types) * n_windows : 0));
   cudaError_t e = cudaFuncSetAttribute(prewarm_need_kernel,
