@@ -73,3 +73,45 @@ def test_event_stream_parity(kb_graphs):
         r = O.gittins_rank_batch(v[None], b.probs[None], np.array([3.0]))[0]
         assert abs(keys[a] - r) <= 1e-5 * r
     assert conditioned > 0
+
+
+def test_sharded_stream_single_rank_matches(kb_graphs):
+    """ShardedRefinementStream (routing + gathered updates + merged global
+    order) on one rank equals the plain stream batch by batch."""
+    import torch
+    from paper_2506_14851_b200.distributed import ShardedRefinementStream
+    from paper_2506_14851_b200.estimator import DemandEngine
+    from paper_2506_14851_b200.graphs import graph_from_kb
+    from paper_2506_14851_b200.queue import HistQueue
+    from paper_2506_14851_b200.stream import RefinementStream
+    graphs = {k: graph_from_kb(kb_graphs[k]) for k in TEMPLATES}
+    n = 8000
+    q = synth.template_queue(graphs, n, seed=13)
+    eng = DemandEngine(graphs)
+    dev = eng.device
+    streams = []
+    for _ in range(2):
+        hq = HistQueue(n, 64)
+        gi = torch.from_numpy(q["graph"]).to(dev)
+        ui = torch.from_numpy(q["unit"].copy()).to(dev)
+        eng.run(gi, ui, torch.arange(n, dtype=torch.int64, device=dev) * 17, n=512,
+                bucket_count=64, queue=hq)
+        hq.est_age[:n] = 0.0
+        hq.age[:n] = 0.0
+        hq.n = n
+        hq.score()
+        streams.append(RefinementStream(eng, hq, gi, ui, bucket_count=64))
+    plain = streams[0]
+    plain.order()
+    sharded = ShardedRefinementStream(streams[1], n)
+    ev = synth.events(graphs, q, 1200, seed=15)
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+    for lo in range(0, 1200, 300):
+        sl = slice(lo, lo + 300)
+        args = (t(ev["next"][sl], torch.int32), t(ev["seed"][sl], torch.int64),
+                t(ev["completed"][sl], torch.int32), t(ev["obs"][sl], torch.float64),
+                t(np.full(300, 2.0), torch.float64))
+        plain.process(t(ev["app"][sl], torch.int32), *args)
+        got = sharded.process(t(ev["app"][sl], torch.int64), *args)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.cpu().numpy(), plain.order_slots.cpu().numpy())
