@@ -224,3 +224,14 @@ class ShardedRefinementStream:
             "pdg_order_update")
         self.sorted_keys, self._k2 = self._k2, self.sorted_keys
         self.sorted_pos, self._p2 = self._p2, self.sorted_pos
+
+
+def reduce_need_aggregate(agg: torch.Tensor, group=None) -> torch.Tensor:
+    """Config 5 on N GPUs: the [types, windows] need aggregate of every shard
+    (PrewarmTables.need(..., agg=...)) summed over ranks in place (one
+    all-reduce of T*K float64)."""
+    import torch.distributed as dist
+    world, _ = _world(group)
+    if world > 1:
+        dist.all_reduce(agg, op=dist.ReduceOp.SUM, group=group)
+    return agg

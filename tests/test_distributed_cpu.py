@@ -162,6 +162,11 @@ def _stream_worker(rank, world, port, n_total, out):
             assert bool(((g >= lo) & (g < hi)).all())
             assert torch.equal(nu, (g % 5).to(torch.int32))
             assert torch.equal(ov[:, 0], g.double())
+        # config 5: the need aggregate summed over ranks
+        from paper_2506_14851_b200.distributed import reduce_need_aggregate
+        agg = torch.full((16, 32), float(rank + 1), dtype=torch.float64)
+        reduce_need_aggregate(agg)
+        assert bool((agg == 3.0).all())
         # route_events alone: every event reaches exactly its owner
         apps = torch.arange(rank, n_total, world, dtype=torch.int64)
         rows, (tag,) = route_events(apps, [apps * 10], n_total)
