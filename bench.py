@@ -476,6 +476,7 @@ def run_ours(args):
         line["masks"] = bench_masks(dev)
         line["config1_refresh_latency"] = bench_refresh_latency()
         line["k1_refresh_1m"] = bench_k1_large(dev)
+        line["config3_1m"] = bench_config3(dev, eng, n, b)
         del eng, q, w
         torch.cuda.empty_cache()
         line["config4_stream"] = bench_stream(dev)
@@ -492,6 +493,63 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# config 3 on one GPU: a 1M-app queue fully re-scored (engine + K1 + global
+# order), and the 125k-app shard one of 8 GPUs holds
+# ---------------------------------------------------------------------------
+def bench_config3(dev, eng, n_graphs, b, sizes=(1_000_000, 125_000), steps=5):
+    import torch
+
+    from paper_2506_14851_b200 import _lib
+    from paper_2506_14851_b200.queue import HistQueue
+    from tools import synth
+    L = _lib.lib()
+    out = {"graphs": n_graphs,
+           "note": "apps are seeded instances of the config-2 bank's depth-8 graphs "
+                   "(app i walks graph i mod graphs, own unit and seed); step = engine "
+                   "(n=512, bit-exact) + K1b + pdg_order over the whole queue; L2 flushed "
+                   "between steps; the 125k row is one GPU's shard of 1M on 8 GPUs "
+                   "(the 8 MB all-gather is not included)"}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for n in sizes:
+        jb = synth.jobs(n, seed=3003)
+        g = (torch.arange(n, dtype=torch.int64, device=dev) % n_graphs).to(torch.int32)
+        u = torch.from_numpy(jb["unit"]).to(dev)
+        sd = torch.from_numpy(jb["seed"]).to(dev)
+        q = HistQueue(n, b)
+        q.n = n
+        q.est_age[:n] = 0.0
+        q.age[:n] = 1.0
+        ok = torch.empty(n, dtype=torch.int64, device=dev)
+        sl = torch.arange(n, dtype=torch.int32, device=dev)
+        osl = torch.empty_like(sl)
+        tb = int(L.pdg_order_temp_bytes(n))
+        temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
+
+        def step():
+            eng.run(g, u, sd, n=N_SAMP, bucket_count=b, visit_cap=VISIT_CAP, queue=q)
+            q.score(PENALTY)
+            _lib.check(L.pdg_order(_lib.ptr(q.keys), _lib.ptr(ok), _lib.ptr(sl), _lib.ptr(osl),
+                                   n, 32, _lib.ptr(temp), temp.numel(), _lib.stream_ptr()),
+                       "pdg_order")
+        for _ in range(2):
+            step()
+        ms = []
+        for _ in range(steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = float(np.median(ms))
+        out[f"apps{n}"] = {"ms_per_rescore": t, "apps_per_s": n / (t / 1e3)}
+        del q, ok, temp
+        torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
