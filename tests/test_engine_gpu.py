@@ -78,7 +78,7 @@ def test_golden_mc_cases_bit_exact(engine, mc_cases, mc_full):
             np.testing.assert_array_equal(s, mc_full[c["full"]])
 
 
-@pytest.mark.parametrize("kinds", [0, 1, 5])
+@pytest.mark.parametrize("kinds", [0, 1, 4, 5])
 def test_understated_bank_features_stay_exact(engine, mc_cases, kinds):
     """pdg_graph_bank.features is a speed hint: a walk kernel compiled
     without the LLM / own-input / K3 paths hands the jobs that need them to
