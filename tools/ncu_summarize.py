@@ -146,6 +146,29 @@ def main():
                   "", "| kernel | launches | total ms | share |", "|---|---|---|---|"]
         for k, n, t, f in ls:
             lines.append(f"| `{k}` | {n} | {t * 1e3:.3f} | {f * 100:.1f}% |")
+        # the step's own kernels (engine, serial completion, K1, the radix
+        # sort of K5): per-launch means, and the engine's share of their sum
+        step = [(k, n, t) for k, n, t, _ in ls
+                if any(x in k for x in ("mc_walk", "mc_engine", "mc_serial", "gittins_rows",
+                                        "gittins_hist", "DeviceRadixSort"))]
+        if step:
+            per = {}
+            for k, n, t in step:
+                grp = ("engine" if ("mc_walk" in k or "mc_engine" in k) else
+                       "serial" if "mc_serial" in k else
+                       "k1" if "gittins" in k else "sort")
+                per.setdefault(grp, [0.0, 0])
+                per[grp][0] += t
+                # one histogram kernel per radix sort; one launch per step otherwise
+                if grp != "sort" or "Histogram" in k:
+                    per[grp][1] += n
+            mean = {g: t / max(n, 1) for g, (t, n) in per.items()}
+            tot = sum(mean.values()) or 1.0
+            summ["launch_step_share"] = {g: m / tot for g, m in mean.items()}
+            lines += ["", "Step kernels, mean time per step (cold): " +
+                      ", ".join(f"{g} {m * 1e3:.3f} ms" for g, m in mean.items()) +
+                      f"; engine share {mean.get('engine', 0.0) / tot * 100:.1f}% "
+                      "(bench.py's live share_of_step must agree)"]
     summ["_tag"] = tag
     json.dump(summ, open(js_path, "w"), indent=1)
     open(os.path.join(PROF, f"{tag}_ncu.md"), "w").write("\n".join(lines) + "\n")
