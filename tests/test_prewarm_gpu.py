@@ -110,3 +110,56 @@ def test_need_grid_vs_oracle(kb_graphs):
         tot += want
         np.testing.assert_allclose(need[i], want, rtol=1e-6, atol=1e-6)
     np.testing.assert_allclose(agg.cpu().numpy(), tot, rtol=1e-6, atol=1e-6)
+
+
+def test_need_full_size_properties():
+    """Config 5 at full size (1M apps x 16 types x 32 windows): need rows are
+    probabilities, nondecreasing in the window, their per-window sum over
+    types is at most the successors' total probability, the aggregate is the
+    column sum, and a sample of apps equals the oracle."""
+    import torch
+    from paper_2506_14851_b200.prewarm import PrewarmTables
+    from tools import synth
+    A, U, R, T, N = 64, synth.U, 64, 16, 1_000_000
+    w = synth.make(A, R, seed=31)
+    rng = np.random.default_rng(32)
+    svc = np.sort(w["dur"], axis=2)
+    counts = np.zeros((A, U, U))
+    for v in range(U):
+        counts[:, :, v] = (w["nxt"] == v).sum(axis=2)
+    s_len = w["succ_len"].reshape(-1)
+    s_nxt = w["succ_nxt"].reshape(-1)
+    s_p = np.zeros(A * U * synth.SLOT)
+    for a_u in range(A * U):
+        a, u = divmod(a_u, U)
+        for q in range(s_len[a_u]):
+            s_p[a_u * synth.SLOT + q] = counts[a, u, s_nxt[a_u * synth.SLOT + q]] / R
+    utype = rng.integers(0, T, A * U)
+    tb = PrewarmTables(svc_sorted=svc.reshape(-1), svc_off=np.arange(A * U) * R,
+                       svc_len=np.full(A * U, R), graph_base=np.arange(A) * U,
+                       succ_off=np.arange(A * U) * synth.SLOT, succ_len=s_len, succ_nxt=s_nxt,
+                       succ_p=s_p, unit_type=utype, n_types=T)
+    gi = rng.integers(0, A, N).astype(np.int32)
+    ui = rng.integers(0, U, N).astype(np.int32)
+    nowv = rng.uniform(0, 100, N)
+    win = np.linspace(2.0, 64.0, 32)
+    dev = "cuda"
+    need, agg = tb.need(torch.from_numpy(gi).to(dev), torch.from_numpy(ui).to(dev),
+                        torch.from_numpy(nowv).to(dev), torch.tensor(win, device=dev))
+    assert need.shape == (N, T, 32)
+    assert bool((need >= 0).all()) and bool((need <= 1.0 + 1e-6).all())
+    assert bool((need[:, :, 1:] >= need[:, :, :-1]).all())        # CDF in the window
+    psum = torch.from_numpy(s_p.reshape(A * U, synth.SLOT).sum(1)).to(dev)
+    colsum = need.sum(1)                                           # [N, 32]
+    bound = psum[torch.from_numpy(gi.astype(np.int64) * U + ui).to(dev)]
+    assert bool((colsum <= bound[:, None] + 1e-5).all())
+    torch.testing.assert_close(agg, need.double().sum(0), rtol=1e-9, atol=1e-6)
+    sel = rng.choice(N, 300, replace=False)
+    got = need[torch.from_numpy(sel).to(dev)].cpu().numpy()
+    for i, a in enumerate(sel):
+        g_, u_ = int(gi[a]), int(ui[a])
+        base = (g_ * U + u_) * synth.SLOT
+        succ = [(s_p[base + q], int(utype[g_ * U + s_nxt[base + q]]))
+                for q in range(s_len[g_ * U + u_])]
+        want = O.need_grid(svc[g_, u_], succ, nowv[a], win, T)
+        np.testing.assert_allclose(got[i], want, rtol=1e-6, atol=1e-6)
