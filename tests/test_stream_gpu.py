@@ -115,3 +115,44 @@ def test_sharded_stream_single_rank_matches(kb_graphs):
         got = sharded.process(t(ev["app"][sl], torch.int64), *args)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(got.cpu().numpy(), plain.order_slots.cpu().numpy())
+
+
+def test_event_stream_full_size_order(kb_graphs):
+    """Config 4 at full size: a 1M-app queue, 5 micro-batches of 1000 events;
+    the incrementally merged order equals a full re-sort, is a permutation and
+    is sorted by (key, arrival)."""
+    import torch
+    from paper_2506_14851_b200.estimator import DemandEngine
+    from paper_2506_14851_b200.graphs import graph_from_kb
+    from paper_2506_14851_b200.queue import HistQueue
+    from paper_2506_14851_b200.stream import RefinementStream
+    graphs = {k: graph_from_kb(kb_graphs[k]) for k in TEMPLATES}
+    n = 1_000_000
+    q = synth.template_queue(graphs, n, seed=23)
+    eng = DemandEngine(graphs)
+    dev = eng.device
+    hq = HistQueue(n, 256)
+    gi = torch.from_numpy(q["graph"]).to(dev)
+    ui = torch.from_numpy(q["unit"].copy()).to(dev)
+    eng.run(gi, ui, torch.arange(n, dtype=torch.int64, device=dev) * 13, n=512,
+            bucket_count=256, queue=hq)
+    hq.est_age[:n] = 0.0
+    hq.age[:n] = 0.0
+    hq.n = n
+    hq.score()
+    st = RefinementStream(eng, hq, gi, ui, bucket_count=256)
+    st.order()
+    ev = synth.events(graphs, q, 5000, seed=29)
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+    for lo in range(0, 5000, 1000):
+        sl = slice(lo, lo + 1000)
+        st.process(t(ev["app"][sl], torch.int32), t(ev["next"][sl], torch.int32),
+                   t(ev["seed"][sl], torch.int64), t(ev["completed"][sl], torch.int32),
+                   t(ev["obs"][sl], torch.float64), t(np.full(1000, 4.0), torch.float64))
+    inc = st.order_slots.clone()
+    full = st.order()
+    assert torch.equal(inc, full)
+    o = full.long()
+    assert torch.equal(torch.sort(o).values, torch.arange(n, device=dev))
+    k = hq.keys[:n][o]
+    assert bool((k[1:] > k[:-1]).all())          # packed (key, arrival): strictly increasing
