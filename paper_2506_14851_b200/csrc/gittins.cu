@@ -431,8 +431,14 @@ struct HostStage {
   double* h = nullptr;     // pinned host
   double* d = nullptr;     // device
   size_t cap = 0;          // doubles
+  double* zh = nullptr;    // mapped pinned host (small batches: read in place by the kernel)
+  double* zd = nullptr;    // its device alias
+  size_t zcap = 0;
 };
 thread_local HostStage g_stage;
+#ifndef PDG_ZERO_COPY_MAX
+#define PDG_ZERO_COPY_MAX (1u << 17)   // doubles (1 MiB): batches up to this skip the copies
+#endif
 }  // namespace
 
 extern "C" int pdg_gittins_rank_f64_host(const double* values, const double* probs,
@@ -447,6 +453,30 @@ extern "C" int pdg_gittins_rank_f64_host(const double* values, const double* pro
   const size_t nb = size_t(n_rows) * size_t(n_bins);
   const size_t need = 2 * nb + 2 * size_t(n_rows);
   HostStage& st = g_stage;
+  if (need <= PDG_ZERO_COPY_MAX) {
+    // scheduler-sized batch: the kernel reads the rows from mapped pinned
+    // memory and writes the ranks back there -- one launch and one sync, no
+    // copy calls on the latency path
+    if (!st.zh) {
+      cudaError_t e = cudaHostAlloc(&st.zh, PDG_ZERO_COPY_MAX * sizeof(double),
+                                    cudaHostAllocMapped);
+      if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_f64_host cudaHostAlloc");
+      e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&st.zd), st.zh, 0);
+      if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_f64_host map");
+      st.zcap = PDG_ZERO_COPY_MAX;
+    }
+    std::memcpy(st.zh, values, nb * sizeof(double));
+    std::memcpy(st.zh + nb, probs, nb * sizeof(double));
+    std::memcpy(st.zh + 2 * nb, ages, size_t(n_rows) * sizeof(double));
+    const size_t in = 2 * nb + size_t(n_rows);
+    int rc = pdg_gittins_rank_f64(st.zd, st.zd + nb, st.zd + 2 * nb, n_rows, n_bins,
+                                  st.zd + in, stream);
+    if (rc != PDG_OK) return rc;
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_f64_host sync");
+    std::memcpy(out_rank, st.zh + in, size_t(n_rows) * sizeof(double));
+    return PDG_OK;
+  }
   if (need > st.cap) {
     size_t cap = 4096;
     while (cap < need) cap <<= 1;
