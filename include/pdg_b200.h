@@ -50,8 +50,9 @@ int pdg_gittins_rank_f64(const double* values, const double* probs,
                          const double* ages, int64_t n_rows, int32_t n_bins,
                          double* out_rank, void* stream);
 /* Same with HOST pointers (what the reference-facing drop-in passes): the
- * library stages them through a reused pinned buffer, runs the kernel on
- * `stream` and returns after the ranks are back in out_rank. */
+ * library stages them through a reused pinned buffer (batches up to 1 MiB in
+ * mapped memory the kernel reads in place; larger ones copied up and back),
+ * runs the kernel on `stream` and returns after the ranks are in out_rank. */
 int pdg_gittins_rank_f64_host(const double* values, const double* probs,
                               const double* ages, int64_t n_rows, int32_t n_bins,
                               double* out_rank, void* stream);

@@ -74,8 +74,9 @@ class RefreshResult:
 
 def gittins_rank_batch(values, probs, ages) -> np.ndarray:
     """Gittins ranks of N aligned support rows; NaN marks exhausted rows.
-    Host arrays go straight to the C ABI (pdg_gittins_rank_f64_host: one
-    staged upload, the K1a kernel, one download)."""
+    Host arrays go straight to the C ABI (pdg_gittins_rank_f64_host: small
+    batches are read in place by the K1a kernel from mapped pinned memory,
+    large ones take one staged upload and one download)."""
     v = np.ascontiguousarray(values, dtype=np.float64)
     p = np.ascontiguousarray(probs, dtype=np.float64)
     a = np.ascontiguousarray(ages, dtype=np.float64)
