@@ -475,6 +475,7 @@ def run_ours(args):
         line["k6_dispatch"] = bench_dispatch(dev)
         line["masks"] = bench_masks(dev)
         line["config1_refresh_latency"] = bench_refresh_latency()
+        line["config1_simulation"] = bench_config1_sim()
         line["k1_refresh_1m"] = bench_k1_large(dev)
         line["config3_1m"] = bench_config3(dev, eng, n, b)
         del eng, q, w
@@ -651,6 +652,20 @@ def bench_k1_large(dev, n=1_000_000, reps=20):
 # config 1: the paper's "policy runtime" (refresh_priorities elapsed_ns,
 # sched.py:269-310) at scheduler-sized batches, drop-in vs the reference
 # ---------------------------------------------------------------------------
+
+def bench_config1_sim():
+    """Config 1 end to end: the reference simulator with its own hot path and
+    with the GPU drop-in (same event log), and the Monte Carlo call latency."""
+    try:
+        from tools.config1_sim_time import measure
+        r = measure()
+    except ImportError as e:
+        return {"unavailable": f"reference pdgsim not importable: {e}"}
+    r["note"] = ("BASELINE config 1 (1000 apps, code-gen + fact-verify, 64 buckets, Gittins, "
+                 "plan prewarm): simcore.run_simulation wall time; MC p50 over the "
+                 "simulation's own monte_carlo_remaining_demand calls (one app each)")
+    return r
+
 
 def bench_refresh_latency():
     try:

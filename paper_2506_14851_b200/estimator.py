@@ -95,6 +95,7 @@ class DemandEngine:
         self._rates = (float(prefill_rate), float(decode_rate))
         self._bind()
         self._scratch = None
+        self._one = {}                  # n -> (pinned host, device, view) for run_one
 
     def refresh(self, name: str, graph=None) -> None:
         """Template refresh after profiling trials were recorded into graph
@@ -194,6 +195,50 @@ class DemandEngine:
         return {"samples": out_samples, "capped": capped, "flags": flags, "queue": queue}
 
 
+    def run_one(self, name: str, unit_local: int, seed: int, obs_up: int, obs_vals,
+                n: int, visit_cap: int = WALK_VISIT_CAP):
+        """One application, host values in and out (the drop-in's call): the
+        job record goes up and the samples, capped count and flags come back
+        through one reused pinned staging buffer -- one upload, one launch, one
+        download, one synchronisation.  Returns (samples f64[n] numpy view of
+        the staging buffer, capped, flags); copy the samples before the next
+        call."""
+        if n < 1:
+            raise EstimationError(f"sample count must be >= 1, got {n}")
+        if name in self.bank.empty_units:
+            raise EstimationError(self.bank.empty_units[name][0][1])
+        st = self._one.get(n)
+        if st is None:
+            nbytes = 64 + 8 * n + 16
+            h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+            d = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            hv = h.numpy()
+            st = self._one[n] = (h, d, hv)
+        h, d, hv = st
+        base = _lib.ptr(d)
+        job = hv[:64]
+        job[0:16].view(np.int32)[:] = (self.bank.index[name], unit_local, obs_up, 0)
+        job[16:24].view(np.int64)[0] = int(seed)
+        job[24:48].view(np.float64)[:] = obs_vals
+        stream = torch.cuda.current_stream(self.device)
+        d[:64].copy_(h[:64], non_blocking=True)
+        jobs = JobsC(base, base + 4, base + 16, base + 8, base + 24)
+        out = OutC(base + 64, n, None, None, None, None, None, 1, None, base + 64 + 8 * n,
+                   base + 68 + 8 * n, None, None)
+        scratch = self._scratch_for(n, 1)
+        L = _lib.lib()
+        _lib.check(L.pdg_mc_remaining_demand(
+            C.byref(self.c_bank), C.byref(jobs), 1, n, visit_cap, 1, self.max_unit_k,
+            self.max_pairs, C.byref(out), _lib.ptr(scratch), scratch.numel(),
+            _lib.stream_ptr(stream)), "pdg_mc_remaining_demand")
+        d2 = d[64:]
+        h[64:].copy_(d2, non_blocking=True)
+        stream.synchronize()
+        tail = hv[64 + 8 * n:]
+        return (hv[64:64 + 8 * n].view(np.float64), int(tail[:4].view(np.int32)[0]),
+                int(tail[4]))
+
+
 # ---------------------------------------------------------------------------
 # drop-in single-application API (estimator.py:305-362)
 # ---------------------------------------------------------------------------
@@ -225,17 +270,9 @@ def monte_carlo_remaining_demand(graph, current_unit: str, observations: Sequenc
     if current_unit not in graph.units:
         raise EstimationError(f"unknown unit {current_unit!r}")
     eng, name = engine_for(graph, env)
-    dev = eng.device
     up, vals = eng.relevant_observation(name, current_unit, observations)
-    t = lambda a, dt: torch.tensor(a, dtype=dt, device=dev)  # noqa: E731
-    k = 1  # histogram not needed by the drop-in caller; smallest row
-    res = eng.run(t([0], torch.int32), t([eng.bank.local_unit(name, current_unit)], torch.int32),
-                  t([int(seed)], torch.int64), t([up], torch.int32),
-                  t([list(vals)], torch.float64), n=n, bucket_count=k, visit_cap=visit_cap,
-                  samples=True)
-    s = res["samples"][0].cpu().numpy()
-    capped = int(res["capped"][0].item())
-    flags = int(res["flags"][0].item())
+    s, capped, flags = eng.run_one(name, eng.bank.local_unit(name, current_unit), int(seed), up,
+                                   vals, n, visit_cap)
     if capped:
         import logging
         logging.getLogger(__name__).warning(
