@@ -132,6 +132,42 @@ def lstf_slack(dist, age: float, deadline: float, now: float) -> float:
 # a4: set_remaining's bucket view (sched.py:170-181, distributions.py:79-133)
 # ---------------------------------------------------------------------------
 
+_STAGE: dict = {}                 # reused pinned host + device buffer per size class
+
+
+def _stage(nbytes: int):
+    cap = 1 << max(12, (nbytes - 1).bit_length())
+    st = _STAGE.get(cap)
+    if st is None:
+        h = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        st = _STAGE[cap] = (h, torch.empty(cap, dtype=torch.uint8, device="cuda"), h.numpy())
+    return st
+
+
+def _bucketize_staged(x: np.ndarray, bucket_count: int, stride: int):
+    """Small batches (the drop-in's one row per call): one upload, the
+    kernel, one download and one synchronisation through a reused pinned
+    buffer."""
+    R, n = x.shape
+    off_lo = (R * n * 8 + 15) // 16 * 16
+    off_w, off_nb, off_c = off_lo + 8 * R, off_lo + 16 * R, off_lo + 20 * R
+    off_c = (off_c + 15) // 16 * 16
+    end = off_c + 2 * R * stride
+    h, d, hv = _stage(end)
+    hv[:8 * R * n] = x.reshape(-1).view(np.uint8)
+    stream = torch.cuda.current_stream()
+    d[:8 * R * n].copy_(h[:8 * R * n], non_blocking=True)
+    base = _lib.ptr(d)
+    _lib.check(_lib.lib().pdg_bucketize(base, R, n, int(bucket_count), base + off_lo,
+                                        base + off_w, base + off_nb, base + off_c, stride,
+                                        _lib.stream_ptr(stream)), "pdg_bucketize")
+    h[off_lo:end].copy_(d[off_lo:end], non_blocking=True)
+    stream.synchronize()
+    return (hv[off_lo:off_w].view(np.float64).copy(), hv[off_w:off_nb].view(np.float64).copy(),
+            hv[off_nb:off_nb + 4 * R].view(np.int32).copy(),
+            hv[off_c:end].view(np.uint16).reshape(R, stride).copy())
+
+
 def bucketize_rows(samples, bucket_count: int):
     """GPU bucketing of sample rows [R, n] -> (lo, width, nbins, counts u16)."""
     x = np.ascontiguousarray(np.asarray(samples, dtype=np.float64))
@@ -139,6 +175,8 @@ def bucketize_rows(samples, bucket_count: int):
         x = x[None, :]
     R, n = x.shape
     stride = (int(bucket_count) + 7) // 8 * 8
+    if R * n <= (1 << 17) and 1 <= n <= 65535 and 1 <= bucket_count <= 1024:
+        return _bucketize_staged(x, bucket_count, stride)
     L = _lib.lib()
     dev = torch.device("cuda")
     t = torch.from_numpy(x).to(dev)
