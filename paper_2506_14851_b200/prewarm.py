@@ -63,6 +63,8 @@ def plan_prewarm_batch(samples: Sequence[Sequence[float]], bucket_count, p_s, t_
         raise ValueError("warm-up duration must be >= 0")
     if J == 0:
         return np.zeros(0, bool), np.zeros(0), np.zeros(0)
+    if J <= 256 and pool.size <= (1 << 16):
+        return _plan_staged(pool, offs, lens, bucket_count, p_s, t_p, knob, now, J)
     tpool = torch.from_numpy(pool if pool.size else np.zeros(1)).to(dev)
     has = torch.empty(J, dtype=torch.uint8, device=dev)
     trig = torch.empty(J, dtype=torch.float64, device=dev)
@@ -74,6 +76,39 @@ def plan_prewarm_batch(samples: Sequence[Sequence[float]], bucket_count, p_s, t_
                                   _lib.ptr(has), _lib.ptr(trig), _lib.ptr(pe),
                                   _lib.stream_ptr()), "pdg_plan_prewarm")
     return has.cpu().numpy().astype(bool), trig.cpu().numpy(), pe.cpu().numpy()
+
+
+def _plan_staged(pool, offs, lens, bucket_count, p_s, t_p, knob, now, J):
+    """Small batches (the drop-in's one job per call): every input in one
+    pinned upload, the kernel, one download, one synchronisation."""
+    from .sched import _stage
+    P = max(int(pool.size), 1)
+    o_i = 8 * P                                   # int32 columns: offs, lens, bucket_count
+    o_f = (o_i + 12 * J + 15) // 16 * 16          # float64 columns: p_s, t_p, knob, now
+    o_out = o_f + 32 * J                          # outputs: trigger, p_e, has_plan
+    end = o_out + 17 * J
+    h, d, hv = _stage(end)
+    if pool.size:
+        hv[:8 * pool.size] = pool.view(np.uint8)
+    ic = hv[o_i:o_i + 12 * J].view(np.int32).reshape(3, J)
+    ic[0], ic[1] = offs, lens
+    ic[2] = np.broadcast_to(np.asarray(bucket_count, dtype=np.int32), (J,))
+    fc = hv[o_f:o_out].view(np.float64).reshape(4, J)
+    for i, x in enumerate((p_s, t_p, knob, now)):
+        fc[i] = np.broadcast_to(np.asarray(x, dtype=np.float64), (J,))
+    stream = torch.cuda.current_stream()
+    d[:o_out].copy_(h[:o_out], non_blocking=True)
+    b = _lib.ptr(d)
+    _lib.check(_lib.lib().pdg_plan_prewarm(
+        b, b + o_i, b + o_i + 4 * J, b + o_i + 8 * J, b + o_f, b + o_f + 8 * J,
+        b + o_f + 16 * J, b + o_f + 24 * J, J, b + o_out + 16 * J, b + o_out, b + o_out + 8 * J,
+        _lib.stream_ptr(stream)), "pdg_plan_prewarm")
+    h[o_out:end].copy_(d[o_out:end], non_blocking=True)
+    stream.synchronize()
+    trig = hv[o_out:o_out + 8 * J].view(np.float64).copy()
+    pe = hv[o_out + 8 * J:o_out + 16 * J].view(np.float64).copy()
+    has = hv[o_out + 16 * J:end].astype(bool)
+    return has, trig, pe
 
 
 def plan_prewarm(completion_dist, p_s: float, t_p: float, knob: float, now: float,
