@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--apps", type=int, default=N_APPS)
     ap.add_argument("--bins", type=int, default=N_BINS)
-    ap.add_argument("--cpu-apps", type=int, default=1200,
+    ap.add_argument("--cpu-apps", type=int, default=3000,
                     help="apps in the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
@@ -136,7 +136,7 @@ def run_reference(args):
     if rank != 0:
         return
     procs = os.cpu_count() or 1
-    sample = max(procs * 40, 80)
+    sample = max(procs * 300, 600)           # ~0.5-1 s of work per step on the box
     for _ in range(max(args.warmup, 1)):
         cpu_rate(min(sample, procs * 4), procs, sample, 1000, args.bins)
     rates = [cpu_rate(sample, procs, sample, 1000 + s, args.bins) for s in range(args.steps)]
