@@ -115,6 +115,20 @@ int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
               int32_t begin_bit, void* temp, size_t temp_bytes, void* stream);
 
 
+/* K5 across ranks (distributed.global_order's exchange as one C call):
+ * ncclAllGather of every rank's `width` packed keys (shards padded with
+ * 0x7FFFFFFFFFFFFFFF, which sorts last) into gathered[world * width] on
+ * `stream`, then a radix sort of the gathered keys into sorted_keys (the
+ * positions are the low 32 bits).  begin_bit = 32 is exact when every shard
+ * is in arrival order (the rank-major gather then is too).  nccl_comm: the
+ * caller's ncclComm_t; NCCL is resolved at run time (libnccl.so.2), and
+ * PDG_EUNSUPPORTED is returned if it cannot be found.  Replaces the Python
+ * min()/sort over _task_sort_key for a sharded queue (simcore.py:339-344). */
+size_t pdg_rank_allgather_sort_temp_bytes(int64_t width, int32_t world);
+int pdg_rank_allgather_sort(void* nccl_comm, const uint64_t* local_keys, int64_t width,
+                            int32_t world, uint64_t* gathered, uint64_t* sorted_keys,
+                            int32_t begin_bit, void* temp, size_t temp_bytes, void* stream);
+
 /* K5b  incremental order after re-scoring rows[0..m) (distinct): the previous
  * order (sorted_*_in, produced by pdg_order with begin_bit 0 or by this call)
  * minus those rows, merged with their new keys (keys[] holds every row's

@@ -11,7 +11,7 @@ for flags in "$@"; do
   out=/tmp/pdg_k1_$i.so
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr \
     -Xcompiler -fPIC -shared -cudart static -I include $flags -o $out \
-    $SRC/abi.cu $SRC/gittins.cu $SRC/engine.cu $SRC/prewarm.cu $SRC/dispatch.cu $SRC/masks.cu \
+    $SRC/*.cu \
     > /tmp/nvcc_k1_$i.log 2>&1 || { echo "build failed: $flags" >> gpurun_out/k1_sweep.txt; i=$((i+1)); continue; }
   echo "== $flags" >> gpurun_out/k1_sweep.txt
   PDG_LIB_PATH=$out timeout 300 python -c "
