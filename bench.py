@@ -896,13 +896,25 @@ def bench_need(dev, n_apps=1_000_000, n_templates=1024, steps=10):
         e1.record()
     torch.cuda.synchronize()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    # the per-successor latest-safe triggers (plan_prewarm per (app, successor))
+    warm = torch.from_numpy(rng.uniform(1.0, 30.0, 16)).to(dev)
+    tb.triggers(g, u, now, warm, 0.3, N_BINS)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    has, _, _ = tb.triggers(g, u, now, warm, 0.3, N_BINS)
+    e1.record()
+    torch.cuda.synchronize()
+    trig = {"ms": e0.elapsed_time(e1), "plans": int(has.sum().item()),
+            "note": "plan_prewarm (bit-exact) for every (app, successor slot), knob 0.3, "
+                    "256 buckets, warm-up per backend type U(1, 30) s"}
     # algorithmic bytes per app: dense need row out + job (graph, unit, now)
     # + the binary-searched service samples (<= 32 lanes x log2(256) probes)
     bytes_app = 16 * 32 * 4 + 4 + 4 + 8
     peak, _ = measured_peaks()
     return {"workload": f"config5: need[{n_apps},16,32] float32 + [16,32] aggregate over "
                         f"{n_apps} apps ({n_templates} depth-8 templates)",
-            "apps_per_s": n_apps / (ms / 1e3), "ms_per_launch": ms,
+            "apps_per_s": n_apps / (ms / 1e3), "ms_per_launch": ms, "triggers": trig,
             "roofline": {"bound": "hbm", "bytes_per_app": bytes_app,
                          "achieved": bytes_app * n_apps / (ms / 1e3) / 1e9, "peak": peak,
                          "unit": "GB/s",

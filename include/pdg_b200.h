@@ -320,6 +320,21 @@ int pdg_prewarm_need(const pdg_prewarm_tables* tables, const int32_t* graph,
                      const double* windows, int32_t n_windows, int32_t n_types,
                      float* need, double* agg, void* stream);
 
+/* Config 5's per-successor plans: plan_prewarm (prewarm.py:42-96) for every
+ * (application, successor slot < 4) of a queue, with the completion
+ * distribution _plan_prewarms builds (simcore.py:450-478: now + the current
+ * unit's service samples, bucket_count buckets), p_s the branch probability
+ * and t_p = warmup_by_type[type of the successor].  Outputs [n, 4]; slots
+ * without a successor or whose successor has no warm content (type < 0) get
+ * has_plan = 0.  Bit-identical to plan_prewarm.  temp:
+ * pdg_prewarm_triggers_temp_bytes(n) bytes. */
+size_t pdg_prewarm_triggers_temp_bytes(int64_t n);
+int pdg_prewarm_triggers(const pdg_prewarm_tables* tables, const int32_t* graph,
+                         const int32_t* unit, const double* now, int64_t n,
+                         const double* warmup_by_type, int32_t n_types, double knob,
+                         int32_t bucket_count, uint8_t* has_plan, double* trigger, double* p_e,
+                         void* temp, size_t temp_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Correlation masks: estimator.pearson (estimator.py:
  * 62-81) for a batch of (x, y) pairs laid out at x/y[off[j] .. off[j]+len[j]);

@@ -41,14 +41,15 @@ struct PlanArgs {
   double* p_e;
   double* scratch;          // per-warp conditioned samples
   int scratch_per_warp;
+  const double* shift;      // optional [J]: samples are relative, completion = shift + s
 };
 
 // count of cond samples >= x (cond = samples > now, or all if none)
 __device__ __forceinline__ int count_ge(const double* s, int n, double now, bool all, double x,
-                                       int lane) {
+                                       int lane, bool rel = false, double sh = 0.0) {
   int c = 0;
   for (int i = lane; i < n; i += 32) {
-    const double v = s[i];
+    const double v = rel ? dadd(sh, s[i]) : s[i];
     c += ((all || v > now) && v >= x) ? 1 : 0;
   }
   return warp_sum(c);
@@ -62,24 +63,48 @@ __global__ void __launch_bounds__(128) prewarm_plan_kernel(PlanArgs a) {
     const double* s = a.pool + a.off[j];
     const int n = a.len[j];
     const double now = a.now[j], p_s = a.p_s[j], t_p = a.t_p[j], knob = a.knob[j];
+    const bool rel = a.shift != nullptr;             // completion = shift + sample (simcore.py:455)
+    const double sh = rel ? a.shift[j] : 0.0;
     if (p_s < knob || n <= 0) {                      // prewarm.py:63-64
       if (lane == 0) { a.has_plan[j] = 0; a.trigger[j] = 0.0; a.p_e[j] = 0.0; }
       continue;
     }
+    // relative pools are sorted (the prewarm tables) and shift + s is
+    // monotone in s: conditioned samples and those >= x are suffixes
+    auto first_ge = [&](double y, bool strict) {
+      int lo_i = 0, hi_i = n;
+      while (lo_i < hi_i) {
+        const int mid = (lo_i + hi_i) >> 1;
+        const double v = dadd(sh, s[mid]);
+        if (strict ? v > y : v >= y) hi_i = mid; else lo_i = mid + 1;
+      }
+      return lo_i;
+    };
     // conditioning on "still running" (prewarm.py:65-67)
     int live = 0;
     double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
-    for (int i = lane; i < n; i += 32) live += s[i] > now ? 1 : 0;
-    live = warp_sum(live);
+    int start_gt = 0;                                // first sample > now (sorted pools)
+    if (rel) {
+      start_gt = first_ge(now, true);
+      live = n - start_gt;
+    } else {
+      for (int i = lane; i < n; i += 32) live += s[i] > now ? 1 : 0;
+      live = warp_sum(live);
+    }
     const bool all = live == 0;
     const int m = all ? n : live;
-    for (int i = lane; i < n; i += 32) {
-      const double v = s[i];
-      if (all || v > now) { lo = fmin(lo, v); hi = fmax(hi, v); }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
-      hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
+    if (rel) {                                       // sorted: the suffix's ends
+      lo = dadd(sh, s[all ? 0 : start_gt]);
+      hi = dadd(sh, s[n - 1]);
+    } else {
+      for (int i = lane; i < n; i += 32) {
+        const double v = s[i];
+        if (all || v > now) { lo = fmin(lo, v); hi = fmax(hi, v); }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(kFull, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(kFull, hi, o));
+      }
     }
     // bucket boundaries (distributions.py:120-126): [lo] if degenerate, else
     // lo + j*w for j = 0..k with w = (hi - lo)/k
@@ -101,9 +126,15 @@ __global__ void __launch_bounds__(128) prewarm_plan_kernel(PlanArgs a) {
       }
       const double x = dadd(ts, t_p);
       int cnt = 0;
-      for (int i = 0; i < n; ++i) {
-        const double v = s[i];
-        cnt += ((all || v > now) && v >= x) ? 1 : 0;
+      if (rel) {                                     // one binary search, not a scan
+        const int start = all ? 0 : start_gt;
+        const int from = first_ge(x, false);
+        cnt = n - (from > start ? from : start);
+      } else {
+        for (int i = 0; i < n; ++i) {
+          const double v = s[i];
+          cnt += ((all || v > now) && v >= x) ? 1 : 0;
+        }
       }
       const double pe = dmul(p_s, __ddiv_rn(small_int_to_double(cnt), small_int_to_double(m)));
       if (pe >= knob && ts > best_ts) { best_ts = ts; best_pe = pe; any = true; }
@@ -117,7 +148,7 @@ __global__ void __launch_bounds__(128) prewarm_plan_kernel(PlanArgs a) {
     }
     if (!anyw) {                                     // prewarm.py:87-96
       const double x = dadd(now, t_p);
-      const int cnt = count_ge(s, n, now, all, x, lane);
+      const int cnt = count_ge(s, n, now, all, x, lane, rel, sh);
       best_ts = now;
       best_pe = dmul(p_s, __ddiv_rn(small_int_to_double(cnt), small_int_to_double(m)));
     }
@@ -431,7 +462,7 @@ extern "C" int pdg_plan_prewarm(const double* pool, const int32_t* off, const in
   }
   if (n_jobs == 0) return PDG_OK;
   PlanArgs a{pool, off, len, bucket_count, p_s, t_p, knob, now, n_jobs, has_plan, trigger, p_e,
-             nullptr, 0};
+             nullptr, 0, nullptr};
   int64_t blocks = (n_jobs * 32 + 127) / 128;
   const int64_t cap = int64_t(sm_count()) * 16;
   if (blocks > cap) blocks = cap;
@@ -514,4 +545,93 @@ extern "C" int pdg_prewarm_need(const pdg_prewarm_tables* t, const int32_t* grap
   if (blocks > cap) blocks = cap;
   prewarm_need_kernel<<<unsigned(blocks), kNeedWarps * 32, smem, (cudaStream_t)stream>>>(a);
   return launch_status("prewarm_need_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Config 5 triggers: plan_prewarm for every (application, successor slot) of
+// a queue, straight from the prewarm tables -- the completion distribution is
+// now + the current unit's service samples (simcore.py:450-478), so the
+// sorted pool serves as the relative sample list (plan_prewarm only uses
+// order-free statistics of it).  A setup kernel lays out the K4a jobs.
+// ---------------------------------------------------------------------------
+namespace pdg {
+__global__ void trigger_jobs_kernel(pdg_prewarm_tables t, const int32_t* __restrict__ graph,
+                                    const int32_t* __restrict__ unit,
+                                    const double* __restrict__ now, int64_t n,
+                                    const double* __restrict__ warmup, int32_t n_types,
+                                    double knob, int32_t bucket_count, int32_t* off,
+                                    int32_t* len, int32_t* bc, double* p_s, double* t_p,
+                                    double* kn, double* nw) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < 4 * n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t app = j >> 2;
+    const int slot = int(j & 3);
+    const int gb = t.graph_base[graph[app]];
+    const int u = gb + unit[app];
+    const int ns = t.succ_len[u];
+    int ty = -1;
+    double p = 0.0;
+    if (slot < ns) {
+      const int so = t.succ_off[u] + slot;
+      ty = t.unit_type[gb + t.succ_nxt[so]];
+      p = t.succ_p[so];
+    }
+    const bool ok = ty >= 0 && ty < n_types;         // successors without warm content: no plan
+    off[j] = t.svc_off[u];
+    len[j] = ok ? t.svc_len[u] : 0;
+    bc[j] = bucket_count;
+    p_s[j] = p;
+    t_p[j] = ok ? warmup[ty] : 0.0;
+    kn[j] = knob;
+    nw[j] = now[app];
+  }
+}
+}  // namespace pdg
+
+extern "C" size_t pdg_prewarm_triggers_temp_bytes(int64_t n) {
+  return size_t(4 * n) * (4 * 3 + 8 * 4) + 256;
+}
+
+extern "C" int pdg_prewarm_triggers(const pdg_prewarm_tables* t, const int32_t* graph,
+                                    const int32_t* unit, const double* now, int64_t n,
+                                    const double* warmup_by_type, int32_t n_types, double knob,
+                                    int32_t bucket_count, uint8_t* has_plan, double* trigger,
+                                    double* p_e, void* temp, size_t temp_bytes, void* stream) {
+  if (!t || n < 0 || n_types < 1 || bucket_count < 1 || !(knob >= 0.0 && knob <= 1.0) ||
+      (n > 0 && (!graph || !unit || !now || !warmup_by_type || !has_plan || !trigger || !p_e ||
+                 !temp))) {
+    set_error("pdg_prewarm_triggers: invalid arguments (knob in [0, 1], bucket_count >= 1)");
+    return PDG_EINVAL;
+  }
+  if (n == 0) return PDG_OK;
+  if (temp_bytes < pdg_prewarm_triggers_temp_bytes(n)) {
+    set_error("pdg_prewarm_triggers: temp_bytes %zu < %zu", temp_bytes,
+              pdg_prewarm_triggers_temp_bytes(n));
+    return PDG_EINVAL;
+  }
+  const int64_t J = 4 * n;
+  char* b = static_cast<char*>(temp);
+  double* p_s = reinterpret_cast<double*>(b);
+  double* t_p = p_s + J;
+  double* kn = t_p + J;
+  double* nw = kn + J;
+  int32_t* off = reinterpret_cast<int32_t*>(nw + J);
+  int32_t* len = off + J;
+  int32_t* bc = len + J;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t blocks = (J + 255) / 256;
+  const int64_t cap = int64_t(sm_count()) * 8;
+  if (blocks > cap) blocks = cap;
+  trigger_jobs_kernel<<<unsigned(blocks), 256, 0, st>>>(*t, graph, unit, now, n, warmup_by_type,
+                                                        n_types, knob, bucket_count, off, len,
+                                                        bc, p_s, t_p, kn, nw);
+  int rc = launch_status("trigger_jobs_kernel");
+  if (rc != PDG_OK) return rc;
+  PlanArgs a{t->svc_sorted, off, len, bc, p_s, t_p, kn, nw, J, has_plan, trigger, p_e,
+             nullptr, 0, nw};
+  int64_t pb = (J * 32 + 127) / 128;
+  const int64_t pcap = int64_t(sm_count()) * 16;
+  if (pb > pcap) pb = pcap;
+  prewarm_plan_kernel<<<unsigned(pb), 128, 0, st>>>(a);
+  return launch_status("prewarm_plan_kernel");
 }

@@ -231,6 +231,27 @@ class PrewarmTables:
             self._win = (windows.clone(), idx)
         return self._win[1]
 
+    def triggers(self, graph_idx, unit_idx, now, warmup_by_type, knob: float,
+                 bucket_count: int, stream=None):
+        """plan_prewarm for every (application, successor slot) of the queue
+        (config 5's latest-safe triggers): (has_plan bool[N,4], trigger
+        f64[N,4], p_e f64[N,4]) on the device."""
+        n = int(graph_idx.numel())
+        dev = self.device
+        has = torch.zeros((n, 4), dtype=torch.uint8, device=dev)
+        trig = torch.zeros((n, 4), dtype=torch.float64, device=dev)
+        pe = torch.zeros((n, 4), dtype=torch.float64, device=dev)
+        L = _lib.lib()
+        tb = int(L.pdg_prewarm_triggers_temp_bytes(n))
+        temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
+        w = torch.as_tensor(warmup_by_type, dtype=torch.float64, device=dev).contiguous()
+        _lib.check(L.pdg_prewarm_triggers(
+            C.byref(self.c), _lib.ptr(graph_idx), _lib.ptr(unit_idx), _lib.ptr(now), n,
+            _lib.ptr(w), int(w.numel()), float(knob), int(bucket_count), _lib.ptr(has),
+            _lib.ptr(trig), _lib.ptr(pe), _lib.ptr(temp), temp.numel(), _lib.stream_ptr(stream)),
+            "pdg_prewarm_triggers")
+        return has.bool(), trig, pe
+
     def need(self, graph_idx, unit_idx, now, windows, *, dense=True, aggregate=True,
              out=None, window_index=True, unit_records=True, stream=None):
         """need[N, T, K] float32 (dense) and/or agg[T, K] float64 over the queue.

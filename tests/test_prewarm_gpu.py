@@ -163,3 +163,47 @@ def test_need_full_size_properties():
                 for q in range(s_len[g_ * U + u_])]
         want = O.need_grid(svc[g_, u_], succ, nowv[a], win, T)
         np.testing.assert_allclose(got[i], want, rtol=1e-6, atol=1e-6)
+
+
+def test_triggers_vs_oracle(kb_graphs):
+    """Config 5's per-successor plans from the prewarm tables equal
+    plan_prewarm on the completion distribution _plan_prewarms builds."""
+    import torch
+    from paper_2506_14851_b200.graphs import graph_from_kb
+    from paper_2506_14851_b200.prewarm import PrewarmTables
+    names = ["plan-execute", "code-gen", "fact-verify", "fanout-reduce", "react-loop",
+             "depth8-100"]
+    graphs = {k: graph_from_kb(kb_graphs[k]) for k in names}
+    tb = PrewarmTables.from_graphs(graphs)
+    rng = np.random.default_rng(18)
+    jobs = [(gi, ui) for gi, k in enumerate(names) for ui in range(len(graphs[k].units))] * 10
+    nowv = rng.uniform(0, 50, len(jobs))
+    nowv[::4] = rng.uniform(1e6, 1e9, len(nowv[::4]))
+    T = tb.n_types
+    warm = rng.uniform(0.0, 30.0, T)
+    g = torch.tensor([j[0] for j in jobs], dtype=torch.int32, device="cuda")
+    u = torch.tensor([j[1] for j in jobs], dtype=torch.int32, device="cuda")
+    now = torch.tensor(nowv, dtype=torch.float64, device="cuda")
+    for knob, bc in ((0.3, 64), (0.05, 10)):
+        has, trig, pe = tb.triggers(g, u, now, warm, knob, bc)
+        has, trig, pe = has.cpu().numpy(), trig.cpu().numpy(), pe.cpu().numpy()
+        planned = 0
+        for i, (gi, ui) in enumerate(jobs):
+            gr = graphs[names[gi]]
+            unit = gr.units[sorted(gr.units)[ui]]
+            if unit.is_llm:
+                svc = [r.input_len / 1e4 + r.output_len / 50.0 for r in unit.records]
+            else:
+                svc = unit.duration_dist.samples
+            comp = [nowv[i] + s for s in svc]
+            for slot, (v, p) in enumerate(sorted(unit.successors.items())[:4]):
+                wc = gr.units[v].warm_content
+                ty = tb.type_ids.get(wc, -1) if wc is not None else -1
+                want = (O.plan_prewarm(comp, bc, p, warm[ty], knob, nowv[i])
+                        if ty >= 0 and svc else None)
+                assert bool(has[i, slot]) == (want is not None), (i, slot)
+                if want is not None:
+                    planned += 1
+                    assert trig[i, slot] == want[0] and pe[i, slot] == want[1], (i, slot)
+            assert not has[i, len(unit.successors):].any()
+        assert planned > 0
