@@ -6,9 +6,16 @@ Workload = BASELINE config 2: "100k queued apps, depth-8 PDGraphs, 256-bin
 demand histograms, full re-score on 1 B200".  Every app owns its own depth-8
 PDGraph (tools/synth.py: chain + 3-way branch + self-loop + back-edge loop,
 256 lognormal duration records per unit) and sits at a random unit with a
-random amount of service attained.  Under torchrun each rank re-scores its
-own 100k-app shard (weak scaling) and the packed (key, arrival position)
-pairs are all-gathered over NCCL for the global order (config 3's exchange).
+random amount of service attained.
+
+Multi-GPU: `--gpus N` without a launcher re-executes this script under
+`torch.distributed.run` (N ranks, one per GPU, NCCL); under torchrun the
+ranks come from the environment.  The headline then scales weakly: each rank
+re-scores its own 100k-app shard and the packed (key, arrival position)
+pairs are all-gathered over NCCL for the global order.  Every line also
+carries `config3`, the strong-scaling run of BASELINE config 3: a 1M-app
+queue split 1M/N per rank, step = engine + K1b + NCCL all-gather + the
+global 1M-key sort, max over ranks.
 
 One step = full re-score of the queue, the reference's policy runtime
 (monte_carlo_remaining_demand(n=512) +
@@ -23,6 +30,11 @@ Each step uses fresh per-app seeds (a genuine re-estimate, nothing cached).
 Timing: W warm-up steps, then K timed steps, each bracketed by CUDA events on
 the launching stream; L2 flushed (256 MiB write) between steps outside the
 events (the 1.6 GB graph bank exceeds L2 anyway); step time = max over ranks.
+
+The reference arm (`--impl reference`) re-scores a bounded sample of the SAME
+queue (same graphs, current units, seeds + step salt, attained service) with
+the CPU restatement of the reference on every host core; its `ms_per_step`
+is the measured wall time of that sample.
 """
 
 from __future__ import annotations
@@ -30,6 +42,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -48,9 +61,12 @@ N_SAMP = 512
 N_REC = 256
 VISIT_CAP = 64
 PENALTY = 2.0
+CONFIG3_APPS = 1_000_000
+SEED_WORLD, SEED_JOBS, SEED_AGES = 1000, 1001, 1002
+SALT_TIMED = 100            # timed step i uses per-app seed + SALT_TIMED + i
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -58,14 +74,69 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--apps", type=int, default=N_APPS)
     ap.add_argument("--bins", type=int, default=N_BINS)
-    ap.add_argument("--cpu-apps", type=int, default=3000,
-                    help="apps in the bounded CPU-baseline sample")
+    ap.add_argument("--cpu-apps", type=int, default=1500,
+                    help="apps in the bounded 1-core CPU-baseline sample")
+    ap.add_argument("--ref-apps", type=int, default=0,
+                    help="apps per reference-arm step (default 256 per host core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
-                    help="skip the config-4 stream and config-5 prewarm sections")
+                    help="skip the secondary sections (configs 1, 4, 5, K1c, K6, masks)")
     ap.add_argument("--ncu", action="store_true",
                     help="profiling run: skip CUPTI launch counting, e2e and CPU legs")
-    return ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo check of the launch + exchange plumbing (no kernels)")
+    return ap.parse_args(argv)
+
+
+def dist_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a launcher: run N ranks of this script under
+    torch.distributed.run (127.0.0.1 rendezvous); rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def init_nccl(local: int):
+    """One NCCL communicator over the node; NCCL's INIT log (comm, rank,
+    nranks) goes to stderr so the rank count can be verified from the run."""
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t = torch.ones(1, device=torch.device("cuda", local))
+    dist.all_reduce(t)                     # forces communicator creation now
+    return int(t.item())
+
+
+def bench_config(n, b, world):
+    """`config` of the headline line (identical in both arms)."""
+    return {"workload": "config2: full re-score = MC demand engine (n=512, bit-exact vs "
+                        "reference) + 256-bucket Gittins + global order",
+            "apps_per_gpu": n, "bins": b, "samples_per_app": N_SAMP,
+            "records_per_unit": N_REC, "units_per_graph": 8, "visit_cap": VISIT_CAP,
+            "queue": f"tools/synth.py make({n}, {N_REC}, seed={SEED_WORLD}+rank), "
+                     f"jobs(seed={SEED_JOBS}+rank), ages(seed={SEED_AGES}+rank)",
+            "parallelism": f"shard-by-app x{world}, NCCL all_gather of 8 B keys",
+            "l2": "flushed between steps (256 MiB write, outside the step events); "
+                  "1.6 GB graph bank > L2"}
 
 
 # ---------------------------------------------------------------------------
@@ -79,7 +150,9 @@ def reachable_units(u: int) -> int:
 
 def ages_for(rng, n, mean_rem, max_rem):
     """est_age (attained service at the estimate) and age now: served since the
-    estimate ~ U(0, 0.9) x E[remaining]; 1% forced exhausted."""
+    estimate ~ U(0, 0.9) x E[remaining]; 1% forced exhausted.
+    Element-wise in the inputs, so a sample of apps gets the same ages as in
+    the full queue."""
     est = rng.uniform(0.0, 200.0, n)
     age = est + rng.uniform(0.0, 0.9, n) * mean_rem
     ex = rng.random(n) < 0.01
@@ -87,76 +160,243 @@ def ages_for(rng, n, mean_rem, max_rem):
     return est, age
 
 
+def hist_mean_max(lo, width, k, counts, n_samp=N_SAMP):
+    """E[remaining] over the bucket midpoints lo + (j + 1/2) w and the top
+    edge lo + k w -- the first estimate's statistics the ages derive from."""
+    j = np.arange(counts.shape[-1], dtype=np.float64)
+    mids = lo[:, None] + (j[None, :] + 0.5) * width[:, None]
+    return (counts * mids).sum(1) / n_samp, lo + k * width
+
+
 # ---------------------------------------------------------------------------
-# CPU (oracle port) timing: cpu_baseline object and --impl reference
+# CPU (oracle port) legs: cpu_baseline objects and --impl reference.  Each
+# leg runs on persistent forked workers that own a fixed shard of the sample
+# (graphs built once per worker, outside the timed steps); a step sends one
+# message to every worker and the parent times send -> last reply.
 # ---------------------------------------------------------------------------
 
-def _cpu_worker(args):
-    """Full re-score of apps [lo, hi) of the synthetic shard on one core:
-    MC(n=512) + bucketize(256) + Gittins row + penalty (the reference policy
-    runtime, restated by the oracle)."""
-    lo_i, hi_i, n_apps, seed, bins = args
+_CPU: dict = {}          # leg state, set by the parent before the workers fork
+
+
+def _worker_loop(conn, init_fn, step_fn, shard):
+    try:
+        state = init_fn(shard)
+        conn.send(("ready", None))
+        while True:
+            msg = conn.recv()
+            if msg is None:
+                break
+            conn.send(("ok", step_fn(state, msg)))
+    except Exception as e:            # surfaced by the parent
+        conn.send(("error", repr(e)))
+
+
+class ShardWorkers:
+    """`procs` forked workers; worker i owns shard i of `items`.  procs == 1
+    runs in-process.  call(msg) -> list of per-shard results."""
+
+    def __init__(self, init_fn, step_fn, items, procs):
+        import multiprocessing as mp
+        edges = np.linspace(0, len(items), max(procs, 1) + 1).astype(int)
+        shards = [items[a:b] for a, b in zip(edges[:-1], edges[1:]) if b > a]
+        self.step_fn = step_fn
+        self.local = None
+        self.conns, self.procs = [], []
+        if procs <= 1:
+            self.local = init_fn(items)
+            return
+        ctx = mp.get_context("fork")
+        for sh in shards:
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_worker_loop, args=(b, init_fn, step_fn, sh), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        for c in self.conns:
+            tag, err = c.recv()
+            if tag != "ready":
+                raise RuntimeError(f"CPU worker failed: {err}")
+
+    @property
+    def n(self):
+        return 1 if self.local is not None else len(self.conns)
+
+    def call(self, msg):
+        if self.local is not None:
+            return [self.step_fn(self.local, msg)]
+        for c in self.conns:
+            c.send(msg)
+        out = []
+        for c in self.conns:
+            tag, val = c.recv()
+            if tag != "ok":
+                raise RuntimeError(f"CPU worker failed: {val}")
+            out.append(val)
+        return out
+
+    def timed(self, msg):
+        t0 = time.perf_counter()
+        out = self.call(msg)
+        return out, time.perf_counter() - t0
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.procs:
+            p.join(10)
+
+
+def _c2_init(apps):
+    """Worker state: oracle graphs of its apps (the same synth documents the
+    GPU bank is built from) and their first estimates (seed + 0), from which
+    the ages derive exactly as in run_ours."""
     from oracle import pdg_oracle as O
     from tools import synth
-    w = synth.make(n_apps, N_REC, seed=seed)
-    jb = synth.jobs(n_apps, seed=seed + 1)
-    rng = np.random.default_rng(seed + 2)
-    graphs = [O.graph_from_kb(synth.kb_doc(w, a)) for a in range(lo_i, hi_i)]
-    t0 = time.perf_counter()
-    keys = []
-    for g, a in zip(graphs, range(lo_i, hi_i)):
-        r = O.mc_remaining_demand(g, f"s{jb['unit'][a]}", [], N_SAMP, int(jb["seed"][a]),
-                                  VISIT_CAP)
-        b = O.bucketize(r.samples.tolist(), bins)
-        est = float(rng.uniform(0, 200))
-        age = est + float(rng.uniform(0, 0.9)) * float(r.samples.mean())
+    st = _CPU["c2"]
+    graphs = {int(a): O.graph_from_kb(synth.kb_doc(st["w"], int(a))) for a in apps}
+    first = []
+    for a in apps:
+        r = O.mc_remaining_demand(graphs[a], f"s{st['unit'][a]}", [], N_SAMP,
+                                  int(st["seed"][a]), VISIT_CAP)
+        b = O.bucketize(r.samples.tolist(), st["bins"])
+        m, mx = hist_mean_max(np.array([b.lo]), np.array([b.width]), np.array([b.k]),
+                              b.counts[None].astype(np.float64))
+        first.append((int(a), float(m[0]), float(mx[0])))
+    return {"apps": [int(a) for a in apps], "graphs": graphs, "first": first, "ages": {}}
+
+
+def _c2_step(state, msg):
+    """("first",) -> first-estimate stats; ("ages", {app: (est, age)});
+    ("step", salt) -> [(app, key)]: MC(n=512) + bucketize(256) + Gittins row
+    + overrun penalty on one core (sched.py:170-181, 244-318,
+    estimator.py:305-362)."""
+    from oracle import pdg_oracle as O
+    if msg[0] == "first":
+        return state["first"]
+    if msg[0] == "ages":
+        state["ages"].update({a: msg[1][a] for a in state["apps"]})
+        return None
+    st = _CPU["c2"]
+    salt = int(msg[1])
+    out = []
+    for a in state["apps"]:
+        est, age = state["ages"][a]
+        r = O.mc_remaining_demand(state["graphs"][a], f"s{st['unit'][a]}", [], N_SAMP,
+                                  int(st["seed"][a]) + salt, VISIT_CAP)
+        b = O.bucketize(r.samples.tolist(), st["bins"])
         v = b.midpoints() + est
         k = O.gittins_rank_batch(v[None], b.probs[None], np.array([age]))[0]
-        keys.append(age * PENALTY if np.isnan(k) else k)
-    np.lexsort((np.arange(len(keys)), np.asarray(keys)))
-    return time.perf_counter() - t0, hi_i - lo_i
+        out.append((a, age * PENALTY if np.isnan(k) else float(k)))
+    return out
 
 
-def cpu_rate(sample_apps, procs, n_apps, seed, bins):
-    if procs <= 1:
-        dt, m = _cpu_worker((0, sample_apps, max(n_apps, sample_apps), seed, bins))
-        return m / dt
-    import multiprocessing as mp
-    edges = np.linspace(0, sample_apps, procs + 1).astype(int)
-    tasks = [(int(a), int(b), max(n_apps, sample_apps), seed, bins)
-             for a, b in zip(edges[:-1], edges[1:]) if b > a]
-    with mp.get_context("fork").Pool(len(tasks)) as pool:
-        res = pool.map(_cpu_worker, tasks)
-    # the shards run concurrently: wall = slowest shard's compute time
-    return sum(m for _, m in res) / max(dt for dt, _ in res)
+class Config2CPU:
+    """The config-2 queue restated on the host for a bounded, evenly strided
+    sample of its apps: same graphs, units, seeds, ages as the GPU arm."""
+
+    def __init__(self, n_apps, sample, bins, procs, rank=0, world=None, jobs=None):
+        from tools import synth
+        w = world if world is not None else synth.make(n_apps, N_REC, seed=SEED_WORLD + rank)
+        jb = jobs if jobs is not None else synth.jobs(n_apps, seed=SEED_JOBS + rank)
+        self.idx = np.unique(np.linspace(0, n_apps - 1, sample).astype(np.int64))
+        _CPU["c2"] = {"w": w, "unit": jb["unit"], "seed": jb["seed"], "bins": bins}
+        self.workers = ShardWorkers(_c2_init, _c2_step, [int(a) for a in self.idx], procs)
+        mean_rem, max_rem = np.zeros(n_apps), np.zeros(n_apps)
+        for part in self.workers.call(("first",)):
+            for a, m, mx in part:
+                mean_rem[a], max_rem[a] = m, mx
+        est, age = ages_for(np.random.default_rng(SEED_AGES + rank), n_apps, mean_rem, max_rem)
+        self.est, self.age = est, age
+        self.workers.call(("ages", {int(a): (float(est[a]), float(age[a])) for a in self.idx}))
+
+    def step(self, salt):
+        """One re-score of the sample + its (key, arrival) order: wall
+        seconds, keys (in self.idx order), order."""
+        parts, dt = self.workers.timed(("step", salt))
+        t0 = time.perf_counter()
+        res = dict(x for part in parts for x in part)
+        keys = np.array([res[int(a)] for a in self.idx])
+        order = np.lexsort((self.idx, keys))
+        return dt + time.perf_counter() - t0, keys, order
+
+    def close(self):
+        self.workers.close()
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
+    world, rank, _ = dist_env()
     if rank != 0:
         return
     procs = os.cpu_count() or 1
-    sample = max(procs * 300, 600)           # ~0.5-1 s of work per step on the box
-    for _ in range(max(args.warmup, 1)):
-        cpu_rate(min(sample, procs * 4), procs, sample, 1000, args.bins)
-    rates = [cpu_rate(sample, procs, sample, 1000 + s, args.bins) for s in range(args.steps)]
-    val = float(np.median(rates))
-    ms = args.apps / val * 1e3
+    sample = args.ref_apps or max(256 * procs, 1024)
+    t_setup = time.perf_counter()
+    c2 = Config2CPU(args.apps, sample, args.bins, procs)
+    t_setup = time.perf_counter() - t_setup
+    for i in range(args.warmup):
+        c2.step(1 + i)
+    dts = [c2.step(SALT_TIMED + i)[0] for i in range(args.steps)]
+    c2.close()
+    m = len(c2.idx)
+    ms_per_step = float(np.sum(dts)) / args.steps * 1e3
+    val = m / (ms_per_step / 1e3)
+    n_gpus = max(args.gpus, world)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2: full re-score (MC n=512 + 256-bucket Gittins) of a "
-                               "100k-app queue of depth-8 PDGraphs",
-                   "apps": args.apps, "bins": args.bins, "samples_per_app": N_SAMP},
+        "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "p50_latency_ms": float(np.median(dts)) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded app-unique depth-8 PDGraphs, 256 records per unit)",
+        "config": bench_config(args.apps, args.bins, n_gpus),
+        "sample_apps": m,
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{sample} apps per step (bounded sample of the {args.apps}-app "
-                                   f"shard), oracle MC+bucketize+Gittins, {procs} processes; "
-                                   f"ms_per_step extrapolated to {args.apps} apps"},
+                         "sample": f"{m} of the {args.apps} apps of the queue the GPU arm "
+                                   f"scores (rank-0 shard; same graphs, units, seeds + step "
+                                   f"salt, ages), oracle MC(n=512)+bucketize({args.bins})+"
+                                   f"Gittins+penalty+order on {procs} processes; ms_per_step "
+                                   f"= measured wall time of the sample step",
+                         "setup_s": t_setup},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# --dry-run: the launch and exchange plumbing on CPU (gloo), no kernels
+# ---------------------------------------------------------------------------
+
+def run_dry(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2506_14851_b200.distributed import global_order, pack_keys, shard_range
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    n_total = args.apps * world
+    lo, hi = shard_range(n_total, world, rank)
+    keys = np.random.default_rng(7).lognormal(2, 1, n_total).astype(np.float32)
+    local = pack_keys(torch.from_numpy(keys[lo:hi]), torch.arange(lo, hi))
+    ms = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        order = global_order(local, n_total,
+                             sort_fn=lambda k: k[torch.sort(k >> 32, stable=True).indices])
+        if i >= args.warmup:
+            ms.append((time.perf_counter() - t0) * 1e3)
+    ranks = [None] * world
+    if world > 1:
+        dist.all_gather_object(ranks, rank)
+    else:
+        ranks = [0]
+    pos = (order & 0xFFFFFFFF).numpy()
+    ok = bool(np.array_equal(pos, np.lexsort((np.arange(n_total), keys.astype(np.float64)))))
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world,
+                          "ranks_seen": ranks, "order_ok": ok, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": float(np.mean(ms))}),
+              flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------
@@ -251,6 +491,15 @@ def count_launches(step):
     return len(ours), sorted(set(ours))
 
 
+def max_over_ranks(vals, world, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -264,20 +513,18 @@ def run_ours(args):
     from paper_2506_14851_b200.queue import HistQueue
     from tools import synth
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    if world > 1:
+        init_nccl(local)
     L = _lib.lib()
     n, b = args.apps, args.bins
 
     # ---- resident state: graph bank + queue + per-app job state ----------
-    w = synth.make(n, N_REC, seed=1000 + rank)
+    w = synth.make(n, N_REC, seed=SEED_WORLD + rank)
     eng = DemandEngine(synth.bank(w, device=str(dev)), device=str(dev))
-    jb = synth.jobs(n, seed=1001 + rank)
+    jb = synth.jobs(n, seed=SEED_JOBS + rank)
     q = HistQueue(n, b)
     g_idx = torch.arange(n, dtype=torch.int32, device=dev)
     u_idx = torch.from_numpy(jb["unit"]).to(dev)
@@ -286,12 +533,10 @@ def run_ours(args):
     # attained service: drawn once from the first estimate's mean / max
     eng.run(g_idx, u_idx, seeds, n=N_SAMP, bucket_count=b, visit_cap=VISIT_CAP, queue=q)
     torch.cuda.synchronize()
-    k = q.nbins[:n].double()
-    j = torch.arange(q.stride, device=dev, dtype=torch.float64)
-    mids = q.lo[:n, None] + (j[None, :] + 0.5) * q.width[:n, None]
-    mean_rem = ((q.counts[:n].double() * mids).sum(1) / N_SAMP).cpu().numpy()
-    max_rem = (q.lo[:n] + k * q.width[:n]).cpu().numpy()
-    est, age = ages_for(np.random.default_rng(1002 + rank), n, mean_rem, max_rem)
+    mean_rem, max_rem = hist_mean_max(q.lo[:n].cpu().numpy(), q.width[:n].cpu().numpy(),
+                                      q.nbins[:n].double().cpu().numpy(),
+                                      q.counts[:n].double().cpu().numpy())
+    est, age = ages_for(np.random.default_rng(SEED_AGES + rank), n, mean_rem, max_rem)
     q.est_age[:n] = torch.from_numpy(est).to(dev)
     q.age[:n] = torch.from_numpy(age).to(dev)
     q.tiebreak[:n] = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int32, device=dev)
@@ -349,11 +594,14 @@ def run_ours(args):
         step(7)
         torch.cuda.synchronize()
     step_ev = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     for i in range(args.steps):
         flush.zero_()
         e0, e1 = ev(), ev()
         e0.record(stream)
-        step(100 + i, record=True)
+        step(SALT_TIMED + i, record=True)
         e1.record(stream)
         step_ev.append((e0, e1))
     torch.cuda.synchronize()
@@ -367,16 +615,15 @@ def run_ours(args):
     step_ms = np.array([a.elapsed_time(b_) for a, b_ in step_ev])
     eng_ms = np.array([a.elapsed_time(b_) for a, b_ in k_ev["engine"]])
     k1_ms = np.array([a.elapsed_time(b_) for a, b_ in k_ev["k1"]])
-    tot = torch.tensor([step_ms.sum(), np.median(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms_per_step = float(tot[0].item()) / args.steps
-    p50 = float(tot[1].item())
+    tot_ms, p50 = max_over_ranks([step_ms.sum(), np.median(step_ms)], world, dev)
+    ms_per_step = tot_ms / args.steps
     value = world * n / (ms_per_step / 1e3)
 
     if args.ncu:
         if rank == 0:
             print(json.dumps({"ncu_run": True, "ms_per_step": ms_per_step}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
         return
 
     # ---- e2e through the public API with pinned HOST buffers --------------
@@ -412,16 +659,13 @@ def run_ours(args):
         e2e_step(300 + i)
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2t = torch.tensor([float(np.sum(e2e_ms)), float(np.median(e2e_ms))], dtype=torch.float64,
-                       device=dev)
-    if world > 1:
-        dist.all_reduce(e2t, op=dist.ReduceOp.MAX)
-    e2e_ms_step = float(e2t[0].item()) / args.steps
+    e2e_tot, e2e_p50 = max_over_ranks([np.sum(e2e_ms), np.median(e2e_ms)], world, dev)
+    e2e_ms_step = e2e_tot / args.steps
     h2d = h_unit.numel() * 4 + h_seed.numel() * 8 + h_age.numel() * 8 + h_est.numel() * 8
     e2e = {"value": world * n / (e2e_ms_step / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(h_order.numel() * 4 + h_keys.numel() * 4),
-           "ms_per_step": e2e_ms_step, "p50_latency_ms": float(e2t[1].item()),
+           "ms_per_step": e2e_ms_step, "p50_latency_ms": e2e_p50,
            "path": "pinned host queue state -> DemandEngine.run + HistQueue.score + "
                    "pdg_order -> pinned host order/keys (wall clock, synchronized)"}
 
@@ -447,6 +691,9 @@ def run_ours(args):
                         "capture (profiles/ncu_summary.json)",
                 "issue_active_frac": ns.get("issue_active_frac"),
                 "warp_instructions": ns.get("warp_instructions")}
+    if ns.get("pcg_floor_ms") is not None:
+        roofline["pcg_floor_ms"] = ns["pcg_floor_ms"]
+        roofline["frac_of_pcg_floor"] = ns["pcg_floor_ms"] / eng_avg
     k1_bytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
     k1 = {"kernel": "gittins_rows_kernel", "avg_launch_ms": float(k1_ms.mean()),
           "bytes_per_app": k1_bytes,
@@ -459,17 +706,33 @@ def run_ours(args):
         "p50_latency_ms": p50, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64 walks/f32 scan/u16 counts",
         "data": "synthetic (seeded app-unique depth-8 PDGraphs, 256 records per unit)",
-        "config": {"workload": "config2: full re-score = MC demand engine (n=512, bit-exact "
-                               "vs reference) + 256-bucket Gittins + global order",
-                   "apps_per_gpu": n, "bins": b, "samples_per_app": N_SAMP,
-                   "records_per_unit": N_REC, "units_per_graph": 8, "visit_cap": VISIT_CAP,
-                   "parallelism": f"shard-by-app x{world}, NCCL all_gather of 8 B keys",
-                   "l2": "flushed between steps (256 MiB write, outside the step events); "
-                         "1.6 GB graph bank > L2"},
+        "config": bench_config(n, b, world),
         "gpu_launches": None if launches is None else launches * args.steps,
         "gpu_launches_per_step": launches, "kernels": kernel_names,
         "e2e": e2e, "roofline": roofline, "k1_refresh": k1, "clocks": clk,
     }
+
+    # ---- like-for-like CPU baseline (rank 0, N = 1): the same apps --------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = Config2CPU(n, args.cpu_apps, b, 1, rank=0, world=w, jobs=jb)
+        cpu_dt, cpu_keys, _ = cpu.step(SALT_TIMED)
+        cpu.close()
+        step(SALT_TIMED)                                  # the GPU's keys of that step
+        gk = q.key_f32[:n].cpu().numpy()[cpu.idx].astype(np.float64)
+        rel = np.abs(gk - cpu_keys) / np.maximum(np.abs(cpu_keys), 1e-300)
+        line["cpu_baseline"] = {
+            "value": len(cpu.idx) / cpu_dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(cpu.idx)} of the {n} apps of this queue (evenly strided; same "
+                      f"graphs, units, seeds, ages, step salt {SALT_TIMED}), oracle "
+                      f"MC(n=512)+bucketize({b})+Gittins row+penalty, 1 process",
+            "sample_wall_s": cpu_dt,
+            "keys_max_rel_err_vs_gpu": float(rel.max())}
+    del w
+
+    # ---- config 3: 1M apps split 1M/N over the ranks (strong scaling) -----
+    line["config3"] = bench_config3(dev, eng, n, b, world, rank, flush)
+
     if world == 1 and not args.no_extra:
         line["k1c_policy"] = bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b)
         line["k6_dispatch"] = bench_dispatch(dev)
@@ -477,79 +740,114 @@ def run_ours(args):
         line["config1_refresh_latency"] = bench_refresh_latency()
         line["config1_simulation"] = bench_config1_sim()
         line["k1_refresh_1m"] = bench_k1_large(dev)
-        line["config3_1m"] = bench_config3(dev, eng, n, b)
-        del eng, q, w
+        del eng, q
         torch.cuda.empty_cache()
-        line["config4_stream"] = bench_stream(dev)
+        line["config4_stream"] = bench_stream(dev, cpu=not args.no_cpu_baseline)
         torch.cuda.empty_cache()
-        line["config5_prewarm"] = bench_need(dev)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate = cpu_rate(args.cpu_apps, 1, args.cpu_apps, 1000, b)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"{args.cpu_apps} of {n} apps (same synthetic generator),"
-                                          " oracle MC(n=512)+bucketize(256)+Gittins row, "
-                                          "1 process"}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+        line["config5_prewarm"] = bench_need(dev, cpu=not args.no_cpu_baseline)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
-# config 3 on one GPU: a 1M-app queue fully re-scored (engine + K1 + global
-# order), and the 125k-app shard one of 8 GPUs holds
+# config 3 (strong scaling): a 1M-app queue split 1M/N over the ranks; step =
+# engine + K1b on the shard, NCCL all-gather of the 8-byte packed keys, the
+# global 1M-key order on every rank.  Time = max over ranks.
 # ---------------------------------------------------------------------------
-def bench_config3(dev, eng, n_graphs, b, sizes=(1_000_000, 125_000), steps=5):
+
+def bench_config3(dev, eng, n_graphs, b, world, rank, flush, total=CONFIG3_APPS, steps=5):
     import torch
+    import torch.distributed as dist
 
     from paper_2506_14851_b200 import _lib
+    from paper_2506_14851_b200.distributed import SENTINEL, shard_range
     from paper_2506_14851_b200.queue import HistQueue
     from tools import synth
     L = _lib.lib()
-    out = {"graphs": n_graphs,
-           "note": "apps are seeded instances of the config-2 bank's depth-8 graphs "
-                   "(app i walks graph i mod graphs, own unit and seed); step = engine "
-                   "(n=512, bit-exact) + K1b + pdg_order over the whole queue; L2 flushed "
-                   "between steps; the 125k row is one GPU's shard of 1M on 8 GPUs "
-                   "(the 8 MB all-gather is not included)"}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for n in sizes:
-        jb = synth.jobs(n, seed=3003)
-        g = (torch.arange(n, dtype=torch.int64, device=dev) % n_graphs).to(torch.int32)
-        u = torch.from_numpy(jb["unit"]).to(dev)
-        sd = torch.from_numpy(jb["seed"]).to(dev)
-        q = HistQueue(n, b)
-        q.n = n
-        q.est_age[:n] = 0.0
-        q.age[:n] = 1.0
-        ok = torch.empty(n, dtype=torch.int64, device=dev)
-        sl = torch.arange(n, dtype=torch.int32, device=dev)
-        osl = torch.empty_like(sl)
-        tb = int(L.pdg_order_temp_bytes(n))
-        temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
+    lo, hi = shard_range(total, world, rank)
+    n = hi - lo
+    width = -(-total // world)
+    jb = synth.jobs(total, seed=3003)
+    g = (torch.arange(lo, hi, dtype=torch.int64, device=dev) % n_graphs).to(torch.int32)
+    u = torch.from_numpy(jb["unit"][lo:hi]).to(dev)
+    sd0 = torch.from_numpy(jb["seed"][lo:hi]).to(dev)
+    sd = sd0.clone()
+    q = HistQueue(width, b)
+    q.n = n
+    q.est_age.zero_()
+    q.age.fill_(1.0)
+    q.tiebreak[:n] = torch.arange(lo, hi, dtype=torch.int32, device=dev)
+    q.keys.fill_(SENTINEL)                 # pad of an uneven shard sorts last
+    gathered = torch.empty(world * width, dtype=torch.int64, device=dev)
+    ok = torch.empty_like(gathered)
+    sl = torch.arange(world * width, dtype=torch.int32, device=dev)
+    osl = torch.empty_like(sl)
+    tb = int(L.pdg_order_temp_bytes(world * width))
+    temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    parts = {"engine": [], "k1": [], "allgather": [], "sort": []}
 
-        def step():
-            eng.run(g, u, sd, n=N_SAMP, bucket_count=b, visit_cap=VISIT_CAP, queue=q)
-            q.score(PENALTY)
-            _lib.check(L.pdg_order(_lib.ptr(q.keys), _lib.ptr(ok), _lib.ptr(sl), _lib.ptr(osl),
-                                   n, 32, _lib.ptr(temp), temp.numel(), _lib.stream_ptr()),
-                       "pdg_order")
-        for _ in range(2):
-            step()
-        ms = []
-        for _ in range(steps):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            step()
-            e1.record()
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
-        t = float(np.median(ms))
-        out[f"apps{n}"] = {"ms_per_rescore": t, "apps_per_s": n / (t / 1e3)}
-        del q, ok, temp
-        torch.cuda.empty_cache()
+    def step(salt, record=False):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if record else None
+        torch.add(sd0, salt, out=sd)
+        if record:
+            evs[0].record(stream)
+        eng.run(g, u, sd, n=N_SAMP, bucket_count=b, visit_cap=VISIT_CAP, queue=q)
+        if record:
+            evs[1].record(stream)
+        q.score(PENALTY)
+        if record:
+            evs[2].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, q.keys[:width])
+            src = gathered
+        else:
+            src = q.keys[:width]
+        if record:
+            evs[3].record(stream)
+        _lib.check(L.pdg_order(_lib.ptr(src), _lib.ptr(ok), _lib.ptr(sl), _lib.ptr(osl),
+                               world * width, 32, _lib.ptr(temp), temp.numel(),
+                               _lib.stream_ptr(stream)), "pdg_order")
+        if record:
+            evs[4].record(stream)
+            for k, (a, c) in zip(parts, zip(evs[:-1], evs[1:])):
+                parts[k].append((a, c))
+
+    for i in range(2):
+        step(50 + i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = []
+    for i in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(60 + i, record=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    if world > 1:
+        dist.barrier()
+    split = {k: float(np.mean([a.elapsed_time(c) for a, c in v])) for k, v in parts.items()}
+    t_mean, t_p50 = max_over_ranks([np.mean(ms), np.median(ms)], world, dev)
+    # the order must hold every global arrival position once (every rank)
+    pos = (ok[:total] & 0xFFFFFFFF).to(torch.int32)
+    perm_ok = bool(torch.equal(torch.sort(pos).values,
+                               torch.arange(total, dtype=torch.int32, device=dev)))
+    out = {"workload": f"config3: {total} apps (instances of this rank's {n_graphs} depth-8 "
+                       f"graphs, own unit and seed) split {total}/{world} per rank; step = engine "
+                       f"(n=512, bit-exact) + K1b + NCCL all_gather of 8 B keys + global "
+                       f"{total}-key radix sort; L2 flushed between steps",
+           "scaling": "strong", "n_gpus": world, "apps_total": total, "apps_per_rank": n,
+           "ms_per_rescore": t_mean, "p50_ms": t_p50, "apps_per_s": total / (t_mean / 1e3),
+           "rank0_split_ms": split, "order_is_permutation": perm_ok,
+           "north_star_target_ms": 10.0}
+    del q, gathered, ok, temp
+    torch.cuda.empty_cache()
     return out
 
 
@@ -780,13 +1078,58 @@ def bench_dispatch(dev, n_tasks=1_000_000, slots=(64, 32, 32), reps=10, cpu_task
 
 STREAM_TEMPLATES = ["code-gen", "fact-verify", "verify-chain-bimodal", "bimodal",
                     "plan-execute", "react-loop", "fanout-reduce", "cond"]
+STREAM_ATTAINED = 5.0
 
 
-def bench_stream(dev, n_apps=1_000_000, n_events=100_000, batch=1000):
+def _c4_init(events):
+    from oracle import pdg_oracle as O
+    st = _CPU["c4"]
+    return {"ev": list(events), "ogs": {k: O.graph_from_kb(st["docs"][k]) for k in st["names"]}}
+
+
+def _c4_step(state, msg):
+    """The reference's per-event path, restated: _complete_unit -> _estimate
+    (monte_carlo_remaining_demand with the observation, simcore.py:562-587,
+    317-325) -> set_remaining(256) -> _refresh([app], force=True) (one
+    Gittins row + penalty, simcore.py:327-337)."""
+    from oracle import pdg_oracle as O
+    st = _CPU["c4"]
+    out = []
+    for e in state["ev"]:
+        a = st["app"][e]
+        nm = st["names"][st["graph"][a]]
+        og = state["ogs"][nm]
+        order_u = st["orders"][nm]
+        ob = st["obs"][e]
+        obs = [O.OObs(order_u[st["completed"][e]], float(ob[0]), float(ob[1]), int(ob[2]))]
+        r = O.mc_remaining_demand(og, order_u[st["next"][e]], obs, N_SAMP, int(st["seed"][e]),
+                                  VISIT_CAP)
+        bz = O.bucketize(r.samples.tolist(), N_BINS)
+        v = bz.midpoints() + STREAM_ATTAINED
+        k = O.gittins_rank_batch(v[None], bz.probs[None], np.array([STREAM_ATTAINED]))[0]
+        out.append((int(e), STREAM_ATTAINED * PENALTY if np.isnan(k) else float(k)))
+    return out
+
+
+def cpu_leg(init_fn, step_fn, items, procs, reps=1):
+    """Events (or jobs) per second of a CPU leg over `items` on `procs`
+    processes: best of `reps` timed passes after one warm pass."""
+    wk = ShardWorkers(init_fn, step_fn, items, procs)
+    try:
+        res = wk.call(("run",))
+        dts = [wk.timed(("run",))[1] for _ in range(reps)]
+    finally:
+        wk.close()
+    return len(items) / min(dts), min(dts), [x for part in res for x in part]
+
+
+def bench_stream(dev, n_apps=1_000_000, n_events=100_000, batch=1000, cpu=True):
     """Config 4: 1M-app queue of template PDGraphs (the reference's own
     archetypes, with correlation masks); 100k unit-completion events with
     observations, applied in micro-batches: K3+K2 re-estimate, K1 re-score of
-    the touched rows, K5 re-sort of the whole queue.  Device-timed."""
+    the touched rows, K5b merge into the global order.  Device-timed.  CPU
+    legs: the reference's per-event path on a bounded sample of the same
+    events, 1 core and all cores."""
     import gzip
     import torch
     from paper_2506_14851_b200.estimator import DemandEngine
@@ -815,7 +1158,7 @@ def bench_stream(dev, n_apps=1_000_000, n_events=100_000, batch=1000):
     h = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
          for k, v in (("app", ev["app"]), ("next", ev["next"]), ("comp", ev["completed"]),
                       ("obs", ev["obs"]), ("seed", ev["seed"]))}
-    h["att"] = torch.full((n_events,), 5.0, dtype=torch.float64).pin_memory()
+    h["att"] = torch.full((n_events,), STREAM_ATTAINED, dtype=torch.float64).pin_memory()
     d = {k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in h.items()}
     stream = torch.cuda.current_stream()
     nb = n_events // batch
@@ -831,6 +1174,7 @@ def bench_stream(dev, n_apps=1_000_000, n_events=100_000, batch=1000):
 
     run_batch(0)                                       # warm-up (re-applies batch 0)
     torch.cuda.synchronize()
+    launches, names = count_launches(lambda _: run_batch(1))
     marks = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
              for _ in range(nb)]
     t0 = torch.cuda.Event(enable_timing=True)
@@ -845,19 +1189,91 @@ def bench_stream(dev, n_apps=1_000_000, n_events=100_000, batch=1000):
     torch.cuda.synchronize()
     total_ms = t0.elapsed_time(t1)
     lat = np.array([a.elapsed_time(b) for a, b in marks])
-    return {"workload": f"config4: {n_apps} queued template apps ({len(STREAM_TEMPLATES)} "
-                        f"reference archetypes), {n_events} refinement events in batches of "
-                        f"{batch}; per batch K3+K2+a4 re-estimate, K1 re-score, K5 full re-sort",
-            "events_per_s": n_events / (total_ms / 1e3), "batch": batch,
-            "batch_latency_ms_p50": float(np.median(lat)),
-            "batch_latency_ms_p99": float(np.percentile(lat, 99)),
-            "note": "latency = batch upload issued -> global order visible (device events); "
-                    "at 100k events/s a 1000-event batch is 10 ms of arrivals"}
+    keys = hq.key_f32[:n_apps].cpu().numpy()
+    # algorithmic bytes per batch: event records in (app, next, completed,
+    # seed, obs[3], attained = 52 B), histogram rows out (2 B/bucket + 40 B),
+    # K1 over the touched rows (row in + 25 B out), and the K5b merge of the
+    # resident order (1M x (8 B key + 4 B slot) read and written) + mark bytes
+    row = 2 * hq.stride + 40
+    bpb = batch * (52 + row + row + 25) + n_apps * (2 * 12 + 1)
+    peak, _ = measured_peaks()
+    ms_b = float(np.mean(lat))
+    out = {"workload": f"config4: {n_apps} queued template apps ({len(STREAM_TEMPLATES)} "
+                       f"reference archetypes), {n_events} refinement events in batches of "
+                       f"{batch}; per batch K3+K2+a4 re-estimate, K1 re-score, K5b merge into "
+                       f"the global order",
+           "events_per_s": n_events / (total_ms / 1e3), "batch": batch,
+           "batch_latency_ms_p50": float(np.median(lat)),
+           "batch_latency_ms_p99": float(np.percentile(lat, 99)),
+           "launches_per_batch": launches, "kernels": names,
+           "roofline": {"bound": "hbm", "bytes_per_batch": bpb,
+                        "achieved": bpb / (ms_b / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": bpb / (ms_b / 1e3) / 1e9 / peak,
+                        "note": "launch-latency bound at 1000-event batches: the batch's "
+                                "algorithmic bytes are dominated by the K5b merge over the "
+                                "resident 1M-app order"},
+           "note": "latency = batch upload issued -> global order visible (device events); "
+                   "at 100k events/s a 1000-event batch is 10 ms of arrivals"}
+    if cpu:
+        _CPU["c4"] = {"docs": {k: docs[k] for k in STREAM_TEMPLATES}, "names": q["names"],
+                      "orders": q["orders"], "graph": q["graph"], "app": ev["app"],
+                      "next": ev["next"], "completed": ev["completed"], "obs": ev["obs"],
+                      "seed": ev["seed"]}
+        procs = os.cpu_count() or 1
+        r1, dt1, res1 = cpu_leg(_c4_init, _c4_step, list(range(300)), 1)
+        rn, dtn, _ = cpu_leg(_c4_init, _c4_step, list(range(min(150 * procs, n_events))), procs)
+        # the last batch holding each sampled event decides the app's key: the
+        # events are on distinct apps, so compare every sampled key
+        rel = max(abs(float(keys[ev["app"][e]]) - k) / max(abs(k), 1e-300) for e, k in res1)
+        out["cpu_baseline"] = {
+            "kind": "port", "unit": "events/s",
+            "value_1core": r1, "sample_1core": 300, "wall_s_1core": dt1,
+            "value_all_cores": rn, "cores": procs, "sample_all_cores": min(150 * procs, n_events),
+            "wall_s_all_cores": dtn,
+            "path": "per event: oracle MC(n=512) with the observation (K3 conditioning) + "
+                    "bucketize(256) + one Gittins row + penalty (simcore.py:562-587 -> "
+                    "_estimate 317-325 -> _refresh([app], force=True) 327-337)",
+            "keys_max_rel_err_vs_gpu": rel}
+    return out
 
 
-def bench_need(dev, n_apps=1_000_000, n_templates=1024, steps=10):
+def _c5_init(jobs):
+    return {"jobs": list(jobs)}
+
+
+def _c5_step(state, msg):
+    """plan_prewarm per (app, successor) (prewarm.py:42-96 via
+    _plan_prewarms, simcore.py:450-487) and the need grid per app."""
+    from oracle import pdg_oracle as O
+    st = _CPU["c5"]
+    U, S = st["U"], st["SLOT"]
+    out = []
+    for a in state["jobs"]:
+        g_, u_ = int(st["g"][a]), int(st["u"][a])
+        now = float(st["now"][a])
+        svc = st["svc"][g_ * U + u_]
+        comp = [now + s for s in svc]
+        base = (g_ * U + u_) * S
+        plans, succ = [], []
+        for slot in range(int(st["s_len"][g_ * U + u_])):
+            ty = int(st["utype"][g_ * U + int(st["s_nxt"][base + slot])])
+            p = float(st["s_p"][base + slot])
+            succ.append((p, ty))
+            plans.append(O.plan_prewarm(comp, N_BINS, p, float(st["warm"][ty]), st["knob"], now)
+                         if ty >= 0 else None)
+        if msg[0] == "need":
+            out.append((a, O.need_grid(svc, succ, now, st["win"], st["T"])))
+        else:
+            out.append((a, plans))
+    return out
+
+
+def bench_need(dev, n_apps=1_000_000, n_templates=1024, steps=10, cpu=True):
     """Config 5: need probability for 16 backend types x 32 windows over 1M
-    apps (templates: depth-8 synth graphs, unit types random in [0,16))."""
+    apps (templates: depth-8 synth graphs, unit types random in [0,16)), and
+    the latest-safe trigger per (app, successor).  CPU legs: plan_prewarm per
+    (app, successor) and the need grid per app on bounded samples of the same
+    jobs, 1 core and all cores."""
     import torch
     from paper_2506_14851_b200.prewarm import PrewarmTables
     from tools import synth
@@ -867,7 +1283,7 @@ def bench_need(dev, n_apps=1_000_000, n_templates=1024, steps=10):
     svc = np.sort(w["dur"], axis=2).reshape(-1)
     counts = np.zeros((A, U, U))
     for v in range(U):
-        counts[:, :, v] = (w["nxt"] == v).sum(axis=2)
+        counts[:, :, v] = np.count_nonzero(w["nxt"] == v, axis=2)
     s_off = np.arange(A * U) * synth.SLOT
     s_len = w["succ_len"].reshape(-1)
     s_nxt = w["succ_nxt"].reshape(-1)
@@ -876,14 +1292,19 @@ def bench_need(dev, n_apps=1_000_000, n_templates=1024, steps=10):
         a, u = divmod(a_u, U)
         for q in range(s_len[a_u]):
             s_p[a_u * synth.SLOT + q] = counts[a, u, s_nxt[a_u * synth.SLOT + q]] / R
+    utype = rng.integers(0, 16, A * U)
     tb = PrewarmTables(svc_sorted=svc, svc_off=np.arange(A * U) * R, svc_len=np.full(A * U, R),
                        graph_base=np.arange(A) * U, succ_off=s_off, succ_len=s_len,
-                       succ_nxt=s_nxt, succ_p=s_p, unit_type=rng.integers(0, 16, A * U),
-                       n_types=16, device=str(dev))
-    g = torch.from_numpy(rng.integers(0, A, n_apps).astype(np.int32)).to(dev)
-    u = torch.from_numpy(rng.integers(0, U, n_apps).astype(np.int32)).to(dev)
-    now = torch.from_numpy(rng.uniform(0, 100, n_apps)).to(dev)
-    win = torch.linspace(2.0, 64.0, 32, dtype=torch.float64, device=dev)
+                       succ_nxt=s_nxt, succ_p=s_p, unit_type=utype, n_types=16,
+                       device=str(dev))
+    gv = rng.integers(0, A, n_apps).astype(np.int32)
+    uv = rng.integers(0, U, n_apps).astype(np.int32)
+    nowv = rng.uniform(0, 100, n_apps)
+    g = torch.from_numpy(gv).to(dev)
+    u = torch.from_numpy(uv).to(dev)
+    now = torch.from_numpy(nowv).to(dev)
+    winv = np.linspace(2.0, 64.0, 32)
+    win = torch.from_numpy(winv).to(dev)
     need = torch.empty((n_apps, 16, 32), dtype=torch.float32, device=dev)
     for _ in range(3):
         tb.need(g, u, now, win, out=need)
@@ -897,34 +1318,79 @@ def bench_need(dev, n_apps=1_000_000, n_templates=1024, steps=10):
     torch.cuda.synchronize()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     # the per-successor latest-safe triggers (plan_prewarm per (app, successor))
-    warm = torch.from_numpy(rng.uniform(1.0, 30.0, 16)).to(dev)
-    tb.triggers(g, u, now, warm, 0.3, N_BINS)
+    knob = 0.3
+    warmv = rng.uniform(1.0, 30.0, 16)
+    warm = torch.from_numpy(warmv).to(dev)
+    tb.triggers(g, u, now, warm, knob, N_BINS)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    has, _, _ = tb.triggers(g, u, now, warm, 0.3, N_BINS)
+    has, trig, pe = tb.triggers(g, u, now, warm, knob, N_BINS)
     e1.record()
     torch.cuda.synchronize()
-    trig = {"ms": e0.elapsed_time(e1), "plans": int(has.sum().item()),
-            "note": "plan_prewarm (bit-exact) for every (app, successor slot), knob 0.3, "
-                    "256 buckets, warm-up per backend type U(1, 30) s"}
+    trig_ms = e0.elapsed_time(e1)
+    jobs = int((s_len.reshape(A, U)[gv, uv]).sum())
+    trig_out = {"ms": trig_ms, "plans": int(has.sum().item()), "app_successor_jobs": jobs,
+                "jobs_per_s": jobs / (trig_ms / 1e3),
+                "note": f"plan_prewarm (bit-exact) for every (app, successor), knob {knob}, "
+                        f"{N_BINS} buckets, warm-up per backend type U(1, 30) s"}
     # algorithmic bytes per app: dense need row out + job (graph, unit, now)
-    # + the binary-searched service samples (<= 32 lanes x log2(256) probes)
     bytes_app = 16 * 32 * 4 + 4 + 4 + 8
     peak, _ = measured_peaks()
-    return {"workload": f"config5: need[{n_apps},16,32] float32 + [16,32] aggregate over "
-                        f"{n_apps} apps ({n_templates} depth-8 templates)",
-            "apps_per_s": n_apps / (ms / 1e3), "ms_per_launch": ms, "triggers": trig,
-            "roofline": {"bound": "hbm", "bytes_per_app": bytes_app,
-                         "achieved": bytes_app * n_apps / (ms / 1e3) / 1e9, "peak": peak,
-                         "unit": "GB/s",
-                         "frac": bytes_app * n_apps / (ms / 1e3) / 1e9 / peak}}
+    out = {"workload": f"config5: need[{n_apps},16,32] float32 + [16,32] aggregate over "
+                       f"{n_apps} apps ({n_templates} depth-8 templates)",
+           "apps_per_s": n_apps / (ms / 1e3), "ms_per_launch": ms, "triggers": trig_out,
+           "roofline": {"bound": "hbm", "bytes_per_app": bytes_app,
+                        "achieved": bytes_app * n_apps / (ms / 1e3) / 1e9, "peak": peak,
+                        "unit": "GB/s",
+                        "frac": bytes_app * n_apps / (ms / 1e3) / 1e9 / peak}}
+    if cpu:
+        _CPU["c5"] = {"U": U, "SLOT": synth.SLOT, "g": gv, "u": uv, "now": nowv,
+                      "svc": svc.reshape(A * U, R), "s_len": s_len, "s_nxt": s_nxt, "s_p": s_p,
+                      "utype": utype, "warm": warmv, "knob": knob, "win": winv, "T": 16}
+        procs = os.cpu_count() or 1
+        sample = np.random.default_rng(79).choice(n_apps, 400, replace=False).tolist()
+        wide = np.random.default_rng(80).choice(n_apps, 100 * procs, replace=False).tolist()
+        jobs_of = lambda apps: int(s_len.reshape(A, U)[gv[apps], uv[apps]].sum())  # noqa
+        t1, dt1, res = cpu_leg(_c5_init, lambda s, m: _c5_step(s, ("plan",)), sample, 1)
+        tn, dtn, _ = cpu_leg(_c5_init, lambda s, m: _c5_step(s, ("plan",)), wide, procs)
+        n1, ndt1, nres = cpu_leg(_c5_init, lambda s, m: _c5_step(s, ("need",)), sample, 1)
+        # cross-check the sample against the device results
+        hs, tr, pv = has.cpu().numpy(), trig.cpu().numpy(), pe.cpu().numpy()
+        mism = 0
+        for a, plans in res:
+            for slot, p in enumerate(plans):
+                want = p is not None
+                if bool(hs[a, slot]) != want or (want and (tr[a, slot] != p[0]
+                                                          or pv[a, slot] != p[1])):
+                    mism += 1
+        nd = need[torch.tensor([a for a, _ in nres], device=dev)].cpu().numpy()
+        nerr = float(max(np.max(np.abs(nd[i] - x)) for i, (_, x) in enumerate(nres)))
+        js1, jsn = jobs_of(np.array(sample)), jobs_of(np.array(wide))
+        out["cpu_baseline"] = {
+            "kind": "port", "cores": procs,
+            "plan_prewarm_jobs_per_s_1core": js1 / dt1,
+            "plan_prewarm_jobs_per_s_all_cores": jsn / dtn,
+            "need_apps_per_s_1core": len(sample) / ndt1,
+            "sample": f"plan_prewarm: {len(sample)} apps ({js1} app x successor jobs) on 1 "
+                      f"core, {len(wide)} apps ({jsn} jobs) on {procs}; need grid: "
+                      f"{len(sample)} apps on 1 core; same jobs as the device run",
+            "triggers_mismatches_vs_gpu": mism, "need_max_abs_err_vs_gpu": nerr}
+        del t1, tn, n1
+    return out
 
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    world, _, _ = dist_env()
+    if args.dry_run:
+        if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+            sys.exit(spawn_ranks(args))
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     else:
         run_ours(args)
 

@@ -15,6 +15,8 @@ reference's for the same inputs.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -63,7 +65,10 @@ def _jump_tensor(device) -> torch.Tensor:
 
 @dataclass
 class RemainingDemand:
-    """Mirror of the reference result type (estimator.py:40-59)."""
+    """Mirror of the reference result type (estimator.py:40-59), used when the
+    reference package is not loaded; ``integration.patch_pdgsim`` switches
+    the drop-in to the reference's own class (``RESULT_TYPE``), so helpers
+    that dispatch on it (sched._samples_of, sched.py:45-48) behave unchanged."""
     samples: list
     sample_count: int
     conditioned: bool = False
@@ -73,12 +78,23 @@ class RemainingDemand:
     def __post_init__(self):
         if self.sample_count != len(self.samples) or self.sample_count <= 0:
             raise EstimationError("sample_count must equal len(samples) and be > 0")
+        if any(s < 0 for s in self.samples):
+            raise EstimationError("remaining-demand samples must be >= 0")
+
+    def __iter__(self):
+        return iter(self.samples)
+
+    def __len__(self) -> int:
+        return self.sample_count
 
     def mean(self) -> float:
         return sum(self.samples) / self.sample_count
 
     def max(self) -> float:
         return max(self.samples)
+
+
+RESULT_TYPE = RemainingDemand       # rebound to pdgsim.estimator.RemainingDemand by patch_pdgsim
 
 
 class DemandEngine:
@@ -243,22 +259,86 @@ class DemandEngine:
 # drop-in single-application API (estimator.py:305-362)
 # ---------------------------------------------------------------------------
 
-_ENGINES: dict = {}
+# One engine per live graph object.  The cache holds the graph weakly (an
+# entry dies with its graph, so a recycled id() can never alias it) and is
+# bounded (least recently used first out).  Each hit re-checks a fingerprint
+# of everything the device tables are compiled from, so in-place mutation is
+# seen: a FIFO-capped record append (pdgraph.py:162-169 -- the deque length
+# stays at capacity but its first and last record objects change), a
+# build_masks pass (estimator.py:108-142 -- mask flags set in place), or a
+# direct append to a unit's sample distribution.
+_ENGINES: "OrderedDict[int, tuple]" = OrderedDict()
+MAX_ENGINES = 64
+
+
+def _tail_id(seq) -> tuple:
+    n = len(seq)
+    return (n, id(seq[0]), id(seq[-1])) if n else (0, 0, 0)
+
+
+def _dist_fp(d) -> tuple:
+    raw = getattr(d, "_samples", None)
+    if raw is None:
+        raw = getattr(d, "samples", ())
+    n = len(raw)
+    return (n, raw[0], raw[-1]) if n else (0,)
+
+
+def _mask_fp(m) -> tuple:
+    if m is None:
+        return ()
+    if isinstance(m, dict):
+        return tuple(sorted((k, bool(v)) for k, v in m.items()))
+    return tuple(sorted((k, bool(v)) for k, v in vars(m).items()))
 
 
 def _fingerprint(graph) -> tuple:
-    return tuple((uid, len(u.records)) for uid, u in sorted(graph.units.items()))
+    """Cheap content fingerprint: per unit the record container and its
+    first/last record identities (a record object in the deque stays alive,
+    so a new last record always has a new identity), the last record's
+    fields, the per-variable sample lists' length and end values, mask
+    flags, successor probabilities, bucket count and capacity."""
+    out = []
+    for uid, u in sorted(graph.units.items()):
+        recs = u.records
+        last = recs[-1] if len(recs) else None
+        out.append((uid, id(recs), _tail_id(recs),
+                    None if last is None else (last.trial_id, last.input_len, last.output_len,
+                                               last.parallelism, last.duration,
+                                               last.next_unit),
+                    _dist_fp(u.input_dist), _dist_fp(u.output_dist),
+                    _dist_fp(u.parallelism_dist), _dist_fp(u.duration_dist),
+                    _mask_fp(getattr(u, "masks", None)),
+                    tuple(sorted(u.successors.items())),
+                    getattr(u, "bucket_count", None), getattr(u, "capacity", None),
+                    bool(u.is_llm)))
+    return (getattr(graph, "entry_unit", None), tuple(out))
+
+
+def _forget(key, ref):
+    hit = _ENGINES.get(key)
+    if hit is not None and hit[0] is ref:
+        del _ENGINES[key]
 
 
 def engine_for(graph, env) -> tuple[DemandEngine, str]:
-    key = (id(graph), float(env.prefill_rate), float(env.decode_rate))
+    rates = (float(env.prefill_rate), float(env.decode_rate))
     fp = _fingerprint(graph)
+    key = id(graph)
     hit = _ENGINES.get(key)
-    if hit is None or hit[1] != fp:
-        eng = DemandEngine({"g": graph}, env.prefill_rate, env.decode_rate)
-        _ENGINES[key] = (eng, fp, graph)
-        hit = _ENGINES[key]
-    return hit[0], "g"
+    if hit is not None and hit[0]() is graph and hit[1] == rates:
+        eng = hit[3]
+        if hit[2] != fp:                    # mutated in place: recompile its tables
+            eng.refresh("g", graph)
+            _ENGINES[key] = (hit[0], rates, fp, eng)
+        _ENGINES.move_to_end(key)
+        return eng, "g"
+    eng = DemandEngine({"g": graph}, *rates)
+    ref = weakref.ref(graph, lambda r, k=key: _forget(k, r))
+    _ENGINES[key] = (ref, rates, fp, eng)
+    while len(_ENGINES) > MAX_ENGINES:
+        _ENGINES.popitem(last=False)
+    return eng, "g"
 
 
 def monte_carlo_remaining_demand(graph, current_unit: str, observations: Sequence, env,
@@ -277,5 +357,5 @@ def monte_carlo_remaining_demand(graph, current_unit: str, observations: Sequenc
         import logging
         logging.getLogger(__name__).warning(
             "%d of %d walks hit the %d-visit cap", capped, n, visit_cap)
-    return RemainingDemand(samples=s.tolist(), sample_count=n, conditioned=bool(flags & 1),
-                           capped_walks=capped)
+    return RESULT_TYPE(samples=s.tolist(), sample_count=n, conditioned=bool(flags & 1),
+                       capped_walks=capped)

@@ -11,7 +11,8 @@ rebinds exactly those names (the same seam SURVEY.md 8(b) lists):
     pdgsim.simcore.plan_prewarm                -> K4a
     pdgsim.sched.ApplicationInstance.set_remaining -> a4 (GPU bucketing)
 
-and ``restore`` undoes it.
+and makes the drop-in return ``pdgsim.estimator.RemainingDemand`` objects;
+``restore`` undoes it.
 """
 
 from __future__ import annotations
@@ -34,6 +35,8 @@ def patch_pdgsim(pdgsim) -> None:
         (simcore, "plan_prewarm"): simcore.plan_prewarm,
         (sched.ApplicationInstance, "set_remaining"): sched.ApplicationInstance.set_remaining,
     })
+    _SAVED[(_est, "RESULT_TYPE")] = _est.RESULT_TYPE
+    _est.RESULT_TYPE = pdgsim.estimator.RemainingDemand     # the reference's own result type
     sched.gittins_rank_batch = _sched.gittins_rank_batch
     simcore.refresh_priorities = _sched.refresh_priorities
     simcore.monte_carlo_remaining_demand = _est.monte_carlo_remaining_demand

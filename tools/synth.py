@@ -34,7 +34,7 @@ def make(n_apps: int, n_rec: int = 256, seed: int = 2026):
     p_back = rng.uniform(0.2, 0.5, n_apps)
     split = rng.dirichlet([1.0, 1.0, 1.0], n_apps)
     # recorded next unit per (app, unit, record); -1 = end
-    nxt = np.full((n_apps, U, n_rec), -1, dtype=np.int64)
+    nxt = np.full((n_apps, U, n_rec), -1, dtype=np.int8)
     nxt[:, 0] = 1
     r = rng.random((n_apps, n_rec))
     c = np.cumsum(split, axis=1)
@@ -44,11 +44,18 @@ def make(n_apps: int, n_rec: int = 256, seed: int = 2026):
     nxt[:, 4] = 5
     nxt[:, 5] = np.where(rng.random((n_apps, n_rec)) < p_back[:, None], 3, 6)
     nxt[:, 6] = 7
+    # every branch keeps at least one record, so every unit stays reachable
+    # from s0 and the graph passes the reference's PDGraph.validate
+    # (pdgraph.py:208-225; a Dirichlet split can otherwise draw no record)
+    if n_rec >= 3:
+        nxt[:, 1, :3] = np.array([2, 3, 4], dtype=np.int8)
+        nxt[:, 2, :2] = np.array([2, 3], dtype=np.int8)
+        nxt[:, 5, :2] = np.array([3, 6], dtype=np.int8)
     # successor tables: sorted by unit id == ascending index; probability =
     # count / n_rec; units never recorded as next are absent
     counts = np.zeros((n_apps, U, U), dtype=np.int64)
     for v in range(U):
-        counts[:, :, v] = (nxt == v).sum(axis=2)
+        counts[:, :, v] = np.count_nonzero(nxt == v, axis=2)
     succ_cum = np.zeros((n_apps, U, SLOT))
     succ_nxt = np.full((n_apps, U, SLOT), -1, dtype=np.int32)
     succ_len = np.zeros((n_apps, U), dtype=np.int32)
