@@ -47,8 +47,8 @@ def _same(g, unit, obs, seed):
 
 
 def test_dropin_sees_record_trial_at_capacity():
-    from pdgsim.pdgraph import UnitRecord, record_trial
     g, trials = _setup()
+    from pdgsim.pdgraph import UnitRecord, record_trial
     for k, uid in enumerate(sorted(g.units)):
         _same(g, uid, [], 100 + k)                      # engine compiled and cached
     for i, tr in enumerate(trials[:12]):
@@ -62,8 +62,8 @@ def test_dropin_sees_record_trial_at_capacity():
 
 
 def test_dropin_sees_build_masks_and_in_place_flags():
-    from pdgsim.estimator import Observation, build_masks
     g, _ = _setup()
+    from pdgsim.estimator import Observation, build_masks
     ex = g.units["extract"].records[7]
     obs = [Observation("extract", ex.input_len, ex.output_len, 1)]
     base = _same(g, "verify", obs, 7)
@@ -81,13 +81,13 @@ def test_dropin_sees_build_masks_and_in_place_flags():
 
 
 def test_dropin_returns_reference_type_when_patched():
+    g, _ = _setup()
     import pdgsim
     from pdgsim.estimator import RemainingDemand
     from pdgsim.pdgraph import RateProfile
     from pdgsim.sched import gittins_rank
     from paper_2506_14851_b200 import integration
     from paper_2506_14851_b200.estimator import monte_carlo_remaining_demand as ours
-    g, _ = _setup()
     integration.patch_pdgsim(pdgsim)
     try:
         r = ours(g, "extract", [], RateProfile(), 256, 5)
