@@ -57,6 +57,22 @@ int pdg_gittins_rank_f64_host(const double* values, const double* probs,
                               const double* ages, int64_t n_rows, int32_t n_bins,
                               double* out_rank, void* stream);
 
+/* Sample form: pdgsim.sched.gittins_rank (sched.py:51-85), bit-identical.
+ * Row r's samples are samples[off[r] .. off[r] + len[r]) (len <= 16384); the
+ * tail {s - age : s > age} is sorted and scanned exactly as the reference
+ * scans it (sequential float64 prefix over groups of equal values).
+ * out_rank NaN: no sample exceeds the age (the reference raises
+ * ExhaustedDistributionError); len 0 rows give NaN too (EstimationError).
+ * Device pointers; max_len >= every len[r]. */
+#define PDG_SAMPLES_MAX 16384
+int pdg_gittins_rank_samples(const double* samples, const int64_t* off, const int32_t* len,
+                             const double* ages, int64_t n_rows, int32_t max_len,
+                             double* out_rank, void* stream);
+/* One distribution from HOST memory (the drop-in gittins_rank): staged in
+ * mapped pinned memory, one launch, one sync. */
+int pdg_gittins_rank_samples_host(const double* samples, int32_t n, double age,
+                                  double* out_rank, void* stream);
+
 /* ---------------------------------------------------------------------------
  * K1b  Gittins rank over the device-resident histogram queue (the
  * bucket_points view cached by ApplicationInstance.set_remaining,
@@ -269,6 +285,19 @@ int pdg_dispatch_plan(const int32_t* backend, const uint8_t* active, const doubl
 int pdg_dispatch_status(const void* temp, int64_t n, int32_t n_backends, int32_t* status_out,
                         void* stream);
 
+/* a11b: Simulator._update_attained (simcore.py:306-313) for every application
+ * of a queue: age_out[a] = completed[a] + max(progress[a], max over tasks t
+ * with task_app[t] == a, task_active[t] != 0 and task_start[t] not NaN (the
+ * backends' active tasks that have started) of min(task_service[t],
+ * max(0, now - (task_start[t] + task_cold[t])))).  Bit-identical to the
+ * reference loop (the max is order-free).  age_out may alias progress or
+ * completed.  temp: 8 * n_apps bytes. */
+int pdg_attained_service(const double* completed, const double* progress, int64_t n_apps,
+                         const int32_t* task_app, const uint8_t* task_active,
+                         const double* task_start, const double* task_cold,
+                         const double* task_service, int64_t n_tasks, double now,
+                         double* age_out, void* temp, size_t temp_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * K4a  batched plan_prewarm (prewarm.py:42-96), bit-exact: one job per
  * (application, successor).  Job j's completion samples (absolute times, the
@@ -321,16 +350,23 @@ int pdg_prewarm_need(const pdg_prewarm_tables* tables, const int32_t* graph,
                      float* need, double* agg, void* stream);
 
 /* Config 5's per-successor plans: plan_prewarm (prewarm.py:42-96) for every
- * (application, successor slot < 4) of a queue, with the completion
- * distribution _plan_prewarms builds (simcore.py:450-478: now + the current
- * unit's service samples, bucket_count buckets), p_s the branch probability
- * and t_p = warmup_by_type[type of the successor].  Outputs [n, 4]; slots
- * without a successor or whose successor has no warm content (type < 0) get
- * has_plan = 0.  Bit-identical to plan_prewarm.  temp:
- * pdg_prewarm_triggers_temp_bytes(n) bytes. */
-size_t pdg_prewarm_triggers_temp_bytes(int64_t n);
+ * (application, successor slot) of a queue, with the completion distribution
+ * _plan_prewarms builds (simcore.py:450-478: now + the current unit's service
+ * samples, bucket_count buckets), p_s the branch probability and t_p =
+ * warmup_by_type[type of the successor].  Outputs [n, slots], successors in
+ * sorted order as _plan_prewarms iterates them.  has_plan[a, s]:
+ *   0  no plan: no successor in slot s, its successor has no warm content
+ *      (type < 0), or plan_prewarm returned None;
+ *   1  plan (trigger, p_e), bit-identical to plan_prewarm;
+ *   PDG_PLAN_OVERFLOW  (every slot of the application) its unit has more
+ *      than `slots` successors -- pass slots >= the bank's largest fan-out;
+ *   PDG_PLAN_BAD_TYPE  the successor's type is >= n_types (no warmup entry).
+ * temp: pdg_prewarm_triggers_temp_bytes(n, slots) bytes. */
+#define PDG_PLAN_OVERFLOW 2
+#define PDG_PLAN_BAD_TYPE 3
+size_t pdg_prewarm_triggers_temp_bytes(int64_t n, int32_t slots);
 int pdg_prewarm_triggers(const pdg_prewarm_tables* tables, const int32_t* graph,
-                         const int32_t* unit, const double* now, int64_t n,
+                         const int32_t* unit, const double* now, int64_t n, int32_t slots,
                          const double* warmup_by_type, int32_t n_types, double knob,
                          int32_t bucket_count, uint8_t* has_plan, double* trigger, double* p_e,
                          void* temp, size_t temp_bytes, void* stream);

@@ -677,3 +677,21 @@ def need_grid(svc_samples: Sequence[float], successors: Sequence[tuple], now: fl
             if t is not None and t >= 0:
                 out[t, k] += p_s * pneed
     return out
+
+
+# ---------------------------------------------------------------------------
+# a11b: Simulator._update_attained (simcore.py:306-313)
+# ---------------------------------------------------------------------------
+
+def update_attained(completed: Sequence[float], progress: Sequence[float],
+                    tasks: Sequence[tuple], now: float) -> list:
+    """attained[a] = completed[a] + max(progress[a], min(service, max(0, now -
+    (start + cold)))) over the active tasks (app, start, cold, service) of
+    app a with start not None, in the reference's operation order."""
+    prog = list(progress)
+    for a, start, cold, service in tasks:
+        if start is None:
+            continue
+        run = max(0.0, now - (start + cold))
+        prog[a] = max(prog[a], min(service, run))
+    return [c + p for c, p in zip(completed, prog)]

@@ -56,9 +56,13 @@ _SIG = {
     "pdg_dispatch_status": (C.c_int, [_P, _I64, _I32, _P, _P]),
     "pdg_order_update_temp_bytes": (C.c_size_t, [_I64, _I64]),
     "pdg_order_update": (C.c_int, [_P, _P, _P, _I64, _P, _I64, _P, _P, _P, _P, C.c_size_t, _P]),
-    "pdg_prewarm_triggers_temp_bytes": (C.c_size_t, [_I64]),
-    "pdg_prewarm_triggers": (C.c_int, [_P, _P, _P, _P, _I64, _P, _I32, C.c_double, _I32, _P, _P,
+    "pdg_gittins_rank_samples": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _P]),
+    "pdg_gittins_rank_samples_host": (C.c_int, [_P, _I32, C.c_double, _P, _P]),
+    "pdg_attained_service": (C.c_int, [_P, _P, _I64, _P, _P, _P, _P, _P, _I64, C.c_double,
                                        _P, _P, C.c_size_t, _P]),
+    "pdg_prewarm_triggers_temp_bytes": (C.c_size_t, [_I64, _I32]),
+    "pdg_prewarm_triggers": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I32, C.c_double, _I32,
+                                       _P, _P, _P, _P, C.c_size_t, _P]),
     "pdg_rank_allgather_sort_temp_bytes": (C.c_size_t, [_I64, C.c_int32]),
     "pdg_rank_allgather_sort": (C.c_int, [_P, _P, _I64, C.c_int32, _P, _P, C.c_int32, _P,
                                           C.c_size_t, _P]),

@@ -17,6 +17,8 @@
 // can start more), and one thread replays the reference loops on those short
 // lists in shared memory, emitting the events (preempt / start) in the order
 // the simulator applies them.
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -286,4 +288,91 @@ extern "C" int pdg_dispatch_status(const void* temp, int64_t n, int32_t n_backen
   return cuda_status(cudaMemcpyAsync(status_out, status, 4, cudaMemcpyDeviceToHost,
                                      (cudaStream_t)stream),
                      "pdg_dispatch_status");
+}
+
+// ---------------------------------------------------------------------------
+// a11b: Simulator._update_attained (simcore.py:306-313) for a whole queue.
+// age[a] = completed[a] + max(progress[a], max over active started tasks t of
+// app a of min(service[t], max(0, now - (start[t] + cold[t])))).  The max is
+// taken with 64-bit atomicMax on order-preserving images of the doubles, so
+// the result does not depend on task order: bit-identical to the reference
+// loop (which returns the first of equal values; only +0/-0 could differ).
+// ---------------------------------------------------------------------------
+namespace pdg {
+__device__ __forceinline__ double from_orderable_u64(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__global__ void attained_init_kernel(const double* __restrict__ progress, int64_t n,
+                                     uint64_t* __restrict__ best) {
+  for (int64_t a = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; a < n;
+       a += int64_t(gridDim.x) * blockDim.x)
+    best[a] = orderable_u64(progress[a]);
+}
+
+__global__ void attained_tasks_kernel(const int32_t* __restrict__ app,
+                                      const uint8_t* __restrict__ active,
+                                      const double* __restrict__ start,
+                                      const double* __restrict__ cold,
+                                      const double* __restrict__ service, int64_t n_tasks,
+                                      int64_t n_apps, double now, uint64_t* __restrict__ best) {
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n_tasks;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const double st = start[t];
+    const int32_t a = app[t];
+    if (!active[t] || st != st || a < 0 || a >= n_apps) continue;  // not running / not started
+    const double x = dsub(now, dadd(st, cold[t]));
+    const double run = x > 0.0 ? x : 0.0;                         // max(0.0, x)
+    const double sv = service[t];
+    const double v = run < sv ? run : sv;                         // min(service, run)
+    atomicMax(reinterpret_cast<unsigned long long*>(best + a),
+              static_cast<unsigned long long>(orderable_u64(v)));
+  }
+}
+
+__global__ void attained_final_kernel(const double* __restrict__ completed,
+                                      const uint64_t* __restrict__ best, int64_t n,
+                                      double* __restrict__ age) {
+  for (int64_t a = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; a < n;
+       a += int64_t(gridDim.x) * blockDim.x)
+    age[a] = dadd(completed[a], from_orderable_u64(best[a]));
+}
+}  // namespace pdg
+
+extern "C" int pdg_attained_service(const double* completed, const double* progress,
+                                    int64_t n_apps, const int32_t* task_app,
+                                    const uint8_t* task_active, const double* task_start,
+                                    const double* task_cold, const double* task_service,
+                                    int64_t n_tasks, double now, double* age_out, void* temp,
+                                    size_t temp_bytes, void* stream) {
+  if (n_apps < 0 || n_tasks < 0 ||
+      (n_apps > 0 && (!completed || !progress || !age_out || !temp)) ||
+      (n_tasks > 0 && (!task_app || !task_active || !task_start || !task_cold ||
+                       !task_service))) {
+    set_error("pdg_attained_service: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (n_apps == 0) return PDG_OK;
+  if (temp_bytes < size_t(n_apps) * 8) {
+    set_error("pdg_attained_service: temp_bytes %zu < %lld", temp_bytes,
+              (long long)(n_apps * 8));
+    return PDG_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint64_t* best = static_cast<uint64_t*>(temp);
+  const int64_t cap = int64_t(sm_count()) * 8;
+  auto grid = [&](int64_t m) { return unsigned(std::min<int64_t>((m + 255) / 256, cap)); };
+  attained_init_kernel<<<grid(n_apps), 256, 0, st>>>(progress, n_apps, best);
+  int rc = launch_status("attained_init_kernel");
+  if (rc != PDG_OK) return rc;
+  if (n_tasks > 0) {
+    attained_tasks_kernel<<<grid(n_tasks), 256, 0, st>>>(task_app, task_active, task_start,
+                                                         task_cold, task_service, n_tasks,
+                                                         n_apps, now, best);
+    rc = launch_status("attained_tasks_kernel");
+    if (rc != PDG_OK) return rc;
+  }
+  attained_final_kernel<<<grid(n_apps), 256, 0, st>>>(completed, best, n_apps, age_out);
+  return launch_status("attained_final_kernel");
 }

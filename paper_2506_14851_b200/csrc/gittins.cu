@@ -241,28 +241,35 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
 }
 
 // ---------------------------------------------------------------------------
-// K1c: lane-per-row scorer for rows of <= 256 buckets (the queue's layout).
-// Each warp stages 32 rows (16 KB of u16 counts) into shared memory with
-// cp.async (12 warps per SM overlap one another's copies and scans), then
-// lane l scans row l sequentially: no shuffles, ~11 issue
-// slots per bucket.  The alive boundary j0 is found with bit-exact float64
-// tests (binary search, values ascend), Z = sum of alive counts, and every
-// bucket j >= j0 contributes (P_j + d_j (Z - S_j)) / S_j; zero-mass buckets
-// never beat the previous positive one (and are +inf before any mass), so
-// they need no masking.  Rows must hold zero counts past nbins.
+// K1b, lane-per-row form for the queue's layout (rows of <= 256 buckets,
+// 16-byte aligned, zero counts past nbins).  Each warp owns a ring of STAGES
+// tiles of 32 rows in shared memory; a tile is filled by TMA bulk copies
+// (cp.async.bulk, one 2*stride-byte copy per row issued by its lane, padded
+// to 33 uint4 per row so that lane-per-row LDS.128 reads are conflict-free)
+// completing on the slot's mbarrier, STAGES-1 tiles ahead of the one being
+// scored; row headers are prefetched into registers with the copies.
+//
+// Per row, lane l scans row l sequentially.  The alive boundary j0 is found
+// with bit-exact float64 tests (binary search, values ascend), Z = sum of
+// alive counts (IDP2A, two counts per instruction).  With t = j - j0,
+// d_j = d0 + t*w, S_j the alive prefix mass and T_j = Z - S_j, the
+// reference's numerator P_j + d_j*T_j (sched.py:118-124) is exactly
+//     d0*Z + w*I_j,   I_j = sum_{k<=j} (k-j0) m_k + t*T_j,   I_{j+1} = I_j + T_j,
+// so a bucket is two exact integer-valued float adds (I += T, T -= m), one
+// FFMA, one MUFU reciprocal, one FMUL and a min -- no per-bucket d_j or P_j.
+// Zero-mass buckets never beat the previous positive one (and are +inf
+// before any mass), so they need no masking.
 // ---------------------------------------------------------------------------
-constexpr int kRowWarps = 12;
 constexpr int kRowU4 = 33;          // uint4 per staged row: 32 + 1 pad (bank spread)
 constexpr int kTileU4 = 32 * kRowU4;
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool pred) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  const int sz = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gsrc), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+#ifndef PDG_ROWS_WARPS
+#define PDG_ROWS_WARPS 6
+#endif
+#ifndef PDG_ROWS_STAGES
+#define PDG_ROWS_STAGES 2
+#endif
+constexpr int kRowWarps = PDG_ROWS_WARPS;
+constexpr int kRowStages = PDG_ROWS_STAGES;
 
 __device__ __forceinline__ float rcp_approx(float x) {    // MUFU.RCP, ~1 ulp; rcp(0) = +inf
   float r;
@@ -270,133 +277,177 @@ __device__ __forceinline__ float rcp_approx(float x) {    // MUFU.RCP, ~1 ulp; r
   return r;
 }
 
-__device__ __forceinline__ float lo16f(uint32_t x) {      // exact u16 -> float
-  return __int_as_float(__byte_perm(x, 0x4B00u, 0x5410)) - 8388608.f;
-}
-__device__ __forceinline__ float hi16f(uint32_t x) {
-  return __int_as_float(__byte_perm(x, 0x4B00u, 0x5432)) - 8388608.f;
+// Two u16 counts of a word -> exact floats: PRMT builds the bit patterns
+// 2^23 + c (selector immediate, magic 0x4B00 in a register), one packed
+// f32x2 add (sm_100 FADD2) removes the 2^23 bias from both.
+__device__ __forceinline__ void u16x2_to_f32(uint32_t x, uint32_t magic, float& lo, float& hi) {
+  uint32_t l, h;
+  asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(l) : "r"(x), "r"(magic));
+  asm("prmt.b32 %0, %1, %2, 0x5432;" : "=r"(h) : "r"(x), "r"(magic));
+  asm("{\n\t.reg .b64 p, q;\n\t"
+      "mov.b64 p, {%2, %3};\n\t"
+      "add.rn.f32x2 q, p, %4;\n\t"
+      "mov.b64 {%0, %1}, q;\n\t}"
+      : "=r"(l), "=r"(h)
+      : "r"(l), "r"(h), "l"(0xCB000000CB000000ull));
+  lo = __uint_as_float(l);
+  hi = __uint_as_float(h);
 }
 
-__global__ void __launch_bounds__(kRowWarps * 32, 1) gittins_rows_kernel(HistArgs a) {
-  extern __shared__ uint4 stage[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint4* buf0 = stage + size_t(wib) * kTileU4;
-  const int64_t ntiles = (a.n + 31) >> 5;
-  const int64_t gw = int64_t(blockIdx.x) * kRowWarps + wib;
-  const int64_t nw = int64_t(gridDim.x) * kRowWarps;
-  auto row_of = [&](int64_t i) -> int64_t { return a.row_idx ? int64_t(__ldg(a.row_idx + i)) : i; };
-  auto issue = [&](int64_t myrow, uint4* dst) {
-    for (int q = 0; q < 32; ++q) {
-      const int64_t r = __shfl_sync(kFull, myrow, q);
-      const uint4* src = reinterpret_cast<const uint4*>(a.counts + (r < 0 ? 0 : r) * a.stride);
-      cp_async16(dst + q * kRowU4 + lane, src + lane, r >= 0);
+struct RowHdr {
+  double lo, w, est, age;
+  int64_t r;                        // < 0: no row (past the end)
+  int k;
+  uint32_t tb;
+};
+
+// Score one staged row (lane-per-row); writes the row's outputs.
+__device__ __forceinline__ void score_staged_row(const HistArgs& a, const uint4* row,
+                                                 const RowHdr& h) {
+  const int64_t r = h.r;
+  const double lo = h.lo, w = h.w, est = h.est, age = h.age;
+  const int k = h.k;
+  // first alive bucket (values ascend): bit-exact float64 tests
+  int j0 = k;
+  double d0 = 0.0;
+  {
+    const double e0 = exact_d(lo, w, est, age, 0);
+    if (e0 > 0.0) {
+      j0 = 0;
+      d0 = e0;
+    } else {
+      int l = 1, hi = k;                             // smallest alive j in [l, hi)
+      while (l < hi) {
+        const int mid = (l + hi) >> 1;
+        if (exact_d(lo, w, est, age, mid) > 0.0) hi = mid; else l = mid + 1;
+      }
+      j0 = l;
+      if (j0 < k) d0 = exact_d(lo, w, est, age, j0);
     }
-    cp_async_commit();
-  };
-  // single-buffered per warp: 12 warps per SM overlap one another's copies
-  for (int64_t t = gw; t < ntiles; t += nw) {
+  }
+  const int c0 = j0 >> 3, cend = (k + 7) >> 3;
+  // alive mass Z
+  uint32_t zi = 0;
+  if (j0 < k) {                                      // else: nothing alive (exhausted)
+    const uint4 v = row[c0];
+    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = c0 * 8 + 2 * q;
+      const uint32_t keep = (j >= j0 ? 0x0000ffffu : 0u) | (j + 1 >= j0 ? 0xffff0000u : 0u);
+      zi = __dp2a_lo(wd[q] & keep, 0x0101u, zi);
+    }
+  }
+  for (int c = c0 + 1; c < cend; ++c) {
+    const uint4 v = row[c];
+    zi = __dp2a_lo(v.x, 0x0101u, zi);
+    zi = __dp2a_lo(v.y, 0x0101u, zi);
+    zi = __dp2a_lo(v.z, 0x0101u, zi);
+    zi = __dp2a_lo(v.w, 0x0101u, zi);
+  }
+  float key;
+  uint8_t flags = 0;
+  if (zi == 0) {                                     // exhausted: sched.py:295-300
+    key = float(dmul(age, a.penalty));
+    flags = PDG_FLAG_OVERRUN;
+  } else {
+    const float Zf = float(zi);
+    const float af = float(dmul(d0, double(zi)));    // d0 * Z
+    const float bf = float(w);
+    float I = -Zf, T = Zf, best = __int_as_float(0x7f800000);
+    auto bucket = [&](float m) {
+      I += T;                                        // exact (integer-valued)
+      T -= m;
+      best = fminf(best, fmaf(bf, I, af) * rcp_approx(Zf - T));
+    };
+    const uint32_t magic = 0x4B00u;
+    {                                                // first chunk: skip j < j0
+      const uint4 v = row[c0];
+      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float m0, m1;
+        u16x2_to_f32(wd[q], magic, m0, m1);
+        if (c0 * 8 + 2 * q >= j0) bucket(m0);
+        if (c0 * 8 + 2 * q + 1 >= j0) bucket(m1);
+      }
+    }
+    for (int c = c0 + 1; c < cend; ++c) {
+      const uint4 v = row[c];
+      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float m0, m1;
+        u16x2_to_f32(wd[q], magic, m0, m1);
+        bucket(m0);
+        bucket(m1);
+      }
+    }
+    key = best;
+  }
+  if (!(key > 0.f)) key = 0.f;
+  if (a.out_f32) a.out_f32[r] = key;
+  if (a.out_flags) a.out_flags[r] = flags;
+  if (a.out_key) a.out_key[r] = (uint64_t(__float_as_uint(key)) << 32) | h.tb;
+}
+
+template <int W, int STAGES>
+__global__ void __launch_bounds__(W * 32, 1) gittins_rows_kernel(HistArgs a) {
+  extern __shared__ __align__(128) uint4 stage[];
+  __shared__ uint64_t bars[W * STAGES];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint4* tiles = stage + size_t(wib) * STAGES * kTileU4;
+  uint64_t* bar = bars + wib * STAGES;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(bar + s, 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const int64_t ntiles = (a.n + 31) >> 5;
+  const int64_t gw = int64_t(blockIdx.x) * W + wib;
+  const int64_t nw = int64_t(gridDim.x) * W;
+  const unsigned row_bytes = unsigned(a.stride) * 2u;     // <= 512, multiple of 16
+  const int kmax = int(a.stride);
+  const uint64_t policy = l2_evict_first_policy();
+
+  // one tile into ring slot `slot`: lane l copies row l and loads its header
+  auto issue = [&](int64_t t, int slot, RowHdr& h) {
     const int64_t i = t * 32 + lane;
     const bool valid = i < a.n;
-    const int64_t r = valid ? row_of(i) : -1;
-    // row headers are loaded while the counts stream into shared memory
-    double lo = 0.0, w = 0.0, est = 0.0, age = 0.0;
-    int k = 1;
-    uint32_t tb = 0;
-    if (valid) {
-      lo = __ldg(a.lo + r);
-      w = __ldg(a.width + r);
-      est = __ldg(a.est + r);
-      age = __ldg(a.age + r);
-      k = __ldg(a.nbins + r);
-      tb = a.tiebreak ? __ldg(a.tiebreak + r) : uint32_t(r);
-    }
-    issue(valid ? r : -1, buf0);
-    cp_async_wait<0>();
+    const int64_t r = valid ? (a.row_idx ? int64_t(__ldg(a.row_idx + i)) : i) : -1;
+    const unsigned total = __reduce_add_sync(kFull, valid ? row_bytes : 0u);
+    fence_proxy_async_smem();                        // earlier reads of the slot first
+    if (lane == 0) mbar_arrive_expect_tx(bar + slot, total);
     __syncwarp();
-    const uint4* row = buf0 + lane * kRowU4;
+    if (valid)
+      bulk_g2s(tiles + slot * kTileU4 + lane * kRowU4, a.counts + r * a.stride, row_bytes,
+               bar + slot, policy);
+    h.r = r;
     if (valid) {
-      // first alive bucket (values ascend): bit-exact float64 tests
-      int j0 = k;
-      double d0 = 0.0;
-      {
-        const double e0 = exact_d(lo, w, est, age, 0);
-        if (e0 > 0.0) {
-          j0 = 0;
-          d0 = e0;
-        } else {
-          int l = 1, h = k;                          // smallest alive j in [l, h)
-          while (l < h) {
-            const int mid = (l + h) >> 1;
-            if (exact_d(lo, w, est, age, mid) > 0.0) h = mid; else l = mid + 1;
-          }
-          j0 = l;
-          if (j0 < k) d0 = exact_d(lo, w, est, age, j0);
-        }
-      }
-      const int c0 = j0 >> 3, cend = (k + 7) >> 3;
-      // alive mass Z: IDP2A sums both u16 counts of a word in one instruction
-      uint32_t zi = 0;
-      if (j0 < k) {                                  // else: nothing alive (exhausted)
-        const uint4 v = row[c0];
-        const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int j = c0 * 8 + 2 * h;
-          const uint32_t keep = (j >= j0 ? 0x0000ffffu : 0u) | (j + 1 >= j0 ? 0xffff0000u : 0u);
-          zi = __dp2a_lo(wd[h] & keep, 0x0101u, zi);
-        }
-      }
-      for (int c = c0 + 1; c < cend; ++c) {
-        const uint4 v = row[c];
-        zi = __dp2a_lo(v.x, 0x0101u, zi);
-        zi = __dp2a_lo(v.y, 0x0101u, zi);
-        zi = __dp2a_lo(v.z, 0x0101u, zi);
-        zi = __dp2a_lo(v.w, 0x0101u, zi);
-      }
-      const float Z = float(zi);
-      float key;
-      uint8_t flags = 0;
-      if (!(Z > 0.f)) {                              // exhausted: sched.py:295-300
-        key = float(dmul(age, a.penalty));
-        flags = PDG_FLAG_OVERRUN;
-      } else {
-        const float df = float(d0), wf = float(w);
-        float S = 0.f, P = 0.f, best = __int_as_float(0x7f800000);
-        // one bucket at offset h of a chunk whose first bucket sits at
-        // (j - j0) = tb: d = tb*w + h*w + d0 (positive terms), ~10 issue slots
-        auto bucket = [&](float m, float d) {
-          S += m;
-          P = fmaf(m, d, P);
-          const float num = fmaf(d, Z - S, P);
-          best = fminf(best, num * rcp_approx(S));     // rcp(0) = inf before any mass
-        };
-        {                                            // first chunk: skip j < j0
-          const uint4 v = row[c0];
-          const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-          const float tb = float(c0 * 8 - j0);
-#pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            if (c0 * 8 + h >= j0)
-              bucket((h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]),
-                     fmaf(tb + float(h), wf, df));
-          }
-        }
-        for (int c = c0 + 1; c < cend; ++c) {
-          const uint4 v = row[c];
-          const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-          const float db = fmaf(float(c * 8 - j0), wf, df);
-#pragma unroll
-          for (int h = 0; h < 8; ++h)
-            bucket((h & 1) ? hi16f(wd[h >> 1]) : lo16f(wd[h >> 1]), fmaf(float(h), wf, db));
-        }
-        key = best;
-      }
-      if (!(key > 0.f)) key = 0.f;
-      if (a.out_f32) a.out_f32[r] = key;
-      if (a.out_flags) a.out_flags[r] = flags;
-      if (a.out_key) a.out_key[r] = (uint64_t(__float_as_uint(key)) << 32) | tb;
+      h.lo = __ldg(a.lo + r);
+      h.w = __ldg(a.width + r);
+      h.est = __ldg(a.est + r);
+      h.age = __ldg(a.age + r);
+      h.k = min(__ldg(a.nbins + r), kmax);
+      h.tb = a.tiebreak ? __ldg(a.tiebreak + r) : uint32_t(r);
     }
+  };
+
+  RowHdr h[STAGES];
+#pragma unroll
+  for (int s = 0; s + 1 < STAGES; ++s)
+    if (gw + s * nw < ntiles) issue(gw + s * nw, s, h[s]);
+  uint32_t q = 0;
+  for (int64_t t = gw; t < ntiles; t += nw, ++q) {
+    const int64_t tn = t + int64_t(STAGES - 1) * nw;
+    if (tn < ntiles) issue(tn, int((q + STAGES - 1) % STAGES), h[STAGES - 1]);
+    const int s = int(q % STAGES);
+    mbar_wait(bar + s, (q / STAGES) & 1u);
+    if (h[0].r >= 0) score_staged_row(a, tiles + s * kTileU4 + lane * kRowU4, h[0]);
     __syncwarp();
+#pragma unroll
+    for (int j = 0; j + 1 < STAGES; ++j) h[j] = h[j + 1];
   }
 }
 
@@ -536,19 +587,20 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
   const int64_t maxb = rows->stride;   // buckets per row are bounded by the stride
   // lane-per-row tiles pay off once every SM has tiles to stream; small
   // (incremental) batches take the warp-per-row kernel's lower latency
-  if (maxb == 256 && n >= int64_t(sm_count()) * 32 * 4) {
-    const size_t smem = size_t(kRowWarps) * kTileU4 * sizeof(uint4);
+  if (maxb <= 256 && n >= int64_t(sm_count()) * 32 * 4) {
+    auto kern = gittins_rows_kernel<kRowWarps, kRowStages>;
+    const size_t smem = size_t(kRowWarps) * kRowStages * kTileU4 * sizeof(uint4);
     static bool attr = false;
     if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(gittins_rows_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(smem));
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gittins_rows_kernel)");
       attr = true;
     }
     int64_t tiles = (n + 31) / 32;
     int64_t nb = (tiles + kRowWarps - 1) / kRowWarps;
     if (nb > sm_count()) nb = sm_count();
-    gittins_rows_kernel<<<unsigned(nb), kRowWarps * 32, smem, s>>>(a);
+    kern<<<unsigned(nb), kRowWarps * 32, smem, s>>>(a);
     return launch_status("gittins_rows_kernel");
   }
   if (maxb <= 256) gittins_hist_kernel<1><<<unsigned(blocks), threads, 0, s>>>(a);
@@ -559,6 +611,135 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
     return PDG_EUNSUPPORTED;
   }
   return launch_status("gittins_hist_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// K1a, sample form (sched.py:51-85): one CTA per distribution; the tail
+// {s - age : s > age} (+inf padding) is bitonic-sorted in shared memory, then
+// one thread replays the reference's scan: prefix sums in sorted order, one
+// candidate per group of equal values, (prefix + d*(n-j)) / j.
+// ---------------------------------------------------------------------------
+namespace pdg {
+__global__ void __launch_bounds__(256) gittins_samples_kernel(
+    const double* __restrict__ samples, const int64_t* __restrict__ off,
+    const int32_t* __restrict__ len, const double* __restrict__ ages, int64_t n_rows,
+    int npow2, double* __restrict__ out) {
+  extern __shared__ double tail[];
+  __shared__ int cnt;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    const double* s = samples + off[r];
+    const int n = len[r];
+    const double age = ages[r];
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    int live = 0;
+    for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+      const bool on = i < n && s[i] > age;
+      tail[i] = on ? dsub(s[i], age) : inf;
+      live += on;
+    }
+    if (live) atomicAdd(&cnt, live);
+    for (int k = 2; k <= npow2; k <<= 1) {             // bitonic sort, ascending
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+          const int p = i ^ j;
+          if (p > i) {
+            const double x = tail[i], y = tail[p];
+            const bool up = (i & k) == 0;
+            if (up ? x > y : x < y) { tail[i] = y; tail[p] = x; }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int m = cnt;
+      double best;
+      if (m == 0) {
+        best = __longlong_as_double(0x7ff8000000000000ll);           // exhausted
+      } else if (tail[0] == tail[m - 1]) {
+        best = tail[0];                                               // degenerate
+      } else {
+        best = inf;
+        double prefix = 0.0;
+        int i = 0;
+        while (i < m) {
+          int j = i;
+          while (j < m && tail[j] == tail[i]) prefix = dadd(prefix, tail[j++]);
+          const double d = tail[i];
+          const double num = dadd(prefix, dmul(d, double(m - j)));
+          const double ratio = __ddiv_rn(num, double(j));
+          if (ratio < best) best = ratio;
+          i = j;
+        }
+      }
+      out[r] = best;
+    }
+    __syncthreads();
+  }
+}
+}  // namespace pdg
+
+extern "C" int pdg_gittins_rank_samples(const double* samples, const int64_t* off,
+                                        const int32_t* len, const double* ages, int64_t n_rows,
+                                        int32_t max_len, double* out_rank, void* stream) {
+  using namespace pdg;
+  if (n_rows < 0 || max_len < 0 || max_len > PDG_SAMPLES_MAX ||
+      (n_rows > 0 && (!samples || !off || !len || !ages || !out_rank))) {
+    set_error("pdg_gittins_rank_samples: invalid arguments (max_len <= %d)", PDG_SAMPLES_MAX);
+    return PDG_EINVAL;
+  }
+  if (n_rows == 0) return PDG_OK;
+  int npow2 = 1;
+  while (npow2 < max_len) npow2 <<= 1;
+  const size_t smem = size_t(npow2) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gittins_samples_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(PDG_SAMPLES_MAX * sizeof(double)));
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gittins_samples_kernel)");
+    attr = true;
+  }
+  const int64_t blocks = n_rows < int64_t(sm_count()) * 8 ? n_rows : int64_t(sm_count()) * 8;
+  gittins_samples_kernel<<<unsigned(blocks), 256, smem, (cudaStream_t)stream>>>(
+      samples, off, len, ages, n_rows, npow2, out_rank);
+  return launch_status("gittins_samples_kernel");
+}
+
+extern "C" int pdg_gittins_rank_samples_host(const double* samples, int32_t n, double age,
+                                             double* out_rank, void* stream) {
+  using namespace pdg;
+  if (n < 0 || n > PDG_SAMPLES_MAX || (n > 0 && !samples) || !out_rank) {
+    set_error("pdg_gittins_rank_samples_host: invalid arguments (n <= %d)", PDG_SAMPLES_MAX);
+    return PDG_EINVAL;
+  }
+  HostStage& st = g_stage;
+  if (!st.zh) {
+    cudaError_t e = cudaHostAlloc(&st.zh, PDG_ZERO_COPY_MAX * sizeof(double),
+                                  cudaHostAllocMapped);
+    if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_samples_host cudaHostAlloc");
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&st.zd), st.zh, 0);
+    if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_samples_host map");
+    st.zcap = PDG_ZERO_COPY_MAX;
+  }
+  // [samples | age | out | off (int64) | len (int32)]
+  std::memcpy(st.zh, samples, size_t(n) * sizeof(double));
+  st.zh[n] = age;
+  int64_t* offp = reinterpret_cast<int64_t*>(st.zh + n + 2);
+  int32_t* lenp = reinterpret_cast<int32_t*>(st.zh + n + 3);
+  *offp = 0;
+  *lenp = n;
+  int rc = pdg_gittins_rank_samples(st.zd, reinterpret_cast<const int64_t*>(st.zd + n + 2),
+                                    reinterpret_cast<const int32_t*>(st.zd + n + 3), st.zd + n,
+                                    1, n, st.zd + n + 1, stream);
+  if (rc != PDG_OK) return rc;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "pdg_gittins_rank_samples_host sync");
+  *out_rank = st.zh[n + 1];
+  return PDG_OK;
 }
 
 extern "C" size_t pdg_order_temp_bytes(int64_t n) {

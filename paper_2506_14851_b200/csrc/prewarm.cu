@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(128) prewarm_plan_kernel(PlanArgs a) {
     const bool rel = a.shift != nullptr;             // completion = shift + sample (simcore.py:455)
     const double sh = rel ? a.shift[j] : 0.0;
     if (p_s < knob || n <= 0) {                      // prewarm.py:63-64
-      if (lane == 0) { a.has_plan[j] = 0; a.trigger[j] = 0.0; a.p_e[j] = 0.0; }
+      // (n < 0: a slot the trigger setup flagged; its has_plan stays)
+      if (lane == 0) { if (n >= 0) a.has_plan[j] = 0; a.trigger[j] = 0.0; a.p_e[j] = 0.0; }
       continue;
     }
     // relative pools are sorted (the prewarm tables) and shift + s is
@@ -275,6 +276,26 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
     if (t3 >= 0 && t3 == t0) { f0 += f3; t3 = -1; }
     if (t3 >= 0 && t3 == t1) { f1 += f3; t3 = -1; }
     if (t3 >= 0 && t3 == t2) { f2 += f3; t3 = -1; }
+    // successors 4.. (no unit records): merged into the first four by type,
+    // or written once per further type (its first occurrence sums the rest)
+    const int ns_all = a.unit_rec ? 0 : a.succ_len[u];
+    auto succ_type = [&](int i) {
+      const int ty = a.unit_type[gbase + a.succ_nxt[a.succ_off[u] + i]];
+      return ty < a.n_types ? ty : -1;               // no need row for that type
+    };
+    for (int i = 4; i < ns_all; ++i) {
+      const int ty = succ_type(i);
+      const float f = float(a.succ_p[a.succ_off[u] + i]) * pneed;
+      if (ty < 0) continue;
+      if (ty == t0) f0 += f;
+      else if (ty == t1) f1 += f;
+      else if (ty == t2) f2 += f;
+      else if (ty == t3) f3 += f;
+    }
+    t0 = t0 < a.n_types ? t0 : -1;
+    t1 = t1 < a.n_types ? t1 : -1;
+    t2 = t2 < a.n_types ? t2 : -1;
+    t3 = t3 < a.n_types ? t3 : -1;
     if (a.need && (TK & 3) == 0) {                   // dense row: 16-B zero stores ...
       float4* row4 = reinterpret_cast<float4*>(a.need + app * int64_t(TK));
       for (int i = lane; i < (TK >> 2); i += 32) __stcs(row4 + i, make_float4(0.f, 0.f, 0.f, 0.f));
@@ -299,6 +320,23 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
         if (t1 >= 0) atomicAdd(cagg + t1 * a.n_windows + kwin, double(f1));
         if (t2 >= 0) atomicAdd(cagg + t2 * a.n_windows + kwin, double(f2));
         if (t3 >= 0) atomicAdd(cagg + t3 * a.n_windows + kwin, double(f3));
+      }
+    }
+    if (ns_all > 4) {                                // types beyond the first four
+      __syncwarp();                                  // after the zero fill and the stores
+      for (int i = 4; i < ns_all; ++i) {
+        const int ty = succ_type(i);
+        if (ty < 0 || ty == t0 || ty == t1 || ty == t2 || ty == t3) continue;
+        bool first = true;
+        for (int k = 4; k < i; ++k) first = first && succ_type(k) != ty;
+        if (!first) continue;
+        float f = 0.f;
+        for (int k = i; k < ns_all; ++k)
+          if (succ_type(k) == ty) f += float(a.succ_p[a.succ_off[u] + k]) * pneed;
+        if (kwin >= 0) {
+          if (a.need) __stcs(a.need + app * int64_t(TK) + ty * a.n_windows + kwin, f);
+          if (a.agg) atomicAdd(cagg + ty * a.n_windows + kwin, double(f));
+        }
       }
     }
     __syncwarp();
@@ -557,15 +595,15 @@ extern "C" int pdg_prewarm_need(const pdg_prewarm_tables* t, const int32_t* grap
 namespace pdg {
 __global__ void trigger_jobs_kernel(pdg_prewarm_tables t, const int32_t* __restrict__ graph,
                                     const int32_t* __restrict__ unit,
-                                    const double* __restrict__ now, int64_t n,
+                                    const double* __restrict__ now, int64_t n, int32_t slots,
                                     const double* __restrict__ warmup, int32_t n_types,
                                     double knob, int32_t bucket_count, int32_t* off,
                                     int32_t* len, int32_t* bc, double* p_s, double* t_p,
-                                    double* kn, double* nw) {
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < 4 * n;
+                                    double* kn, double* nw, uint8_t* has_plan) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < int64_t(slots) * n;
        j += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t app = j >> 2;
-    const int slot = int(j & 3);
+    const int64_t app = j / slots;
+    const int slot = int(j - app * slots);
     const int gb = t.graph_base[graph[app]];
     const int u = gb + unit[app];
     const int ns = t.succ_len[u];
@@ -576,40 +614,48 @@ __global__ void trigger_jobs_kernel(pdg_prewarm_tables t, const int32_t* __restr
       ty = t.unit_type[gb + t.succ_nxt[so]];
       p = t.succ_p[so];
     }
-    const bool ok = ty >= 0 && ty < n_types;         // successors without warm content: no plan
+    // successors without warm content: no plan (simcore.py:462-464); a fan-out
+    // wider than the output or a type without a warmup entry is flagged
+    const uint8_t flag = ns > slots ? uint8_t(PDG_PLAN_OVERFLOW)
+                       : ty >= n_types ? uint8_t(PDG_PLAN_BAD_TYPE) : uint8_t(0);
+    const bool ok = ty >= 0 && flag == 0;
     off[j] = t.svc_off[u];
-    len[j] = ok ? t.svc_len[u] : 0;
+    len[j] = ok ? t.svc_len[u] : -1;                 // -1: the plan kernel leaves has_plan
     bc[j] = bucket_count;
     p_s[j] = p;
     t_p[j] = ok ? warmup[ty] : 0.0;
     kn[j] = knob;
     nw[j] = now[app];
+    if (!ok) has_plan[j] = flag;
   }
 }
 }  // namespace pdg
 
-extern "C" size_t pdg_prewarm_triggers_temp_bytes(int64_t n) {
-  return size_t(4 * n) * (4 * 3 + 8 * 4) + 256;
+extern "C" size_t pdg_prewarm_triggers_temp_bytes(int64_t n, int32_t slots) {
+  return size_t(slots > 0 ? slots : 0) * size_t(n) * (4 * 3 + 8 * 4) + 256;
 }
 
 extern "C" int pdg_prewarm_triggers(const pdg_prewarm_tables* t, const int32_t* graph,
                                     const int32_t* unit, const double* now, int64_t n,
-                                    const double* warmup_by_type, int32_t n_types, double knob,
-                                    int32_t bucket_count, uint8_t* has_plan, double* trigger,
-                                    double* p_e, void* temp, size_t temp_bytes, void* stream) {
-  if (!t || n < 0 || n_types < 1 || bucket_count < 1 || !(knob >= 0.0 && knob <= 1.0) ||
+                                    int32_t slots, const double* warmup_by_type,
+                                    int32_t n_types, double knob, int32_t bucket_count,
+                                    uint8_t* has_plan, double* trigger, double* p_e,
+                                    void* temp, size_t temp_bytes, void* stream) {
+  if (!t || n < 0 || slots < 1 || slots > 64 || n_types < 1 || bucket_count < 1 ||
+      !(knob >= 0.0 && knob <= 1.0) ||
       (n > 0 && (!graph || !unit || !now || !warmup_by_type || !has_plan || !trigger || !p_e ||
                  !temp))) {
-    set_error("pdg_prewarm_triggers: invalid arguments (knob in [0, 1], bucket_count >= 1)");
+    set_error("pdg_prewarm_triggers: invalid arguments (1 <= slots <= 64, knob in [0, 1], "
+              "bucket_count >= 1)");
     return PDG_EINVAL;
   }
   if (n == 0) return PDG_OK;
-  if (temp_bytes < pdg_prewarm_triggers_temp_bytes(n)) {
+  if (temp_bytes < pdg_prewarm_triggers_temp_bytes(n, slots)) {
     set_error("pdg_prewarm_triggers: temp_bytes %zu < %zu", temp_bytes,
-              pdg_prewarm_triggers_temp_bytes(n));
+              pdg_prewarm_triggers_temp_bytes(n, slots));
     return PDG_EINVAL;
   }
-  const int64_t J = 4 * n;
+  const int64_t J = int64_t(slots) * n;
   char* b = static_cast<char*>(temp);
   double* p_s = reinterpret_cast<double*>(b);
   double* t_p = p_s + J;
@@ -622,9 +668,10 @@ extern "C" int pdg_prewarm_triggers(const pdg_prewarm_tables* t, const int32_t* 
   int64_t blocks = (J + 255) / 256;
   const int64_t cap = int64_t(sm_count()) * 8;
   if (blocks > cap) blocks = cap;
-  trigger_jobs_kernel<<<unsigned(blocks), 256, 0, st>>>(*t, graph, unit, now, n, warmup_by_type,
-                                                        n_types, knob, bucket_count, off, len,
-                                                        bc, p_s, t_p, kn, nw);
+  trigger_jobs_kernel<<<unsigned(blocks), 256, 0, st>>>(*t, graph, unit, now, n, slots,
+                                                        warmup_by_type, n_types, knob,
+                                                        bucket_count, off, len, bc, p_s, t_p,
+                                                        kn, nw, has_plan);
   int rc = launch_status("trigger_jobs_kernel");
   if (rc != PDG_OK) return rc;
   PlanArgs a{t->svc_sorted, off, len, bc, p_s, t_p, kn, nw, J, has_plan, trigger, p_e,

@@ -133,6 +133,18 @@ def plan_prewarm(completion_dist, p_s: float, t_p: float, knob: float, now: floa
 # need-probability grid (config 5)
 # ---------------------------------------------------------------------------
 
+def _check_index(graph_idx, unit_idx, now, device):
+    """The queue columns the prewarm kernels read: int32 graph / unit indices
+    and float64 `now`, contiguous, on the tables' device."""
+    for nm, x, dt in (("graph_idx", graph_idx, torch.int32), ("unit_idx", unit_idx, torch.int32),
+                      ("now", now, torch.float64)):
+        if not isinstance(x, torch.Tensor) or x.dtype != dt or not x.is_contiguous() \
+                or x.device != device:
+            raise TypeError(f"{nm} must be a contiguous {dt} tensor on {device}")
+    if not (graph_idx.numel() == unit_idx.numel() == now.numel()):
+        raise ValueError("graph_idx, unit_idx and now must have one entry per application")
+
+
 class PrewarmTablesC(C.Structure):
     _fields_ = [(nm, C.c_void_p) for nm in ("svc_sorted", "svc_off", "svc_len", "graph_base",
                                             "succ_off", "succ_len", "succ_nxt", "succ_p",
@@ -147,6 +159,8 @@ class PrewarmTables:
                  succ_nxt, succ_p, unit_type, n_types, device="cuda"):
         _lib.lib()
         dev = torch.device(device)
+        if dev.type == "cuda" and dev.index is None and torch.cuda.is_available():
+            dev = torch.device("cuda", torch.cuda.current_device())
 
         def t(a, dt):
             a = np.ascontiguousarray(np.asarray(a, dtype=dt))
@@ -178,7 +192,12 @@ class PrewarmTables:
             rec[:U, 2 + i] = np.where(has, ut_a[gof + nx_a[idx]] if nx_a.size else -1, -1)
             pf = np.where(has, p_a[idx] if p_a.size else 0.0, 0.0).astype(np.float32)
             rec[:U, 6 + i] = pf.view(np.int32)
-        self.t["unit_rec"] = t(rec.reshape(-1), np.int32)
+        # the packed records hold four successors: wider fan-outs take the
+        # table-walking need kernel
+        self.max_succ = int(sl_a.max()) if sl_a.size else 0
+        self.max_type = int(ut_a.max()) if ut_a.size else -1
+        if self.max_succ <= 4:
+            self.t["unit_rec"] = t(rec.reshape(-1), np.int32)
         self.c = PrewarmTablesC(*[_lib.ptr(self.t[nm]) if nm in self.t else None
                                   for nm, _ in PrewarmTablesC._fields_])
         self.n_units = int(np.asarray(svc_len).size)
@@ -234,34 +253,44 @@ class PrewarmTables:
     def triggers(self, graph_idx, unit_idx, now, warmup_by_type, knob: float,
                  bucket_count: int, stream=None):
         """plan_prewarm for every (application, successor slot) of the queue
-        (config 5's latest-safe triggers): (has_plan bool[N,4], trigger
-        f64[N,4], p_e f64[N,4]) on the device."""
+        (config 5's latest-safe triggers, _plan_prewarms simcore.py:450-478):
+        (has_plan bool[N,S], trigger f64[N,S], p_e f64[N,S]) on the device,
+        S = the bank's largest fan-out, successors in sorted order."""
+        if len(warmup_by_type) <= self.max_type:
+            raise ValueError(f"warmup_by_type has {len(warmup_by_type)} entries; the tables "
+                             f"hold backend type {self.max_type}")
+        _check_index(graph_idx, unit_idx, now, self.device)
         n = int(graph_idx.numel())
+        S = max(self.max_succ, 1)
         dev = self.device
-        has = torch.zeros((n, 4), dtype=torch.uint8, device=dev)
-        trig = torch.zeros((n, 4), dtype=torch.float64, device=dev)
-        pe = torch.zeros((n, 4), dtype=torch.float64, device=dev)
-        L = _lib.lib()
-        tb = int(L.pdg_prewarm_triggers_temp_bytes(n))
-        temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
-        w = torch.as_tensor(warmup_by_type, dtype=torch.float64, device=dev).contiguous()
-        _lib.check(L.pdg_prewarm_triggers(
-            C.byref(self.c), _lib.ptr(graph_idx), _lib.ptr(unit_idx), _lib.ptr(now), n,
-            _lib.ptr(w), int(w.numel()), float(knob), int(bucket_count), _lib.ptr(has),
-            _lib.ptr(trig), _lib.ptr(pe), _lib.ptr(temp), temp.numel(), _lib.stream_ptr(stream)),
-            "pdg_prewarm_triggers")
-        return has.bool(), trig, pe
+        stream = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(stream):              # outputs and temp live on `stream`
+            has = torch.zeros((n, S), dtype=torch.uint8, device=dev)
+            trig = torch.zeros((n, S), dtype=torch.float64, device=dev)
+            pe = torch.zeros((n, S), dtype=torch.float64, device=dev)
+            L = _lib.lib()
+            tb = int(L.pdg_prewarm_triggers_temp_bytes(n, S))
+            temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
+            w = torch.as_tensor(warmup_by_type, dtype=torch.float64, device=dev).contiguous()
+            _lib.check(L.pdg_prewarm_triggers(
+                C.byref(self.c), _lib.ptr(graph_idx), _lib.ptr(unit_idx), _lib.ptr(now), n, S,
+                _lib.ptr(w), int(w.numel()), float(knob), int(bucket_count), _lib.ptr(has),
+                _lib.ptr(trig), _lib.ptr(pe), _lib.ptr(temp), temp.numel(),
+                _lib.stream_ptr(stream)), "pdg_prewarm_triggers")
+            return has == 1, trig, pe
 
     def need(self, graph_idx, unit_idx, now, windows, *, dense=True, aggregate=True,
              out=None, window_index=True, unit_records=True, stream=None):
         """need[N, T, K] float32 (dense) and/or agg[T, K] float64 over the queue.
         window_index: per-(unit, window) lower bounds computed once per window
         grid instead of a binary search per application."""
+        _check_index(graph_idx, unit_idx, now, self.device)
         n = int(graph_idx.numel())
         K = int(windows.numel())
         dev = self.device
         self.c.win_idx = _lib.ptr(self._window_index(windows, stream)) if window_index else None
-        self.c.unit_rec = _lib.ptr(self.t["unit_rec"]) if unit_records else None
+        self.c.unit_rec = (_lib.ptr(self.t["unit_rec"])
+                           if unit_records and "unit_rec" in self.t else None)
         need = out if out is not None else (
             torch.empty((n, self.n_types, K), dtype=torch.float32, device=dev) if dense else None)
         agg = torch.zeros((self.n_types, K), dtype=torch.float64, device=dev) if aggregate else None

@@ -100,6 +100,37 @@ class HistQueue:
             self.tiebreak[sl] = torch.as_tensor(np.asarray(tiebreak, dtype=np.int64).astype(np.int32))
         self.n = max(self.n, start + m)
 
+    # -- attained service (a11b) -------------------------------------------------
+    def update_attained(self, completed, progress, task_app, task_active, task_start,
+                        task_cold, task_service, now: float, n: Optional[int] = None,
+                        stream=None) -> None:
+        """Simulator._update_attained (simcore.py:306-313) for the first n rows
+        on the device: age = completed + max(progress, min(service, max(0, now -
+        (start + cold)))) over each row's active started tasks (task_app = the
+        task's queue row, task_start NaN = not started)."""
+        n = self.n if n is None else int(n)
+        nt = int(task_app.numel())
+        f64, i32, u8 = torch.float64, torch.int32, torch.uint8
+        for nm, x, dt in (("completed", completed, f64), ("progress", progress, f64),
+                          ("task_app", task_app, i32), ("task_active", task_active, u8),
+                          ("task_start", task_start, f64), ("task_cold", task_cold, f64),
+                          ("task_service", task_service, f64)):
+            if x.dtype != dt or not x.is_contiguous() or x.device != self.age.device:
+                raise TypeError(f"{nm} must be a contiguous {dt} tensor on {self.age.device}")
+        if completed.numel() < n or progress.numel() < n or task_active.numel() < nt \
+                or task_start.numel() < nt or task_cold.numel() < nt \
+                or task_service.numel() < nt:
+            raise ValueError("update_attained: column shorter than its table")
+        if getattr(self, "_att_temp", None) is None or self._att_temp.numel() < 8 * n:
+            self._att_temp = torch.empty(max(8 * self.capacity, 16), dtype=torch.uint8,
+                                         device=self.age.device)
+        _lib.check(_lib.lib().pdg_attained_service(
+            _lib.ptr(completed), _lib.ptr(progress), n, _lib.ptr(task_app),
+            _lib.ptr(task_active), _lib.ptr(task_start), _lib.ptr(task_cold),
+            _lib.ptr(task_service), nt, float(now), _lib.ptr(self.age),
+            _lib.ptr(self._att_temp), self._att_temp.numel(), _lib.stream_ptr(stream)),
+            "pdg_attained_service")
+
     # -- scoring ---------------------------------------------------------------
     def score(self, penalty: float = 2.0, n: Optional[int] = None, stream=None,
               keys: bool = True, rows: Optional[torch.Tensor] = None) -> None:

@@ -13,6 +13,8 @@ call.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import ctypes as C
+import math
 import time
 from dataclasses import dataclass
 from enum import Enum
@@ -111,13 +113,21 @@ def _samples_of(dist) -> list:
 
 
 def gittins_rank(dist, age: float) -> float:
-    """Sample form (sched.py:51-85): the distinct samples weighted by
-    multiplicity form the support; same result as the reference's scan."""
+    """Sample form (sched.py:51-85) on the device, bit-identical to the
+    reference's scan: pdg_gittins_rank_samples_host sorts the tail
+    {s - age : s > age} and scans it in the reference's operation order."""
     samples = _samples_of(dist)
     if not samples:
         raise EstimationError("gittins_rank: empty distribution")
-    vals, cnt = np.unique(np.asarray(samples, dtype=float), return_counts=True)
-    return gittins_rank_points(vals, cnt / cnt.sum(), age)
+    s = np.ascontiguousarray(np.asarray(samples, dtype=np.float64))
+    out = C.c_double(0.0)
+    _lib.check(_lib.lib().pdg_gittins_rank_samples_host(
+        s.ctypes.data, int(s.size), float(age), C.byref(out), None),
+        "pdg_gittins_rank_samples_host")
+    if math.isnan(out.value):
+        raise ExhaustedDistributionError(
+            f"no sample exceeds age {age}; distribution exhausted")
+    return out.value
 
 
 def lstf_slack(dist, age: float, deadline: float, now: float) -> float:

@@ -146,3 +146,17 @@ def test_hist_queue_full_size_and_order():
     if mism.any():
         a, bb = want[order[mism]], want[ref_order[mism]]
         assert np.all(np.abs(a - bb) <= 2e-5 * np.maximum(a, bb))
+
+
+def test_rank_samples_bit_exact_vs_oracle(S):
+    """Sample form on the device (pdg_gittins_rank_samples_host) equals the
+    reference-pinned oracle bit for bit (tests/test_gittins_samples_cpu.py)."""
+    from tests.test_gittins_samples_cpu import cases
+    for s, age in cases(1, 80) + [([3.0] * 16384, 1.0), (list(np.arange(16384.0)), 100.5)]:
+        if any(x > age for x in s):
+            assert S.gittins_rank(s, age) == O.gittins_rank_samples(s, age), (len(s), age)
+        else:
+            with pytest.raises(S.ExhaustedDistributionError):
+                S.gittins_rank(s, age)
+    with pytest.raises(S.EstimationError):
+        S.gittins_rank([], 0.0)

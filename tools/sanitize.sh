@@ -1,0 +1,44 @@
+#!/bin/bash
+# compute-sanitizer (memcheck, racecheck, synccheck, initcheck) over the small-case
+# GPU parity tests: engine <0> (synth duration graphs) and <7> (golden KB graphs,
+# LLM + own-input + K3), mc_serial_kernel (forced Lemire rejections), K1a/K1b,
+# K1c, K4a/K4b/triggers, K5/K5b, K6, masks.  Only the repo's kernels (pdg::) are checked.
+set -u
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out/sanitizer
+TESTS=(
+  "tests/test_engine_gpu.py::test_golden_mc_cases_bit_exact"
+  "tests/test_engine_gpu.py::test_understated_bank_features_stay_exact"
+  "tests/test_engine_gpu.py::test_lemire_rejection_replayed_exactly"
+  "tests/test_engine_gpu.py::test_visit_cap_zero_and_empty_units"
+  "tests/test_engine_gpu.py::test_wide_graph_32_units_many_successors"
+  "tests/test_engine_gpu.py::test_histogram_rows_match_set_remaining"
+  "tests/test_workload_gpu.py::test_synth_sample_bit_exact"
+  "tests/test_gittins_gpu.py::test_rank_batch_matches_reference_golden"
+  "tests/test_gittins_gpu.py::test_rank_batch_empty_and_zero_width"
+  "tests/test_gittins_gpu.py::test_refresh_priorities_ragged_and_overrun"
+  "tests/test_gittins_gpu.py::test_hist_queue_vs_oracle"
+  "tests/test_policy_gpu.py"
+  "tests/test_prewarm_gpu.py::test_plan_prewarm_batch_matches_reference"
+  "tests/test_prewarm_gpu.py::test_need_grid_vs_oracle"
+  "tests/test_prewarm_gpu.py::test_triggers_vs_oracle"
+  "tests/test_dispatch_gpu.py::test_plan_random_tables_vs_oracle"
+  "tests/test_masks_gpu.py::test_masks_golden_graphs"
+  "tests/test_stream_gpu.py::test_event_stream_parity"
+  "tests/test_collective_gpu.py"
+)
+for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
+  extra=""
+  [ "$tool" = memcheck ] && extra="--leak-check no --check-device-heap yes"
+  [ "$tool" = racecheck ] && extra="--racecheck-report all"
+  log=gpurun_out/sanitizer/$tool.log
+  : > $log
+  for t in "${TESTS[@]}"; do
+    echo "=== $t" >> $log
+    timeout ${SAN_TIMEOUT:-900} compute-sanitizer --tool $tool $extra --kernel-name kns=3pdg \
+      --print-limit 50 --error-exitcode 99 \
+      python -m pytest -q -x -p no:cacheprovider "$t" >> $log 2>&1
+    echo "exit $?" >> $log
+  done
+done
+echo done
