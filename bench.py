@@ -128,8 +128,9 @@ def init_nccl(local: int):
 
 def bench_config(n, b, world):
     """`config` of the headline line (identical in both arms)."""
-    return {"workload": "config2: full re-score = MC demand engine (n=512, bit-exact vs "
-                        "reference) + 256-bucket Gittins + global order",
+    return {"workload": "config2: full re-score = attained service (_update_attained) + MC "
+                        "demand engine (n=512, bit-exact vs reference) + 256-bucket Gittins "
+                        "+ global order",
             "apps_per_gpu": n, "bins": b, "samples_per_app": N_SAMP,
             "records_per_unit": N_REC, "units_per_graph": 8, "visit_cap": VISIT_CAP,
             "queue": f"tools/synth.py make({n}, {N_REC}, seed={SEED_WORLD}+rank), "
@@ -148,16 +149,41 @@ def reachable_units(u: int) -> int:
     return {0: 8, 1: 7, 2: 6, 3: 5, 4: 5, 5: 5, 6: 2, 7: 1}[int(u)]
 
 
+NOW = 10000.0          # simulated clock of the re-score
+
+
 def ages_for(rng, n, mean_rem, max_rem):
-    """est_age (attained service at the estimate) and age now: served since the
-    estimate ~ U(0, 0.9) x E[remaining]; 1% forced exhausted.
-    Element-wise in the inputs, so a sample of apps gets the same ages as in
-    the full queue."""
+    """_update_attained's inputs (simcore.py:306-313) per app: completed
+    service (= est_age, the attained service at the estimate), the current
+    unit's progress and one active task (start, cold delay, service; start NaN
+    = not started).  Served since the estimate ~ U(0, 0.9) x E[remaining]; 1%
+    forced exhausted.  Element-wise in the inputs, so a sample of
+    apps gets the same values as in the full queue.  Returns (est, age,
+    columns); age is the attained service the device computes from them,
+    evaluated here with the reference's operation order."""
     est = rng.uniform(0.0, 200.0, n)
-    age = est + rng.uniform(0.0, 0.9, n) * mean_rem
+    served = rng.uniform(0.0, 0.9, n) * mean_rem
     ex = rng.random(n) < 0.01
-    age[ex] = est[ex] + 1.01 * max_rem[ex]
-    return est, age
+    served[ex] = 1.01 * max_rem[ex]
+    progress = served * rng.uniform(0.0, 1.0, n)
+    cold = np.where(rng.random(n) < 0.5, 0.0, rng.uniform(0.0, 5.0, n))
+    start = NOW - served - cold
+    start[(rng.random(n) < 0.2) & ~ex] = np.nan
+    service = served * rng.uniform(1.0, 1.5, n)
+    cols = {"completed": est, "progress": progress, "start": start, "cold": cold,
+            "service": service}
+    return est, attained(cols), cols
+
+
+def attained(c):
+    """completed + max(progress, min(service, max(0, now - (start + cold)))),
+    as Simulator._update_attained evaluates it (one task per app)."""
+    with np.errstate(invalid="ignore"):
+        x = NOW - (c["start"] + c["cold"])
+        run = np.where(x > 0.0, x, 0.0)
+        v = np.where(run < c["service"], run, c["service"])
+        prog = np.where(~np.isnan(c["start"]) & (v > c["progress"]), v, c["progress"])
+    return c["completed"] + prog
 
 
 def hist_mean_max(lo, width, k, counts, n_samp=N_SAMP):
@@ -266,10 +292,10 @@ def _c2_init(apps):
 
 
 def _c2_step(state, msg):
-    """("first",) -> first-estimate stats; ("ages", {app: (est, age)});
-    ("step", salt) -> [(app, key)]: MC(n=512) + bucketize(256) + Gittins row
-    + overrun penalty on one core (sched.py:170-181, 244-318,
-    estimator.py:305-362)."""
+    """("first",) -> first-estimate stats; ("ages", {app: (completed, progress,
+    start, cold, service)}); ("step", salt) -> [(app, key)]: _update_attained
+    + MC(n=512) + bucketize(256) + Gittins row + overrun penalty on one core
+    (simcore.py:306-313, sched.py:170-181, 244-318, estimator.py:305-362)."""
     from oracle import pdg_oracle as O
     if msg[0] == "first":
         return state["first"]
@@ -280,7 +306,9 @@ def _c2_step(state, msg):
     salt = int(msg[1])
     out = []
     for a in state["apps"]:
-        est, age = state["ages"][a]
+        est, prog, start, cold, service = state["ages"][a]
+        age = O.update_attained([est], [prog], [] if start != start else
+                                [(0, start, cold, service)], NOW)[0]
         r = O.mc_remaining_demand(state["graphs"][a], f"s{st['unit'][a]}", [], N_SAMP,
                                   int(st["seed"][a]) + salt, VISIT_CAP)
         b = O.bucketize(r.samples.tolist(), st["bins"])
@@ -305,9 +333,11 @@ class Config2CPU:
         for part in self.workers.call(("first",)):
             for a, m, mx in part:
                 mean_rem[a], max_rem[a] = m, mx
-        est, age = ages_for(np.random.default_rng(SEED_AGES + rank), n_apps, mean_rem, max_rem)
+        est, age, cols = ages_for(np.random.default_rng(SEED_AGES + rank), n_apps, mean_rem,
+                                  max_rem)
         self.est, self.age = est, age
-        self.workers.call(("ages", {int(a): (float(est[a]), float(age[a])) for a in self.idx}))
+        self.workers.call(("ages", {int(a): tuple(float(cols[k][a]) for k in (
+            "completed", "progress", "start", "cold", "service")) for a in self.idx}))
 
     def step(self, salt):
         """One re-score of the sample + its (key, arrival) order: wall
@@ -351,7 +381,8 @@ def run_reference(args):
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": "port",
                          "sample": f"{m} of the {args.apps} apps of the queue the GPU arm "
                                    f"scores (rank-0 shard; same graphs, units, seeds + step "
-                                   f"salt, ages), oracle MC(n=512)+bucketize({args.bins})+"
+                                   f"salt, attained-service inputs), oracle _update_attained+"
+                                   f"MC(n=512)+bucketize({args.bins})+"
                                    f"Gittins+penalty+order on {procs} processes; ms_per_step "
                                    f"= measured wall time of the sample step",
                          "setup_s": t_setup},
@@ -536,11 +567,23 @@ def run_ours(args):
     mean_rem, max_rem = hist_mean_max(q.lo[:n].cpu().numpy(), q.width[:n].cpu().numpy(),
                                       q.nbins[:n].double().cpu().numpy(),
                                       q.counts[:n].double().cpu().numpy())
-    est, age = ages_for(np.random.default_rng(SEED_AGES + rank), n, mean_rem, max_rem)
+    est, age, cols = ages_for(np.random.default_rng(SEED_AGES + rank), n, mean_rem, max_rem)
     q.est_age[:n] = torch.from_numpy(est).to(dev)
-    q.age[:n] = torch.from_numpy(age).to(dev)
     q.tiebreak[:n] = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int32, device=dev)
     q.n = n
+    # the scheduler's per-app attained-service inputs (one running task per
+    # app), resident; every step recomputes q.age from them (a11b)
+    att = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in cols.items()}
+    t_app = torch.arange(n, dtype=torch.int32, device=dev)
+    t_active = torch.ones(n, dtype=torch.uint8, device=dev)
+
+    def update_age():
+        q.update_attained(att["completed"], att["progress"], t_app, t_active, att["start"],
+                          att["cold"], att["service"], NOW)
+
+    update_age()
+    torch.cuda.synchronize()
+    assert np.array_equal(q.age[:n].cpu().numpy(), age), "attained service differs"
 
     stream = torch.cuda.current_stream()
     gathered = torch.empty(world * n, dtype=torch.int64, device=dev)
@@ -557,6 +600,7 @@ def run_ours(args):
 
     def step(salt, record=False):
         torch.add(seeds0, salt, out=seeds)                  # fresh estimate seeds
+        update_age()                                        # _update_attained, all apps
         if record:
             e0, e1, e2 = ev(), ev(), ev()
             e0.record(stream)
@@ -632,7 +676,7 @@ def run_ours(args):
     # back the global order and the keys
     h_unit = torch.from_numpy(jb["unit"]).pin_memory()
     h_seed = torch.from_numpy(jb["seed"]).pin_memory()
-    h_age = torch.from_numpy(age).pin_memory()
+    h_cols = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in cols.items()}
     h_est = torch.from_numpy(est).pin_memory()
     h_order = torch.empty(world * n, dtype=torch.int32).pin_memory()
     h_keys = torch.empty(n, dtype=torch.float32).pin_memory()
@@ -640,7 +684,8 @@ def run_ours(args):
     def e2e_step(salt):
         u_idx.copy_(h_unit, non_blocking=True)
         seeds0.copy_(h_seed, non_blocking=True)
-        q.age[:n].copy_(h_age, non_blocking=True)
+        for k, v in h_cols.items():
+            att[k].copy_(v, non_blocking=True)
         q.est_age[:n].copy_(h_est, non_blocking=True)
         step(salt)
         h_order.copy_(out_slots, non_blocking=True)
@@ -661,13 +706,16 @@ def run_ours(args):
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_tot, e2e_p50 = max_over_ranks([np.sum(e2e_ms), np.median(e2e_ms)], world, dev)
     e2e_ms_step = e2e_tot / args.steps
-    h2d = h_unit.numel() * 4 + h_seed.numel() * 8 + h_age.numel() * 8 + h_est.numel() * 8
+    h2d = h_unit.numel() * 4 + h_seed.numel() * 8 + h_est.numel() * 8 + \
+        sum(v.numel() * 8 for v in h_cols.values())
     e2e = {"value": world * n / (e2e_ms_step / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(h_order.numel() * 4 + h_keys.numel() * 4),
            "ms_per_step": e2e_ms_step, "p50_latency_ms": e2e_p50,
-           "path": "pinned host queue state -> DemandEngine.run + HistQueue.score + "
-                   "pdg_order -> pinned host order/keys (wall clock, synchronized)"}
+           "path": "pinned host queue state (units, seeds, estimate ages, attained-service "
+                   "inputs) -> HistQueue.update_attained + DemandEngine.run + "
+                   "HistQueue.score + pdg_order -> pinned host order/keys (wall clock, "
+                   "synchronized)"}
 
     # ---- roofline of the dominant kernel (the engine) ----------------------
     reach = np.array([reachable_units(u) for u in jb["unit"]])
@@ -724,8 +772,9 @@ def run_ours(args):
         line["cpu_baseline"] = {
             "value": len(cpu.idx) / cpu_dt, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{len(cpu.idx)} of the {n} apps of this queue (evenly strided; same "
-                      f"graphs, units, seeds, ages, step salt {SALT_TIMED}), oracle "
-                      f"MC(n=512)+bucketize({b})+Gittins row+penalty, 1 process",
+                      f"graphs, units, seeds, attained-service inputs, step salt {SALT_TIMED}), "
+                      f"oracle _update_attained+MC(n=512)+bucketize({b})+Gittins row+penalty, "
+                      f"1 process",
             "sample_wall_s": cpu_dt,
             "keys_max_rel_err_vs_gpu": float(rel.max())}
     del w
@@ -740,6 +789,7 @@ def run_ours(args):
         line["config1_refresh_latency"] = bench_refresh_latency()
         line["config1_simulation"] = bench_config1_sim()
         line["k1_refresh_1m"] = bench_k1_large(dev)
+        line["config2_llm"] = bench_llm(dev, cpu_sample=0 if args.no_cpu_baseline else 200)
         del eng, q
         torch.cuda.empty_cache()
         line["config4_stream"] = bench_stream(dev, cpu=not args.no_cpu_baseline)
@@ -944,6 +994,63 @@ def bench_k1_large(dev, n=1_000_000, reps=20):
             "apps_per_s": n / (ms / 1e3),
             "roofline": {"bound": "hbm", "bytes_per_app": nbytes, "achieved": ach,
                          "peak": peak, "unit": "GB/s", "frac": ach / peak}}
+
+
+# ---------------------------------------------------------------------------
+# config 2, LLM variant: the engine on depth-8 templates mixing LLM units,
+# own-input units and upstream-conditioned (K3) units, 3 in 4 apps conditioned
+# on an observation (mc_walk_kernel<7>; estimator.py:236-302, 305-362)
+# ---------------------------------------------------------------------------
+
+def bench_llm(dev, n_apps=100_000, templates=256, reps=10, cpu_sample=200):
+    import torch
+    from oracle import pdg_oracle as O
+    from paper_2506_14851_b200.estimator import DemandEngine
+    from paper_2506_14851_b200.graphs import graph_from_kb
+    from paper_2506_14851_b200.queue import HistQueue
+    from tools import synth
+    docs = synth.llm_docs(templates, 200, seed=2027)
+    eng = DemandEngine({k: graph_from_kb(v) for k, v in docs.items()}, device=str(dev))
+    q = synth.llm_queue(docs, n_apps, seed=9)
+    jobs = synth.llm_jobs(eng, q, dev)
+    hq = HistQueue(n_apps, N_BINS)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        res = eng.run(*jobs, n=N_SAMP, bucket_count=N_BINS, visit_cap=VISIT_CAP, queue=hq)
+    torch.cuda.synchronize()
+    fl = res["flags"].cpu().numpy()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        eng.run(*jobs, n=N_SAMP, bucket_count=N_BINS, visit_cap=VISIT_CAP, queue=hq)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    out = {"workload": f"config2-llm: {n_apps} apps over {templates} depth-8 templates "
+                       "(LLM, own-input and K3-conditioned units; tools/synth.llm_docs), "
+                       "MC n=512 + 256-bucket rows", "apps": n_apps,
+           "engine_ms": ms, "apps_per_s": n_apps / (ms / 1e3),
+           "conditioned_frac": float((fl & 1).mean()),
+           "replayed_serial": int(((fl & 4) != 0).sum()),
+           "bank_features": int(eng.bank.features)}
+    if cpu_sample:
+        og = {k: O.graph_from_kb(v) for k, v in docs.items()}
+        idx = np.linspace(0, n_apps - 1, cpu_sample).astype(int)
+        t0 = time.perf_counter()
+        for a in idx:
+            o = q["obs"][a]
+            obs = [] if o is None else [O.OObs(o[0], o[1], o[2], o[3])]
+            r = O.mc_remaining_demand(og[q["names"][q["graph"][a]]], f"s{q['unit'][a]}", obs,
+                                      N_SAMP, int(q["seed"][a]), VISIT_CAP)
+            O.bucketize(r.samples.tolist(), N_BINS)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": len(idx) / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                               "sample": f"{len(idx)} evenly strided apps of this queue, oracle "
+                                         "MC(n=512, conditioned)+bucketize(256)"}
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -86,3 +86,26 @@ def test_full_size_queue_properties():
     r = np.where(np.isnan(r), ag * 2.0, r)
     got = key.cpu().numpy()[sel].astype(np.float64)
     assert np.max(np.abs(got - r) / np.maximum(r, 1e-30)) < 1e-5
+
+
+def test_llm_workload_sample_bit_exact():
+    """The LLM / own-input / K3 depth-8 workload (bench's config2_llm section):
+    a random sample of apps, conditioned on upstream observations, is
+    bit-identical to the oracle."""
+    from paper_2506_14851_b200.estimator import DemandEngine
+    from paper_2506_14851_b200.graphs import graph_from_kb
+    docs = synth.llm_docs(12, 200, seed=5)
+    eng = DemandEngine({k: graph_from_kb(v) for k, v in docs.items()})
+    q = synth.llm_queue(docs, 400, seed=6)
+    res = eng.run(*synth.llm_jobs(eng, q, eng.device), n=512, bucket_count=256, samples=True)
+    S = res["samples"].cpu().numpy()
+    fl = res["flags"].cpu().numpy()
+    assert (fl & 1).sum() > 20                               # conditioned apps present
+    og = {k: O.graph_from_kb(v) for k, v in docs.items()}
+    for a in np.random.default_rng(1).choice(400, 150, replace=False):
+        o = q["obs"][a]
+        obs = [] if o is None else [O.OObs(o[0], o[1], o[2], o[3])]
+        want = O.mc_remaining_demand(og[q["names"][q["graph"][a]]], f"s{q['unit'][a]}", obs,
+                                     512, int(q["seed"][a]))
+        np.testing.assert_array_equal(S[a], want.samples)
+        assert bool(fl[a] & 1) == want.conditioned

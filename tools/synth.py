@@ -153,3 +153,110 @@ def events(graphs: dict, q: dict, n_events: int, seed: int = 7):
         obs[e] = (r.input_len, r.output_len, float(r.parallelism))
     return {"app": apps, "completed": q["unit"][apps].copy(), "next": nxt, "obs": obs,
             "seed": rng.integers(0, 2**62, n_events).astype(np.int64)}
+
+
+# ---------------------------------------------------------------------------
+# config-2 LLM variant: depth-8 templates mixing LLM, own-input and
+# upstream-conditioned (K3) units, as knowledge-base documents
+# ---------------------------------------------------------------------------
+
+# s0 plan (LLM) -> s1 retrieve (docker) -> {s2 draft | s3 refine | s4 tool};
+# s2 draft (LLM, output ~ own input, self-loop) -> {s2 | s3};
+# s3 refine (LLM, input ~ upstream output) -> s4 tool (dnn) -> s5 verify
+# (LLM, output ~ upstream output) -> {s3 back edge | s6}; s6 run (docker) ->
+# s7 report (LLM, output ~ own input) -> end
+LLM_KINDS = ["llm", "docker", "llm", "llm", "dnn", "llm", "docker", "llm"]
+LLM_MASKS = {2: {"output_own_input": True}, 3: {"input_upstream_output": True},
+             5: {"output_upstream_output": True}, 7: {"output_own_input": True}}
+
+
+def llm_docs(n_templates: int, n_trials: int = 200, seed: int = 2027) -> dict:
+    """n_templates KB documents with the synth topology.  Every trial writes
+    one record per unit (same trial_id across units, so K3 joins records);
+    LLM lengths are lognormal, the masked dependencies are real correlations
+    (own input -> output, upstream output -> input / output)."""
+    rng = np.random.default_rng(seed)
+    docs = {}
+    for t in range(n_templates):
+        T = n_trials
+        p_self, p_back = rng.uniform(0.3, 0.6), rng.uniform(0.2, 0.4)
+        split = rng.dirichlet([1.0, 1.0, 1.0])
+        ln = lambda m, s, size=T: np.exp(np.log(m) - s * s / 2 + s * rng.standard_normal(size))  # noqa: E731
+        inp = np.zeros((U, T))
+        out = np.zeros((U, T))
+        dur = np.zeros((U, T))
+        for u in range(U):
+            if LLM_KINDS[u] == "llm":
+                inp[u] = ln(rng.uniform(300, 3000), 0.5)
+                out[u] = ln(rng.uniform(100, 900), 0.5)
+            else:
+                dur[u] = ln(rng.uniform(1.0, 40.0), 0.5)
+        out[2] = inp[2] * rng.uniform(0.2, 0.5) * ln(1.0, 0.15)       # own input
+        inp[3] = out[2] * rng.uniform(1.0, 2.0) + ln(200.0, 0.3)        # upstream output
+        out[5] = out[3] * rng.uniform(0.3, 0.8) * ln(1.0, 0.2)          # upstream output
+        out[7] = inp[7] * rng.uniform(0.1, 0.4) * ln(1.0, 0.15)         # own input
+        nxt = np.full((U, T), -1)
+        nxt[0] = 1
+        r = rng.random(T)
+        nxt[1] = 2 + (r >= split[0]) + (r >= split[0] + split[1])
+        nxt[2] = np.where(rng.random(T) < p_self, 2, 3)
+        nxt[3], nxt[4] = 4, 5
+        nxt[5] = np.where(rng.random(T) < p_back, 3, 6)
+        nxt[6] = 7
+        nxt[1, :3], nxt[2, :2], nxt[5, :2] = [2, 3, 4], [2, 3], [3, 6]
+        units = []
+        for u in range(U):
+            kind = LLM_KINDS[u]
+            backend = ({"kind": "llm-inference", "model_id": "base-7b", "warmup_time": 0.0}
+                       if kind == "llm" else
+                       {"kind": "docker-exec", "image_id": f"img-{t}-{u}", "warmup_time": 15.0}
+                       if kind == "docker" else
+                       {"kind": "dnn-tool", "tool_id": f"tool-{t}-{u}", "warmup_time": 8.0})
+            recs = [{"trial_id": k, "input_len": float(inp[u, k]), "output_len": float(out[u, k]),
+                     "parallelism": 1, "duration": float(dur[u, k]),
+                     "next_unit": UNIT_IDS[nxt[u, k]] if nxt[u, k] >= 0 else None}
+                    for k in range(T)]
+            units.append({"unit_id": UNIT_IDS[u], "backend": backend, "records": recs,
+                          "masks": dict(LLM_MASKS.get(u, {})), "capacity": 1000,
+                          "bucket_count": 16})
+        docs[f"llm8-{t}"] = {"app_id": f"llm8-{t}", "entry_unit": "s0", "units": units}
+    return docs
+
+
+def llm_queue(docs: dict, n_apps: int, seed: int = 9):
+    """n_apps instances: template, current unit, and (for 3 in 4 apps) an
+    observation of a recorded upstream execution of the current unit."""
+    rng = np.random.default_rng(seed)
+    names = list(docs)
+    gi = rng.integers(0, len(names), n_apps).astype(np.int32)
+    ui = rng.integers(0, U, n_apps).astype(np.int32)
+    obs = []
+    for a in range(n_apps):
+        doc = docs[names[gi[a]]]
+        cur = UNIT_IDS[ui[a]]
+        ups = [u for u in doc["units"]
+               if any(r["next_unit"] == cur for r in u["records"])] if rng.random() < 0.75 else []
+        if ups:
+            up = ups[rng.integers(0, len(ups))]
+            r = up["records"][rng.integers(0, len(up["records"]))]
+            obs.append((up["unit_id"], r["input_len"], r["output_len"], r["parallelism"]))
+        else:
+            obs.append(None)
+    return {"names": names, "graph": gi, "unit": ui, "obs": obs,
+            "seed": rng.integers(0, 2**62, n_apps).astype(np.int64)}
+
+
+def llm_jobs(eng, q: dict, device):
+    """Device job arrays for DemandEngine.run from llm_queue(): graph, unit,
+    seed, conditioning upstream (local index, -1 = none) and its values."""
+    import torch
+    names, n = q["names"], len(q["graph"])
+    ou = np.full(n, -1, dtype=np.int32)
+    ov = np.zeros((n, 3))
+    gidx = np.array([eng.bank.index[nm] for nm in names], dtype=np.int32)
+    for a, o in enumerate(q["obs"]):
+        if o is not None:
+            ou[a] = eng.bank.local_unit(names[q["graph"][a]], o[0])
+            ov[a] = o[1:]
+    t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(device)  # noqa: E731
+    return (t(gidx[q["graph"]]), t(q["unit"]), t(q["seed"]), t(ou), t(ov))
