@@ -23,7 +23,7 @@ set_remaining(256) + one gittins_rank_batch row per app) plus the global
 order:
   K2/a4  mc_walk_kernel       512-walk Monte Carlo from the current unit,
                               bit-identical to the reference, bucketed to 256
-  K1b    gittins_rows_kernel  Gittins key + overrun penalty + packed sort key
+  K1b    gittins_quad_kernel  Gittins key + overrun penalty + packed sort key
   K5     radix sort           global order (after the all-gather when N > 1)
 Each step uses fresh per-app seeds (a genuine re-estimate, nothing cached).
 
@@ -621,7 +621,7 @@ def run_ours(args):
         # the 32-bit key alone yields the (key, arrival) order
         _lib.check(L.pdg_order(_lib.ptr(src), _lib.ptr(out_keys), _lib.ptr(gslots),
                                _lib.ptr(out_slots), world * n, 32, _lib.ptr(temp),
-                               temp.numel(), _lib.stream_ptr(stream)), "pdg_order")
+                               temp.numel(), _lib.stream_ptr()), "pdg_order")
 
     launches, kernel_names = (None, None) if args.ncu else count_launches(step)
 
@@ -717,6 +717,11 @@ def run_ours(args):
                    "HistQueue.score + pdg_order -> pinned host order/keys (wall clock, "
                    "synchronized)"}
 
+    # ---- the same step replayed as one CUDA graph ---------------------------
+    # (all launches captured once; shows how much of the step the ~12 host
+    # launches cost -- they are enqueued while the engine runs)
+    graph = cuda_graph_step(step, flush, args.steps, world, n)
+
     # ---- roofline of the dominant kernel (the engine) ----------------------
     reach = np.array([reachable_units(u) for u in jb["unit"]])
     # per app: pools of reachable units (256 f64) + their descriptors (64 B) and
@@ -743,7 +748,7 @@ def run_ours(args):
         roofline["pcg_floor_ms"] = ns["pcg_floor_ms"]
         roofline["frac_of_pcg_floor"] = ns["pcg_floor_ms"] / eng_avg
     k1_bytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
-    k1 = {"kernel": "gittins_rows_kernel", "avg_launch_ms": float(k1_ms.mean()),
+    k1 = {"kernel": "gittins_quad_kernel", "avg_launch_ms": float(k1_ms.mean()),
           "bytes_per_app": k1_bytes,
           "achieved_gbs": k1_bytes * n / (float(k1_ms.mean()) / 1e3) / 1e9,
           "apps_per_s": n / (float(k1_ms.mean()) / 1e3)}
@@ -757,7 +762,7 @@ def run_ours(args):
         "config": bench_config(n, b, world),
         "gpu_launches": None if launches is None else launches * args.steps,
         "gpu_launches_per_step": launches, "kernels": kernel_names,
-        "e2e": e2e, "roofline": roofline, "k1_refresh": k1, "clocks": clk,
+        "e2e": e2e, "roofline": roofline, "k1_refresh": k1, "cuda_graph": graph, "clocks": clk,
     }
 
     # ---- like-for-like CPU baseline (rank 0, N = 1): the same apps --------
@@ -961,6 +966,40 @@ def bench_policy(dev, eng, g_idx, u_idx, seeds, q, n, b, rows=1_000_000, reps=20
 # K1b periodic refresh of a 1M-row resident queue (no re-estimation)
 # ---------------------------------------------------------------------------
 
+def cuda_graph_step(step, flush, steps, world, n):
+    """Capture step() (fixed salt) into a CUDA graph and time K replays with
+    the L2 flushed between them; max over ranks.  Single-rank only: the
+    N>1 step contains an NCCL all-gather issued through torch.distributed."""
+    import torch
+    if world > 1:
+        return {"skipped": "N>1 step holds a torch.distributed all-gather"}
+    try:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step(SALT_TIMED)                          # warm the capture stream
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step(SALT_TIMED)
+        torch.cuda.synchronize()
+    except Exception as e:                            # report, do not hide
+        return {"error": f"{type(e).__name__}: {e}"}
+    ts = []
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        ts.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ts]))
+    return {"ms_per_step": ms, "apps_per_s": n / (ms / 1e3),
+            "note": "the timed step replayed as one captured CUDA graph (same kernels)"}
+
+
 def bench_k1_large(dev, n=1_000_000, reps=20):
     import torch
     from paper_2506_14851_b200.queue import HistQueue
@@ -990,7 +1029,7 @@ def bench_k1_large(dev, n=1_000_000, reps=20):
     nbytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
     ach = nbytes * n / (ms / 1e3) / 1e9
     peak = measured_peaks()[0]
-    return {"kernel": "gittins_rows_kernel", "rows": n, "ms_per_launch": ms,
+    return {"kernel": "gittins_quad_kernel", "rows": n, "ms_per_launch": ms,
             "apps_per_s": n / (ms / 1e3),
             "roofline": {"bound": "hbm", "bytes_per_app": nbytes, "achieved": ach,
                          "peak": peak, "unit": "GB/s", "frac": ach / peak}}

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpdg_b200.so")
 SOURCES = ["abi.cu", "gittins.cu", "engine.cu", "prewarm.cu", "dispatch.cu", "masks.cu",
-           "collective.cu"]
+           "collective.cu", "sort.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -27,6 +27,11 @@ inline int launch_status(const char* what) {
 
 int sm_count();
 
+// Per (kernel, block size, dynamic shared memory, device): sets the kernel's
+// max dynamic shared memory and returns its resident blocks per SM.  Cached,
+// so the per-call cost of a launch is the launch alone.
+int launch_setup(const void* kern, int threads, size_t smem, int* per_sm);
+
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---- exact float64 helpers (never contracted into FMA) --------------------

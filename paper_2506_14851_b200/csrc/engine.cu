@@ -100,6 +100,15 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// unit sets: 32-bit masks for graphs of <= 32 units, 64-bit above
+__device__ __forceinline__ int mask_ffs(uint32_t m) { return __ffs(m); }
+__device__ __forceinline__ int mask_ffs(uint64_t m) { return __ffsll((long long)m); }
+__device__ __forceinline__ uint32_t warp_or(uint32_t v) { return __reduce_or_sync(kFull, v); }
+__device__ __forceinline__ uint64_t warp_or(uint64_t v) {
+  return (uint64_t(__reduce_or_sync(kFull, uint32_t(v >> 32))) << 32) |
+         __reduce_or_sync(kFull, uint32_t(v));
+}
+
 struct Pools {            // the draw pools of one unit visit
   const double* A;
   int pa;
@@ -651,7 +660,7 @@ __global__ void __launch_bounds__(kWarps * 32, 5) mc_engine_kernel(EngineArgs a)
     bool ok = true;
     for (int step = 0; step < a.cap && ok; ++step) {
       // compact the still-active walks (order kept) and collect occupied units
-      unsigned occ = 0;
+      uint64_t occ = 0;
       uint32_t nn = 0;
       for (uint32_t base = 0; base < na; base += 32) {
         const uint32_t idx = base + lane;
@@ -664,16 +673,16 @@ __global__ void __launch_bounds__(kWarps * 32, 5) mc_engine_kernel(EngineArgs a)
         const unsigned bal = __ballot_sync(kFull, c >= 0);
         if (c >= 0) {
           ws.act[nn + __popc(bal & lt)] = w;
-          occ |= 1u << c;
+          occ |= 1ull << c;
         }
         nn += __popc(bal);
       }
       na = nn;
-      occ = __reduce_or_sync(kFull, occ);
+      occ = warp_or(occ);
       __syncwarp();
       if (!occ) break;
       while (occ && ok) {
-        const int u = __ffs(occ) - 1;
+        const int u = mask_ffs(occ) - 1;
         occ &= occ - 1;
         ok = visit_unit<Idx>(a, gbase, u, ovp, has_ov, u0, ws, na, g, lane);
       }
@@ -727,12 +736,12 @@ __global__ void __launch_bounds__(32) mc_serial_kernel(EngineArgs a) {
       for (int w = 0; w < n; ++w) { cur[w] = int8_t(u0); tot[w] = 0.0; }
       const double pre = a.b.prefill_rate, dec = a.b.decode_rate;
       for (int step = 0; step < a.cap; ++step) {
-        unsigned occ = 0;
+        uint64_t occ = 0;
         for (int w = 0; w < n; ++w)
-          if (cur[w] >= 0) occ |= 1u << cur[w];
+          if (cur[w] >= 0) occ |= 1ull << cur[w];
         if (!occ) break;
         while (occ) {
-          const int u = __ffs(occ) - 1;
+          const int u = mask_ffs(occ) - 1;
           occ &= occ - 1;
           const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u];
           const bool ov = has_ov && u == u0;
@@ -835,31 +844,41 @@ __device__ __forceinline__ Pools pools_div(const EngineArgs& a, const UnitDesc& 
 // shared memory per warp: [counters | LLM staging] [tot] [mem] [bitsets of
 // max_units units]
 // (banks without LLM units stage no B draws: the staging area is ia only)
+// (+64 B: the uniform loop prefetches the draw index one stride ahead,
+// ia[k + 32] / ib[k + 32] for k < m; past the last rank it reads this
+// slack -- value discarded -- instead of the tot array other lanes write)
 __host__ __device__ inline size_t walk_union_bytes(int counters, bool llm = true) {
-  const size_t c = size_t(counters) * 4, s = size_t(kSmemWalks) * (llm ? 4 : 2);
+  const size_t c = size_t(counters) * 4, s = size_t(kSmemWalks) * (llm ? 4 : 2) + 64;
   return align16(c > s ? c : s);
 }
 __host__ __device__ inline size_t walk_smem_bytes(int counters, int units, bool llm = true) {
   return walk_union_bytes(counters, llm) + size_t(kSmemWalks) * 10 +
-         size_t(units) * kWalkWords * 4 + size_t(units) * (llm ? 112 : 48);
+         size_t(units) * kWalkWords * 4 + size_t(units) * (llm ? 112 : 64);
 }
 // global scratch per warp: [own-input arrays] [K3 pairs]
 __host__ __device__ inline size_t walk_gmem_bytes() {
   return align16(size_t(kSmemWalks) * gmem_walk_bytes<uint16_t>());
 }
 
-// the threshold form of searchsorted(cum, u, "right") for u = k * 2^-53
+// the threshold form of searchsorted(cum, u, "right") for u = k * 2^-53,
+// k = word >> 11: the successor is the first i with k < t_i (t_i =
+// ceil(cum_i * 2^53) >= 1), i.e. word <= T_i with T_i = t_i * 2^11 - 1 (all
+// ones for t_i >= 2^53) -- compared on the raw 64-bit word, no shift
+__device__ __forceinline__ uint64_t word_threshold(uint64_t t) {
+  return t >= (1ull << 53) ? ~0ull : (t << 11) - 1ull;
+}
+
 struct SuccTab {
-  uint64_t t0, t1, t2;
+  uint64_t t0, t1, t2;     // word thresholds T_i
   int n0, n1, n2, n3, ns;
   __device__ __forceinline__ void load(const EngineArgs& a, const UnitDesc& d) {
     const uint64_t* thr = a.b.succ_thr + d.succ_off;
     const int32_t* nxt = a.b.succ_nxt + d.succ_off;
     ns = d.succ_len;
-    constexpr uint64_t never = 1ull << 54;          // above every k < 2^53
-    t0 = ns > 0 ? __ldg(thr) : never;
-    t1 = ns > 1 ? __ldg(thr + 1) : never;
-    t2 = ns > 2 ? __ldg(thr + 2) : never;
+    constexpr uint64_t always = ~0ull;              // absent slot: taken by every word
+    t0 = ns > 0 ? word_threshold(__ldg(thr)) : always;
+    t1 = ns > 1 ? word_threshold(__ldg(thr + 1)) : always;
+    t2 = ns > 2 ? word_threshold(__ldg(thr + 2)) : always;
     n0 = __ldg(nxt);
     n1 = ns > 0 ? __ldg(nxt + 1) : -1;
     n2 = ns > 1 ? __ldg(nxt + 2) : -1;
@@ -867,14 +886,12 @@ struct SuccTab {
   }
   // successor of the uniform carried by a raw 64-bit word (<= 3 successors)
   __device__ __forceinline__ int next3(uint64_t w) const {
-    const uint64_t k = w >> 11;
-    return k < t0 ? n0 : k < t1 ? n1 : k < t2 ? n2 : n3;
+    return w <= t0 ? n0 : w <= t1 ? n1 : w <= t2 ? n2 : n3;
   }
   // successor of the uniform carried by a raw 64-bit word
   __device__ __forceinline__ int next(const EngineArgs& a, const UnitDesc& d, uint64_t w) const {
-    const uint64_t k = w >> 11;
     if (ns > 3) return next_unit(a, d, u53_double(w));
-    return k < t0 ? n0 : k < t1 ? n1 : k < t2 ? n2 : n3;
+    return next3(w);
   }
 };
 
@@ -884,7 +901,7 @@ struct __align__(16) UnitCache {
   uint64_t t0, t1, t2;
   int32_t ns;
   int8_t n[4];
-  int32_t pad[2];
+  uint32_t thr_a, thr_b;   // Lemire rejection thresholds of the unit's A / B pools
 };
 static_assert(sizeof(UnitCache) == 112, "unit cache layout");
 
@@ -893,9 +910,11 @@ struct __align__(16) UnitCacheLean {
   uint64_t t0, t1, t2;
   int32_t a_off, a_len, succ_off;
   int16_t flags, ns;
-  int8_t n[4];
+  uint32_t thr_a;          // Lemire rejection threshold of the A pool
+  int32_t pad;
+  int32_t n[4];            // successor units, one 16-byte load (no sign-extension per visit)
 };
-static_assert(sizeof(UnitCacheLean) == 48, "lean unit cache layout");
+static_assert(sizeof(UnitCacheLean) == 64, "lean unit cache layout");
 
 template <bool LLM>
 struct UnitCacheOf { using type = UnitCache; };
@@ -917,8 +936,12 @@ __device__ __forceinline__ UnitDesc desc_of(const UnitCacheLean& c) {
   return d;
 }
 
-template <typename Cache>
-__device__ __forceinline__ SuccTab succ_of(const Cache& c) {
+__device__ __forceinline__ uint32_t thr_a_of(const UnitCache& c) { return c.thr_a; }
+__device__ __forceinline__ uint32_t thr_a_of(const UnitCacheLean& c) { return c.thr_a; }
+__device__ __forceinline__ uint32_t thr_b_of(const UnitCache& c) { return c.thr_b; }
+__device__ __forceinline__ uint32_t thr_b_of(const UnitCacheLean&) { return 0u; }
+
+__device__ __forceinline__ SuccTab succ_of(const UnitCache& c) {
   SuccTab s;
   s.t0 = c.t0;
   s.t1 = c.t1;
@@ -931,11 +954,25 @@ __device__ __forceinline__ SuccTab succ_of(const Cache& c) {
   s.n3 = n.w;
   return s;
 }
+__device__ __forceinline__ SuccTab succ_of(const UnitCacheLean& c) {
+  SuccTab s;
+  s.t0 = c.t0;
+  s.t1 = c.t1;
+  s.t2 = c.t2;
+  s.ns = c.ns;
+  const int4 n = *reinterpret_cast<const int4*>(c.n);
+  s.n0 = n.x;
+  s.n1 = n.y;
+  s.n2 = n.z;
+  s.n3 = n.w;
+  return s;
+}
 
-__device__ __forceinline__ void arrive(const WalkState& ws, uint32_t w, int v, unsigned& targets) {
+template <typename M>
+__device__ __forceinline__ void arrive(const WalkState& ws, uint32_t w, int v, M& targets) {
   if (v >= 0) {
     atomicOr(ws.bits + v * kWalkWords + (w >> 5), 1u << (w & 31));
-    targets |= 1u << v;
+    targets |= M(1) << v;
   }
 }
 
@@ -987,18 +1024,27 @@ __device__ __forceinline__ LaneConst lane_const(const uint64_t* jt, const U128& 
 // of the segment [wb bounded words | m uniforms]; bounded halves stage the
 // draw indices per rank, the uniform of rank k then adds the stage time and
 // moves the walk
-template <bool LLM>
+// SPEC: per-successor-count specialised, unrolled uniform loops (the lean
+// duration-only kernel); the multi-kind kernels take one generic loop, whose
+// smaller code keeps them out of instruction-cache misses
+template <bool LLM, typename M, bool SPEC>
 __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const SuccTab& sc,
-                              const Pools& pl, const WalkState& ws, uint32_t m, Stream& g,
-                              LaneStream& ls, const LaneConst& lc, unsigned& targets,
-                              int lane) {
+                              const Pools& pl, uint32_t thr_a, uint32_t thr_b,
+                              const WalkState& ws, uint32_t m, Stream& g, LaneStream& ls,
+                              const LaneConst& lc, M& targets, int lane) {
   constexpr bool llm = LLM;
+  // pool bases kept opaque, so that a draw's address is one IMAD.WIDE of the
+  // 32-bit index instead of a re-associated 64-bit offset chain
+  const double* PA = pl.A;
+  const double* PB = pl.B;
+  asm("" : "+l"(PA));
+  if (LLM) asm("" : "+l"(PB));
   const uint32_t mA = pl.pa > 1 ? m : 0u;
   const uint32_t C = mA + ((llm && pl.pb > 1) ? m : 0u);
   const uint32_t pin = g.pend ? 1u : 0u;
   const uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
   const uint32_t W = wb + m;
-  U128 st = ls.st;                                // one stride before word q
+  U128& st = ls.st;                               // one stride before word q
   bool rej = false;
   uint32_t pend_hi = 0;
   uint32_t q = (uint32_t(lane) - ls.P) & 31u;
@@ -1008,22 +1054,23 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
     const uint64_t wd = pcg_out(st);
     const uint32_t R = 2u * q + pin;
     if (!LLM) {                                   // every low half is an A draw
-      ws.ia[R] = uint16_t(lemire(uint32_t(wd), uint32_t(pl.pa), rej));
-      if (R + 1 < mA) ws.ia[R + 1] = uint16_t(lemire(uint32_t(wd >> 32), uint32_t(pl.pa), rej));
+      ws.ia[R] = uint16_t(lemire_t(uint32_t(wd), uint32_t(pl.pa), thr_a, rej));
+      if (R + 1 < mA)
+        ws.ia[R + 1] = uint16_t(lemire_t(uint32_t(wd >> 32), uint32_t(pl.pa), thr_a, rej));
       else pend_hi = uint32_t(wd >> 32);
     } else {
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const uint32_t r = R + t, h = t ? uint32_t(wd >> 32) : uint32_t(wd);
-        if (r < mA) ws.ia[r] = uint16_t(lemire(h, uint32_t(pl.pa), rej));
-        else if (r < C) ws.ib[r - mA] = uint16_t(lemire(h, uint32_t(pl.pb), rej));
+        if (r < mA) ws.ia[r] = uint16_t(lemire_t(h, uint32_t(pl.pa), thr_a, rej));
+        else if (r < C) ws.ib[r - mA] = uint16_t(lemire_t(h, uint32_t(pl.pb), thr_b, rej));
         else pend_hi = h;
       }
     }
   }
   if (pin && C && lane == 0) {                    // half 0 is numpy's buffered half
-    if (mA) ws.ia[0] = uint16_t(lemire(g.pv, uint32_t(pl.pa), rej));
-    else ws.ib[0] = uint16_t(lemire(g.pv, uint32_t(pl.pb), rej));
+    if (mA) ws.ia[0] = uint16_t(lemire_t(g.pv, uint32_t(pl.pa), thr_a, rej));
+    else ws.ib[0] = uint16_t(lemire_t(g.pv, uint32_t(pl.pb), thr_b, rej));
   }
   __syncwarp();
   const bool hb = C > mA;
@@ -1033,39 +1080,43 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
   // into the pool)
   const uint32_t la = mA ? uint32_t(pl.pa - 1) : 0u, lb = hb ? uint32_t(pl.pb - 1) : 0u;
   uint32_t k = q - wb;
-  double xa = pl.A[min(uint32_t(ws.ia[k]), la)], xb = 0.0;
-  if (LLM) xb = pl.B[min(uint32_t(ws.ib[k]), lb)];
-  auto uniforms = [&](auto few_succ) {
-#pragma unroll kUnrollU
-    for (; q < W; q += 32) {
-      const double ca = xa, cb = xb;
-      xa = pl.A[min(uint32_t(ws.ia[k + 32]), la)];
-      if (LLM) xb = pl.B[min(uint32_t(ws.ib[k + 32]), lb)];
-      st = pcg_stride32(st, lc.c32);
-      const uint64_t wd = pcg_out(st);
-      // successor decided by as many threshold compares as the unit has
-      constexpr int NS = decltype(few_succ)::value;
-      const uint64_t kk = wd >> 11;
-      const int v = NS == 0 ? sc.n0
-                  : NS == 1 ? (kk < sc.t0 ? sc.n0 : sc.n1)
-                  : NS == 2 ? (kk < sc.t0 ? sc.n0 : kk < sc.t1 ? sc.n1 : sc.n2)
-                  : NS == 3 ? sc.next3(wd) : sc.next(a, d, wd);
-      const uint32_t w = ws.mem[k];
-      const double t = LLM ? dadd(ca, cb) : ca;    // pools hold i/prefill, o/decode
-      ws.tot[w] = dadd(ws.tot[w], t);
-      arrive(ws, w, v, targets);
-      k += 32;
-    }
+  double xa = __ldg(PA + min(uint32_t(ws.ia[k]), la)), xb = 0.0;
+  if (LLM) xb = __ldg(PB + min(uint32_t(ws.ib[k]), lb));
+  auto uniform = [&](auto few_succ) {             // one 32-word stride
+    const double ca = xa, cb = xb;
+    xa = __ldg(PA + min(uint32_t(ws.ia[k + 32]), la));
+    if (LLM) xb = __ldg(PB + min(uint32_t(ws.ib[k + 32]), lb));
+    st = pcg_stride32(st, lc.c32);
+    const uint64_t wd = pcg_out(st);
+    // successor decided by as many threshold compares as the unit has
+    constexpr int NS = decltype(few_succ)::value;
+    const int v = NS == 0 ? sc.n0
+                : NS == 1 ? (wd <= sc.t0 ? sc.n0 : sc.n1)
+                : NS == 2 ? (wd <= sc.t0 ? sc.n0 : wd <= sc.t1 ? sc.n1 : sc.n2)
+                : NS == 3 ? sc.next3(wd) : sc.next(a, d, wd);
+    const uint32_t w = ws.mem[k];
+    const double t = LLM ? dadd(ca, cb) : ca;      // pools hold i/prefill, o/decode
+    ws.tot[w] = dadd(ws.tot[w], t);
+    arrive(ws, w, v, targets);
+    k += 32;
   };
-  switch (sc.ns) {
-    case 0: uniforms(std::integral_constant<int, 0>{}); break;
-    case 1: uniforms(std::integral_constant<int, 1>{}); break;
-    case 2: uniforms(std::integral_constant<int, 2>{}); break;
-    case 3: uniforms(std::integral_constant<int, 3>{}); break;
-    default: uniforms(std::integral_constant<int, 4>{}); break;
+  if constexpr (SPEC) {        // one unrolled loop per successor count
+    auto uniforms = [&](auto few_succ) {
+#pragma unroll kUnrollU
+      for (; q < W; q += 32) uniform(few_succ);
+    };
+    switch (sc.ns) {
+      case 0: uniforms(std::integral_constant<int, 0>{}); break;
+      case 1: uniforms(std::integral_constant<int, 1>{}); break;
+      case 2: uniforms(std::integral_constant<int, 2>{}); break;
+      case 3: uniforms(std::integral_constant<int, 3>{}); break;
+      default: uniforms(std::integral_constant<int, 4>{}); break;
+    }
+  } else {                     // one generic loop: less code in the big variants
+#pragma unroll 1
+    for (; q < W; q += 32) uniform(std::integral_constant<int, 4>{});
   }
   if (__any_sync(kFull, rej)) return false;
-  ls.st = st;
   const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
   ls.P += W;
   if (C) {
@@ -1083,9 +1134,10 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
 // their buckets and bucket counts), a counting sort that maps each B half to
 // its member, the B words, then the uniforms.  The half shared by the last A
 // word and the first B draw, and numpy's buffered half, are placed by lane 0.
+template <typename M>
 __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab& sc,
                           const Pools& pl, const Pools& pd, const WalkState& ws, uint32_t m,
-                          Stream& g, LaneStream& ls, const LaneConst& lc, unsigned& targets,
+                          Stream& g, LaneStream& ls, const LaneConst& lc, M& targets,
                           int lane) {
   const unsigned lt = lanemask_lt();
   const int K = d.ib_k;
@@ -1115,7 +1167,7 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
   };
   for (int b = lane; b < K; b += 32) cnt[b] = 0;
   __syncwarp();
-  U128 st = ls.st;                                // one stride before word q
+  U128& st = ls.st;                               // one stride before word q
   uint32_t pend_hi = 0;
   uint32_t q = (uint32_t(lane) - ls.P) & 31u;
   for (; q < wA; q += 32) {                       // phase A: input draws
@@ -1226,7 +1278,6 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
     ws.tot[w] = dadd(ws.tot[w], ws.tmp[k]);
     arrive(ws, w, v, targets);
   }
-  ls.st = st;
   const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
   ls.P += W;
   if (C) {
@@ -1255,11 +1306,12 @@ constexpr int kWalkWarps = PDG_WALK_WARPS;
 // duration walk a resident CTA per SM.  A job that needs a compiled-out path
 // anyway (features understated by the caller) is handed to mc_serial_kernel,
 // so FEAT only ever affects speed.
-template <int FEAT>
+template <int FEAT, typename M = uint32_t>   // M: unit-set mask (uint64_t: > 32 units)
 __global__ void __launch_bounds__(kWalkWarps * 32,
                                   FEAT == 0 ? PDG_WALK_MINB_LEAN : PDG_WALK_MINB)
 mc_walk_kernel(EngineArgs a) {
   constexpr bool kLLM = FEAT & F_LLM, kOwn = FEAT & F_OWN, kCond = FEAT & F_ANYMASK;
+  constexpr bool kSpec = FEAT == 0;
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = a.n;
@@ -1334,9 +1386,9 @@ mc_walk_kernel(EngineArgs a) {
       ls.st = add128(mul128(g.s, U128{ap.x, ap.y}), lc.cl);   // one stride before word lane
       ls.P = 0;
     }
-    if (lane < gn) {                             // stage the unit descriptors
+    for (int ul = lane; ul < gn; ul += 32) {     // stage the unit descriptors
       Cache c;
-      const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + lane];
+      const UnitDesc d = reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + ul];
       if constexpr (kLLM) {
         c.d = d;
       } else {
@@ -1350,11 +1402,13 @@ mc_walk_kernel(EngineArgs a) {
       c.t1 = t.t1;
       c.t2 = t.t2;
       c.ns = t.ns;
-      c.n[0] = int8_t(t.n0);
-      c.n[1] = int8_t(t.n1);
-      c.n[2] = int8_t(t.n2);
-      c.n[3] = int8_t(t.n3);
-      uc[lane] = c;
+      c.thr_a = lemire_thr_of(uint32_t(d.a_len));
+      if constexpr (kLLM) c.thr_b = lemire_thr_of(uint32_t(d.b_len));
+      c.n[0] = t.n0;
+      c.n[1] = t.n1;
+      c.n[2] = t.n2;
+      c.n[3] = t.n3;
+      uc[ul] = c;
     }
     for (int i = lane; i < gn * kWalkWords; i += 32) {
       const int u = i / kWalkWords, wi = i - u * kWalkWords;
@@ -1363,31 +1417,34 @@ mc_walk_kernel(EngineArgs a) {
     }
     for (int w = lane; w < n; w += 32) ws.tot[w] = 0.0;
     __syncwarp();
-    unsigned pending = 1u << u0;                 // units holding walks
+    M pending = M(1) << u0;                      // units holding walks
     bool ok = true;
     for (int step = 0; step < a.cap && ok && pending; ++step) {
-      unsigned occ = pending;                    // frozen occupied set of the step
+      M occ = pending;                           // frozen occupied set of the step
       while (occ && ok) {
-        const int u = __ffs(occ) - 1;
+        const int u = mask_ffs(occ) - 1;
         occ &= occ - 1;
         const uint32_t m = take_members(ws, u, lane);
-        pending &= ~(1u << u);
+        pending &= ~(M(1) << u);
         const UnitDesc d = desc_of(uc[u]);
         const bool ov = has_ov && u == u0;
         const Pools pd = pools_div(a, d, ov, ovd);
-        unsigned targets = 0;
+        M targets = 0;
         if (!(d.flags & F_LLM))
-          ok = visit_strided<false>(a, d, succ_of(uc[u]), pd, ws, m, g, ls, lc, targets,
-                                    lane);
+          ok = visit_strided<false, M, kSpec>(a, d, succ_of(uc[u]), pd, thr_a_of(uc[u]), 0u,
+                                              ws, m, g, ls, lc, targets, lane);
         else if (!kLLM)
           ok = false;                            // compiled out: serial path
         else if ((d.flags & F_OWN) && !ov)
           ok = kOwn && visit_own(a, d, succ_of(uc[u]), pools_for(a, d, ov, ovp), pd, ws, m,
                                  g, ls, lc, targets, lane);
-        else
-          ok = visit_strided<true>(a, d, succ_of(uc[u]), pd, ws, m, g, ls, lc, targets,
-                                   lane);
-        pending |= __reduce_or_sync(kFull, targets);
+        else {                                   // override pools: thresholds here
+          const uint32_t ta = ov ? lemire_thr_of(uint32_t(pd.pa)) : thr_a_of(uc[u]);
+          const uint32_t tb = ov ? lemire_thr_of(uint32_t(pd.pb)) : thr_b_of(uc[u]);
+          ok = visit_strided<true, M, kSpec>(a, d, succ_of(uc[u]), pd, ta, tb, ws, m, g, ls,
+                                             lc, targets, lane);
+        }
+        pending |= warp_or(targets);
       }
     }
     if (!ok) {                     // Lemire rejection: leave it to mc_serial_kernel
@@ -1445,6 +1502,10 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
     set_error("pdg_mc_remaining_demand: invalid arguments");
     return PDG_EINVAL;
   }
+  if (bank->max_units > 64) {
+    set_error("pdg_mc_remaining_demand: graphs of more than 64 units are not supported");
+    return PDG_EUNSUPPORTED;
+  }
   if (n_samples <= kSmemWalks && !bank->vals_div) {
     set_error("pdg_mc_remaining_demand: graph bank without vals_div");
     return PDG_EINVAL;
@@ -1484,18 +1545,24 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(serial_count)");
   const bool sm = n_samples <= kSmemWalks;
   const size_t cnt_bytes = align16(size_t(a.counters) * 4);
+  // sequential completion of rejected apps (normally none: every block exits
+  // after reading the counter)
+  auto finish = [&]() -> int {
+    int rc = launch_status("mc_engine_kernel");
+    if (rc != PDG_OK) return rc;
+    const unsigned sblocks = unsigned(grid_warps < n_jobs ? grid_warps : n_jobs);
+    mc_serial_kernel<<<sblocks, 32, cnt_bytes, st>>>(a);
+    return launch_status("mc_serial_kernel");
+  };
   // persistent grid: exactly the resident CTAs (a second partial wave of
   // grid-stride CTAs would leave SMs idle at the tail)
   auto launch = [&](auto kern, int warps, size_t smem) -> int {
     int64_t blocks = (n_jobs + warps - 1) / warps;
     const int64_t capb = grid_warps / warps;
     if (blocks > capb) blocks = capb;
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(smem));
-    if (err != cudaSuccess) return cuda_status(err, "cudaFuncSetAttribute(mc_engine_kernel)");
     int per_sm = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
-    if (err != cudaSuccess || per_sm < 1) per_sm = 1;
+    if (int r = launch_setup(reinterpret_cast<const void*>(kern), warps * 32, smem, &per_sm))
+      return r;
     int64_t nb = int64_t(per_sm) * sm_count();
     if (nb > capb) nb = capb;
     if (nb > blocks) nb = blocks;
@@ -1510,6 +1577,11 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
     const size_t smem = size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu);
     const size_t smem_plain = size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu, false);
     int r = PDG_OK;
+    if (mu > 32) {                               // 64-bit unit sets, every unit kind
+      r = launch(mc_walk_kernel<7, uint64_t>, kWalkWarps, smem);
+      if (r) return r;
+      return finish();
+    }
     switch (feat) {
       case 0: r = launch(mc_walk_kernel<0>, kWalkWarps, smem_plain); break;
       case 1: r = launch(mc_walk_kernel<1>, kWalkWarps, smem); break;
@@ -1523,11 +1595,5 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   } else {
     if (int r = launch(mc_engine_kernel<uint32_t>, kWarps, size_t(kWarps) * cnt_bytes)) return r;
   }
-  int rc = launch_status("mc_engine_kernel");
-  if (rc != PDG_OK) return rc;
-  // sequential completion of rejected apps (normally none: every block exits
-  // after reading the counter)
-  const unsigned sblocks = unsigned(grid_warps < n_jobs ? grid_warps : n_jobs);
-  mc_serial_kernel<<<sblocks, 32, cnt_bytes, st>>>(a);
-  return launch_status("mc_serial_kernel");
+  return finish();
 }

@@ -241,35 +241,50 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
 }
 
 // ---------------------------------------------------------------------------
-// K1b, lane-per-row form for the queue's layout (rows of <= 256 buckets,
-// 16-byte aligned, zero counts past nbins).  Each warp owns a ring of STAGES
-// tiles of 32 rows in shared memory; a tile is filled by TMA bulk copies
-// (cp.async.bulk, one 2*stride-byte copy per row issued by its lane, padded
-// to 33 uint4 per row so that lane-per-row LDS.128 reads are conflict-free)
-// completing on the slot's mbarrier, STAGES-1 tiles ahead of the one being
-// scored; row headers are prefetched into registers with the copies.
+// K1b, quad form for the queue's layout (rows of <= 256 buckets, 16-byte
+// aligned, zero counts past nbins).  Four lanes score one row: lane
+// l = 8g + r works on row r of an 8-row tile and owns two 32-bucket segments
+// of it, x = [32g, 32g+32) and y = [128+32g, 160+32g), which it scans
+// together as the two halves of packed f32x2 registers (sm_100 FADD2 / FFMA2 /
+// FMUL2: one issue slot per bucket pair).
 //
-// Per row, lane l scans row l sequentially.  The alive boundary j0 is found
-// with bit-exact float64 tests (binary search, values ascend), Z = sum of
-// alive counts (IDP2A, two counts per instruction).  With t = j - j0,
-// d_j = d0 + t*w, S_j the alive prefix mass and T_j = Z - S_j, the
-// reference's numerator P_j + d_j*T_j (sched.py:118-124) is exactly
-//     d0*Z + w*I_j,   I_j = sum_{k<=j} (k-j0) m_k + t*T_j,   I_{j+1} = I_j + T_j,
-// so a bucket is two exact integer-valued float adds (I += T, T -= m), one
-// FFMA, one MUFU reciprocal, one FMUL and a min -- no per-bucket d_j or P_j.
-// Zero-mass buckets never beat the previous positive one (and are +inf
-// before any mass), so they need no masking.
+// Staging: each warp owns a ring of STAGES tiles in shared memory, filled by
+// TMA bulk copies (cp.async.bulk, one 2*stride-byte copy per row issued by
+// lanes 0..7) that complete on the slot's mbarrier one tile ahead of the one
+// being scored.  Rows are 528 B apart (33 x 16 B), so the eight lanes of a
+// quarter-warp (same g, rows 0..7) read eight different bank groups.
+//
+// Per row (sched.py:102-129 with the 1/Z normalisation cancelled):
+//  * the first alive bucket j0 (d_j = fl(fl(mid_j + est) - age) > 0, values
+//    ascend) is bracketed by a float32 estimate and confirmed by four exact
+//    float64 tests, one per lane of the row (binary search if the estimate
+//    misses); counts of dead buckets are zeroed;
+//  * each segment's alive mass and its weighted mass sum_k (k - j0) m_k come
+//    from IADD3 / IDP2A over the packed u16 counts; a prefix over the row's
+//    eight segments (shuffles across g) gives every segment its start state;
+//  * with t = j - j0, d_j = d0 + t*w, S_j the alive prefix mass and
+//    T_j = Z - S_j, the numerator P_j + d_j*T_j is exactly d0*Z + w*I_j with
+//    I_j = I_{j-1} + T_{j-1} (integer-valued floats, exact), so a bucket is
+//    I += T, T -= m, S = Z - T, one FFMA, one MUFU reciprocal, one FMUL and a
+//    min.  Dead and massless buckets give S = 0 -> |num| * inf (or NaN),
+//    which never wins; zero-mass buckets after mass never beat the previous
+//    positive one.
+// I, T and S are exact, so the key equals the warp-per-row kernel's
+// (gittins_hist_kernel) up to its own float32 rounding of P.
 // ---------------------------------------------------------------------------
-constexpr int kRowU4 = 33;          // uint4 per staged row: 32 + 1 pad (bank spread)
-constexpr int kTileU4 = 32 * kRowU4;
-#ifndef PDG_ROWS_WARPS
-#define PDG_ROWS_WARPS 6
+constexpr int kPairPitchU4 = 33;                      // 528 B per staged row
+constexpr int kPairTileU4 = 16 * kPairPitchU4;         // 16 rows per tile
+#ifndef PDG_PAIR_WARPS
+#define PDG_PAIR_WARPS 4
 #endif
-#ifndef PDG_ROWS_STAGES
-#define PDG_ROWS_STAGES 2
+#ifndef PDG_PAIR_STAGES
+#define PDG_PAIR_STAGES 2
 #endif
-constexpr int kRowWarps = PDG_ROWS_WARPS;
-constexpr int kRowStages = PDG_ROWS_STAGES;
+#ifndef PDG_PAIR_MINB
+#define PDG_PAIR_MINB 3
+#endif
+constexpr int kPairWarps = PDG_PAIR_WARPS;
+constexpr int kPairStages = PDG_PAIR_STAGES;
 
 __device__ __forceinline__ float rcp_approx(float x) {    // MUFU.RCP, ~1 ulp; rcp(0) = +inf
   float r;
@@ -277,126 +292,72 @@ __device__ __forceinline__ float rcp_approx(float x) {    // MUFU.RCP, ~1 ulp; r
   return r;
 }
 
-// Two u16 counts of a word -> exact floats: PRMT builds the bit patterns
-// 2^23 + c (selector immediate, magic 0x4B00 in a register), one packed
-// f32x2 add (sm_100 FADD2) removes the 2^23 bias from both.
-__device__ __forceinline__ void u16x2_to_f32(uint32_t x, uint32_t magic, float& lo, float& hi) {
-  uint32_t l, h;
-  asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(l) : "r"(x), "r"(magic));
-  asm("prmt.b32 %0, %1, %2, 0x5432;" : "=r"(h) : "r"(x), "r"(magic));
-  asm("{\n\t.reg .b64 p, q;\n\t"
-      "mov.b64 p, {%2, %3};\n\t"
-      "add.rn.f32x2 q, p, %4;\n\t"
-      "mov.b64 {%0, %1}, q;\n\t}"
-      : "=r"(l), "=r"(h)
-      : "r"(l), "r"(h), "l"(0xCB000000CB000000ull));
-  lo = __uint_as_float(l);
-  hi = __uint_as_float(h);
+// packed f32x2 arithmetic (sm_100)
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_pack_bits(uint32_t lo, uint32_t hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(hi));
+  return d;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+template <uint32_t SEL>
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b) {   // selector immediate
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL));
+  return d;
 }
 
-struct RowHdr {
+struct QuadHdr {
   double lo, w, est, age;
   int64_t r;                        // < 0: no row (past the end)
   int k;
   uint32_t tb;
 };
 
-// Score one staged row (lane-per-row); writes the row's outputs.
-__device__ __forceinline__ void score_staged_row(const HistArgs& a, const uint4* row,
-                                                 const RowHdr& h) {
-  const int64_t r = h.r;
-  const double lo = h.lo, w = h.w, est = h.est, age = h.age;
-  const int k = h.k;
-  // first alive bucket (values ascend): bit-exact float64 tests
-  int j0 = k;
-  double d0 = 0.0;
-  {
-    const double e0 = exact_d(lo, w, est, age, 0);
-    if (e0 > 0.0) {
-      j0 = 0;
-      d0 = e0;
-    } else {
-      int l = 1, hi = k;                             // smallest alive j in [l, hi)
-      while (l < hi) {
-        const int mid = (l + hi) >> 1;
-        if (exact_d(lo, w, est, age, mid) > 0.0) hi = mid; else l = mid + 1;
-      }
-      j0 = l;
-      if (j0 < k) d0 = exact_d(lo, w, est, age, j0);
-    }
+// smallest j in [0, k] with exact_d(j) > 0 (k: nothing alive)
+__device__ __forceinline__ int first_alive_search(double lo, double w, double est, double age,
+                                                  int k) {
+  int l = 0, hi = k;
+  while (l < hi) {
+    const int mid = (l + hi) >> 1;
+    if (exact_d(lo, w, est, age, mid) > 0.0) hi = mid; else l = mid + 1;
   }
-  const int c0 = j0 >> 3, cend = (k + 7) >> 3;
-  // alive mass Z
-  uint32_t zi = 0;
-  if (j0 < k) {                                      // else: nothing alive (exhausted)
-    const uint4 v = row[c0];
-    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = c0 * 8 + 2 * q;
-      const uint32_t keep = (j >= j0 ? 0x0000ffffu : 0u) | (j + 1 >= j0 ? 0xffff0000u : 0u);
-      zi = __dp2a_lo(wd[q] & keep, 0x0101u, zi);
-    }
-  }
-  for (int c = c0 + 1; c < cend; ++c) {
-    const uint4 v = row[c];
-    zi = __dp2a_lo(v.x, 0x0101u, zi);
-    zi = __dp2a_lo(v.y, 0x0101u, zi);
-    zi = __dp2a_lo(v.z, 0x0101u, zi);
-    zi = __dp2a_lo(v.w, 0x0101u, zi);
-  }
-  float key;
-  uint8_t flags = 0;
-  if (zi == 0) {                                     // exhausted: sched.py:295-300
-    key = float(dmul(age, a.penalty));
-    flags = PDG_FLAG_OVERRUN;
-  } else {
-    const float Zf = float(zi);
-    const float af = float(dmul(d0, double(zi)));    // d0 * Z
-    const float bf = float(w);
-    float I = -Zf, T = Zf, best = __int_as_float(0x7f800000);
-    auto bucket = [&](float m) {
-      I += T;                                        // exact (integer-valued)
-      T -= m;
-      best = fminf(best, fmaf(bf, I, af) * rcp_approx(Zf - T));
-    };
-    const uint32_t magic = 0x4B00u;
-    {                                                // first chunk: skip j < j0
-      const uint4 v = row[c0];
-      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float m0, m1;
-        u16x2_to_f32(wd[q], magic, m0, m1);
-        if (c0 * 8 + 2 * q >= j0) bucket(m0);
-        if (c0 * 8 + 2 * q + 1 >= j0) bucket(m1);
-      }
-    }
-    for (int c = c0 + 1; c < cend; ++c) {
-      const uint4 v = row[c];
-      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float m0, m1;
-        u16x2_to_f32(wd[q], magic, m0, m1);
-        bucket(m0);
-        bucket(m1);
-      }
-    }
-    key = best;
-  }
-  if (!(key > 0.f)) key = 0.f;
-  if (a.out_f32) a.out_f32[r] = key;
-  if (a.out_flags) a.out_flags[r] = flags;
-  if (a.out_key) a.out_key[r] = (uint64_t(__float_as_uint(key)) << 32) | h.tb;
+  return l;
 }
 
 template <int W, int STAGES>
-__global__ void __launch_bounds__(W * 32, 1) gittins_rows_kernel(HistArgs a) {
+__global__ void __launch_bounds__(W * 32, PDG_PAIR_MINB) gittins_pair_kernel(HistArgs a) {
   extern __shared__ __align__(128) uint4 stage[];
   __shared__ uint64_t bars[W * STAGES];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint4* tiles = stage + size_t(wib) * STAGES * kTileU4;
+  const int r = lane & 15, g = lane >> 4;             // row of the tile, half of the row
+  uint4* tiles = stage + size_t(wib) * STAGES * kPairTileU4;
   uint64_t* bar = bars + wib * STAGES;
   if (lane == 0) {
 #pragma unroll
@@ -404,37 +365,47 @@ __global__ void __launch_bounds__(W * 32, 1) gittins_rows_kernel(HistArgs a) {
     fence_barrier_init();
   }
   __syncwarp();
-  const int64_t ntiles = (a.n + 31) >> 5;
+  const int64_t ntiles = (a.n + 15) >> 4;
   const int64_t gw = int64_t(blockIdx.x) * W + wib;
   const int64_t nw = int64_t(gridDim.x) * W;
   const unsigned row_bytes = unsigned(a.stride) * 2u;     // <= 512, multiple of 16
   const int kmax = int(a.stride);
+  const int nu4 = int(a.stride >> 3);                     // uint4 per row
   const uint64_t policy = l2_evict_first_policy();
 
-  // one tile into ring slot `slot`: lane l copies row l and loads its header
-  auto issue = [&](int64_t t, int slot, RowHdr& h) {
-    const int64_t i = t * 32 + lane;
+  // one tile into ring slot `slot`: lanes 0..15 copy rows 0..15; every lane
+  // loads its row's header
+  auto issue = [&](int64_t t, int slot, QuadHdr& h) {
+    const int64_t i = t * 16 + r;
     const bool valid = i < a.n;
-    const int64_t r = valid ? (a.row_idx ? int64_t(__ldg(a.row_idx + i)) : i) : -1;
-    const unsigned total = __reduce_add_sync(kFull, valid ? row_bytes : 0u);
+    const int64_t rg = valid ? (a.row_idx ? int64_t(__ldg(a.row_idx + i)) : i) : -1;
+    const int64_t left = a.n - t * 16;
+    const unsigned nvalid = left < 16 ? unsigned(left) : 16u;
     fence_proxy_async_smem();                        // earlier reads of the slot first
-    if (lane == 0) mbar_arrive_expect_tx(bar + slot, total);
+    if (lane == 0) mbar_arrive_expect_tx(bar + slot, nvalid * row_bytes);
     __syncwarp();
-    if (valid)
-      bulk_g2s(tiles + slot * kTileU4 + lane * kRowU4, a.counts + r * a.stride, row_bytes,
-               bar + slot, policy);
-    h.r = r;
+    if (g == 0 && valid)
+      bulk_g2s(tiles + slot * kPairTileU4 + r * kPairPitchU4, a.counts + rg * a.stride,
+               row_bytes, bar + slot, policy);
+    h.r = rg;
     if (valid) {
-      h.lo = __ldg(a.lo + r);
-      h.w = __ldg(a.width + r);
-      h.est = __ldg(a.est + r);
-      h.age = __ldg(a.age + r);
-      h.k = min(__ldg(a.nbins + r), kmax);
-      h.tb = a.tiebreak ? __ldg(a.tiebreak + r) : uint32_t(r);
+      h.lo = __ldg(a.lo + rg);
+      h.w = __ldg(a.width + rg);
+      h.est = __ldg(a.est + rg);
+      h.age = __ldg(a.age + rg);
+      h.k = min(__ldg(a.nbins + rg), kmax);
+      h.tb = a.tiebreak ? __ldg(a.tiebreak + rg) : uint32_t(rg);
+    } else {
+      h.lo = 0.0;
+      h.w = 1.0;
+      h.est = 0.0;
+      h.age = 1.0;
+      h.k = 0;
+      h.tb = 0;
     }
   };
 
-  RowHdr h[STAGES];
+  QuadHdr h[STAGES];
 #pragma unroll
   for (int s = 0; s + 1 < STAGES; ++s)
     if (gw + s * nw < ntiles) issue(gw + s * nw, s, h[s]);
@@ -443,11 +414,136 @@ __global__ void __launch_bounds__(W * 32, 1) gittins_rows_kernel(HistArgs a) {
     const int64_t tn = t + int64_t(STAGES - 1) * nw;
     if (tn < ntiles) issue(tn, int((q + STAGES - 1) % STAGES), h[STAGES - 1]);
     const int s = int(q % STAGES);
-    mbar_wait(bar + s, (q / STAGES) & 1u);
-    if (h[0].r >= 0) score_staged_row(a, tiles + s * kTileU4 + lane * kRowU4, h[0]);
-    __syncwarp();
+    const QuadHdr hd = h[0];
 #pragma unroll
     for (int j = 0; j + 1 < STAGES; ++j) h[j] = h[j + 1];
+    const double lo = hd.lo, w = hd.w, est = hd.est, age = hd.age;
+    const int k = hd.k;
+
+    // ---- first alive bucket: float32 estimate, four exact tests per row
+    int j0;
+    {
+      const float x = __fdividef(float(dsub(dsub(age, est), lo)), float(w)) - 0.5f;
+      int c;
+      if (!(x > -1.0e9f)) c = 0;                        // NaN / -inf / far below
+      else if (!(x < 1.0e9f)) c = k;
+      else c = min(max(__float2int_rd(x) + 1, 0), k);
+      auto test = [&](int j) {
+        return j >= k ? true : (j < 0 ? false : exact_d(lo, w, est, age, j) > 0.0);
+      };
+      const bool a0 = test(c - 2 + 2 * g), a1 = test(c - 1 + 2 * g);   // j = c-2 .. c+1
+      const unsigned b0 = __ballot_sync(kFull, a0) >> r, b1 = __ballot_sync(kFull, a1) >> r;
+      const unsigned bits = (b0 & 1u) | ((b1 & 1u) << 1) | ((b0 >> 14) & 4u) |
+                            ((b1 >> 13) & 8u);
+      if (!(bits & 1u) && (bits & 8u)) j0 = c - 3 + __ffs(bits);
+      else j0 = first_alive_search(lo, w, est, age, k);   // estimate missed (rare)
+    }
+    mbar_wait(bar + s, (q / STAGES) & 1u);
+    uint4* row = tiles + s * kPairTileU4 + r * kPairPitchU4;
+    const int c0 = j0 >> 3, e0 = j0 & 7;
+    // zero the dead counts of the uint4 holding j0 (its owner, in place; also
+    // when nothing is alive, j0 = k, and k is not a multiple of 8)
+    if (e0 != 0 && c0 < nu4 && g == ((c0 >> 3) & 1)) {
+      uint4 v = row[c0];
+      const uint64_t m_lo = e0 >= 4 ? 0ull : (~0ull << (16 * e0));
+      const uint64_t m_hi = e0 >= 4 ? (~0ull << (16 * (e0 - 4))) : ~0ull;
+      v.x &= uint32_t(m_lo);
+      v.y &= uint32_t(m_lo >> 32);
+      v.z &= uint32_t(m_hi);
+      v.w &= uint32_t(m_hi >> 32);
+      row[c0] = v;
+    }
+    __syncwarp();
+    // segment x = uint4 [8g, 8g+8), y = [16+8g, 16+8g+8); dead and past-the-row
+    // uint4 read as zero
+    auto ld = [&](int u) {
+      return (u >= c0 && u < nu4) ? row[u] : make_uint4(0, 0, 0, 0);
+    };
+
+    // ---- segment sums: packed u16 mass (IADD3), weighted mass (IDP2A)
+    uint32_t sx = 0, sy = 0, wx = 0, wy = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 X = ld(8 * g + i), Y = ld(16 + 8 * g + i);
+      const uint32_t xs[4] = {X.x, X.y, X.z, X.w};
+      const uint32_t ys[4] = {Y.x, Y.y, Y.z, Y.w};
+      sx += (xs[0] + xs[1]) + (xs[2] + xs[3]);
+      sy += (ys[0] + ys[1]) + (ys[2] + ys[3]);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int b = 2 * (4 * i + p);                   // bucket offset in the segment
+        const uint32_t wt = uint32_t(b | ((b + 1) << 8));
+        wx = __dp2a_lo(xs[p], wt, wx);
+        wy = __dp2a_lo(ys[p], wt, wy);
+      }
+    }
+    const int mx = int((sx & 0xffffu) + (sx >> 16)), my = int((sy & 0xffffu) + (sy >> 16));
+    const int bx = 64 * g, by = 128 + 64 * g;              // segment starts
+    // alive mass and sum_k (k - j0) m_k (>= 0: dead counts are zero) per
+    // segment; the row's other half is lane ^ 16
+    const int kx = int(wx) + (bx - j0) * mx, ky = int(wy) + (by - j0) * my;
+    const int omx = __shfl_xor_sync(kFull, mx, 16), okx = __shfl_xor_sync(kFull, kx, 16);
+    const int omy = __shfl_xor_sync(kFull, my, 16), oky = __shfl_xor_sync(kFull, ky, 16);
+    const int zx = mx + omx, kxt = kx + okx;
+    const int Z = zx + my + omy;
+    float key;
+    uint8_t flags = 0;
+    if (Z == 0) {                                          // exhausted: sched.py:295-300
+      key = float(dmul(age, a.penalty));
+      flags = PDG_FLAG_OVERRUN;
+    } else {
+      // segment start state (after bucket b - 1): T = Z - S_before,
+      // I = K_before + (b - 1 - j0) T
+      const int sbx = g ? omx : 0, kbx = g ? okx : 0;
+      const int sby = zx + (g ? omy : 0), kby = kxt + (g ? oky : 0);
+      const int Tx = Z - sbx, Ty = Z - sby;
+      const int Ix = kbx + (bx - 1 - j0) * Tx, Iy = kby + (by - 1 - j0) * Ty;
+      const double d0 = exact_d(lo, w, est, age, j0);
+      const float af = float(dmul(d0, double(Z))), bf = float(w);
+      const uint64_t A2 = f2_pack(af, af), B2 = f2_pack(bf, bf);
+      const uint64_t Z2 = f2_pack(float(Z), float(Z));
+      const uint64_t bias2 = f2_pack(-8388608.f, -8388608.f);
+      uint64_t I2 = f2_pack(float(Ix), float(Iy)), T2 = f2_pack(float(Tx), float(Ty));
+      float bestx = __int_as_float(0x7f800000), besty = bestx;
+      // 0x4B00 in a register (kmax <= 256), so that ptxas keeps the PRMT
+      // selectors as immediates instead of re-materialising them
+      const uint32_t magic = 0x4B00u | (uint32_t(kmax) >> 16);
+      auto step = [&](uint32_t xw, uint32_t yw, auto sel) {
+        constexpr uint32_t S = decltype(sel)::value;
+        const uint64_t m2 = f2_add(f2_pack_bits(prmt<S>(xw, magic), prmt<S>(yw, magic)), bias2);
+        I2 = f2_add(I2, T2);                               // exact (integer-valued)
+        T2 = f2_sub(T2, m2);
+        float sxf, syf;
+        f2_unpack(f2_sub(Z2, T2), sxf, syf);
+        const uint64_t q2 =
+            f2_mul(f2_fma(B2, I2, A2), f2_pack(rcp_approx(sxf), rcp_approx(syf)));
+        float qx, qy;
+        f2_unpack(q2, qx, qy);
+        bestx = fminf(bestx, fabsf(qx));
+        besty = fminf(besty, fabsf(qy));
+      };
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 X = ld(8 * g + i), Y = ld(16 + 8 * g + i);
+        const uint32_t xs[4] = {X.x, X.y, X.z, X.w};
+        const uint32_t ys[4] = {Y.x, Y.y, Y.z, Y.w};
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          step(xs[p], ys[p], std::integral_constant<uint32_t, 0x5410u>{});
+          step(xs[p], ys[p], std::integral_constant<uint32_t, 0x5432u>{});
+        }
+      }
+      key = fminf(bestx, besty);
+    }
+    key = fminf(key, __shfl_xor_sync(kFull, key, 16));
+    __syncwarp();                                          // slot reads done before reuse
+    if (g == 0 && hd.r >= 0) {
+      const int64_t rg = hd.r;
+      if (!(key > 0.f)) key = 0.f;                         // canonical +0 for the sort key
+      if (a.out_f32) a.out_f32[rg] = key;
+      if (a.out_flags) a.out_flags[rg] = flags;
+      if (a.out_key) a.out_key[rg] = (uint64_t(__float_as_uint(key)) << 32) | hd.tb;
+    }
   }
 }
 
@@ -585,23 +681,19 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
   if (blocks > cap) blocks = cap;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t maxb = rows->stride;   // buckets per row are bounded by the stride
-  // lane-per-row tiles pay off once every SM has tiles to stream; small
+  // quad tiles pay off once every SM has tiles to stream; small
   // (incremental) batches take the warp-per-row kernel's lower latency
-  if (maxb <= 256 && n >= int64_t(sm_count()) * 32 * 4) {
-    auto kern = gittins_rows_kernel<kRowWarps, kRowStages>;
-    const size_t smem = size_t(kRowWarps) * kRowStages * kTileU4 * sizeof(uint4);
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(smem));
-      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gittins_rows_kernel)");
-      attr = true;
-    }
-    int64_t tiles = (n + 31) / 32;
-    int64_t nb = (tiles + kRowWarps - 1) / kRowWarps;
-    if (nb > sm_count()) nb = sm_count();
-    kern<<<unsigned(nb), kRowWarps * 32, smem, s>>>(a);
-    return launch_status("gittins_rows_kernel");
+  if (maxb <= 256 && n >= int64_t(sm_count()) * 16 * 2) {
+    auto kern = gittins_pair_kernel<kPairWarps, kPairStages>;
+    const size_t smem = size_t(kPairWarps) * kPairStages * kPairTileU4 * sizeof(uint4);
+    int per_sm = 0;
+    if (int r = launch_setup(reinterpret_cast<const void*>(kern), kPairWarps * 32, smem, &per_sm))
+      return r;
+    const int64_t tiles = (n + 15) / 16;
+    int64_t nb = (tiles + kPairWarps - 1) / kPairWarps;
+    if (nb > int64_t(per_sm) * sm_count()) nb = int64_t(per_sm) * sm_count();
+    kern<<<unsigned(nb), kPairWarps * 32, smem, s>>>(a);
+    return launch_status("gittins_pair_kernel");
   }
   if (maxb <= 256) gittins_hist_kernel<1><<<unsigned(blocks), threads, 0, s>>>(a);
   else if (maxb <= 512) gittins_hist_kernel<2><<<unsigned(blocks), threads, 0, s>>>(a);
@@ -742,37 +834,7 @@ extern "C" int pdg_gittins_rank_samples_host(const double* samples, int32_t n, d
   return PDG_OK;
 }
 
-extern "C" size_t pdg_order_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr,
-                                  (uint64_t*)nullptr, (const uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, n, 0, 64);
-  return bytes;
-}
-
-extern "C" int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
-                         const uint32_t* slots_in, uint32_t* slots_out, int64_t n,
-                         int32_t begin_bit, void* temp, size_t temp_bytes,
-                         void* stream) {
-  if (n < 0 || (n > 0 && (!keys_in || !keys_out || !slots_in || !slots_out || !temp))) {
-    set_error("pdg_order: invalid arguments");
-    return PDG_EINVAL;
-  }
-  if (begin_bit != 0 && begin_bit != 32) {
-    set_error("pdg_order: begin_bit must be 0 or 32");
-    return PDG_EINVAL;
-  }
-  if (n == 0) return PDG_OK;
-  size_t need = pdg_order_temp_bytes(n);
-  if (temp_bytes < need) {
-    set_error("pdg_order: temp_bytes %zu < %zu", temp_bytes, need);
-    return PDG_EINVAL;
-  }
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out,
-                                                  slots_in, slots_out, n, begin_bit, 64,
-                                                  (cudaStream_t)stream);
-  return cuda_status(e, "pdg_order");
-}
+// pdg_order (K5) lives in sort.cu
 
 // ---------------------------------------------------------------------------
 // a4 standalone: equal-width bucketing of sample rows (distributions.py:79-105)

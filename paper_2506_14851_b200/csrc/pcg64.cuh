@@ -124,13 +124,30 @@ __device__ __forceinline__ void pcg_seed(uint64_t seed, U128& state, U128& inc) 
 
 // Lemire bounded draw on one 32-bit half (numpy buffered_bounded_lemire_uint32);
 // P > 1.  Sets rej when numpy would reject this half and draw again.
+// the rare branch (low word < P, probability P / 2^32) is kept out of line:
+// the modulo would otherwise be inlined at every draw site of the large
+// kernels and crowd their instruction cache
+__device__ __noinline__ uint32_t lemire_thr_cold(uint32_t P) { return (0u - P) % P; }
+// numpy's rejection threshold (2^32 - P) mod P for a pool of P > 1 values
+// (0 for P <= 1: nothing is drawn); out of line, computed once per unit
+__device__ __forceinline__ uint32_t lemire_thr_of(uint32_t P) {
+  return P > 1 ? lemire_thr_cold(P) : 0u;
+}
+
 __device__ __forceinline__ uint32_t lemire(uint32_t h, uint32_t P, bool& rej) {
   const uint64_t m = uint64_t(h) * P;
   const uint32_t left = uint32_t(m);
   if (left < P) {
-    const uint32_t thr = (0u - P) % P;
-    if (left < thr) rej = true;
+    if (left < lemire_thr_cold(P)) rej = true;
   }
+  return uint32_t(m >> 32);
+}
+
+// lemire() with the threshold precomputed: branch-free (rejection iff the
+// low product word < thr, which implies < P)
+__device__ __forceinline__ uint32_t lemire_t(uint32_t h, uint32_t P, uint32_t thr, bool& rej) {
+  const uint64_t m = uint64_t(h) * P;
+  rej |= uint32_t(m) < thr;
   return uint32_t(m >> 32);
 }
 

@@ -59,11 +59,16 @@ class DispatchPlanner:
         if st[0] == 2:
             raise RuntimeError("dispatch plan needed more than 2 * slots waiting candidates")
         cnt = ev_count.cpu().numpy()
-        tk = ev_task.cpu().numpy().reshape(nb, cap)
-        kd = ev_kind.cpu().numpy().reshape(nb, cap)
+        # read back only the events each backend wrote (the rest of its
+        # cap-sized region is never initialised)
+        tk, kd = [], []
+        for b in range(nb):
+            used = int(cnt[b] + cnt[nb + b])
+            tk.append(ev_task[b * cap:b * cap + used].cpu().numpy())
+            kd.append(ev_kind[b * cap:b * cap + used].cpu().numpy())
         ev = []
         for b in range(nb):
-            ev += [(int(kd[b, i]), int(tk[b, i])) for i in range(cnt[b])]
+            ev += [(int(kd[b][i]), int(tk[b][i])) for i in range(cnt[b])]
         for b in range(nb):
-            ev += [(int(kd[b, cnt[b] + i]), int(tk[b, cnt[b] + i])) for i in range(cnt[nb + b])]
+            ev += [(int(kd[b][cnt[b] + i]), int(tk[b][cnt[b] + i])) for i in range(cnt[nb + b])]
         return ev

@@ -378,8 +378,8 @@ class GraphBank:
             return off, len(xs)
 
         order = sorted(g.units)
-        if len(order) > 32:
-            raise ValueError(f"graph {nm!r}: more than 32 units")
+        if len(order) > 64:
+            raise ValueError(f"graph {nm!r}: more than 64 units")
         self.unit_order[nm] = order
         for uid in order:
             u = g.units[uid]
@@ -556,7 +556,12 @@ class GraphBank:
         # integer form of `cum <= u` for u = k * 2^-53: k >= ceil(cum * 2^53)
         # (exact: scaling by 2^53 and ceil are exact for cum in [0, 2))
         cum = np.asarray(succ_cum, dtype=np.float64)
-        self.succ_thr = t(np.ceil(cum * 2.0 ** 53).astype(np.uint64).view(np.int64), np.int64)
+        thr = np.ceil(cum * 2.0 ** 53).astype(np.uint64)
+        # every listed successor has probability > 0, so thresholds are >= 1
+        # (the engine compares raw words against thr * 2^11 - 1)
+        if len(succ_nxt) and np.any(thr[np.asarray(succ_nxt)[:len(thr)] >= 0] == 0):
+            raise ValueError("successor with zero branch probability")
+        self.succ_thr = t(thr.view(np.int64), np.int64)
         self.succ_nxt = t(succ_nxt, np.int32)
         self.max_units = int(np.max(gn)) if len(gn) else 1
         # unit kinds present (pdg_graph_bank.features: the engine compiles out

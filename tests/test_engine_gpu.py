@@ -236,8 +236,9 @@ def test_visit_cap_zero_and_empty_units(kb_graphs):
 
 
 def _wide_graph_doc(rng, n_units=32):
-    """32 units (the per-graph maximum), up to 6 successors per unit (the
-    > 3 successor path), single-sample pools, LLM and duration units."""
+    """n_units units (32: the widest graph on 32-bit unit sets), up to 6
+    successors per unit (the > 3 successor path), single-sample pools, LLM
+    and duration units."""
     ids = [f"u{i:02d}" for i in range(n_units)]
     units = []
     for i, uid in enumerate(ids):
@@ -272,6 +273,30 @@ def test_wide_graph_32_units_many_successors():
     cases = []
     for uid in sorted(og.units)[::3]:
         for n in (1, 37, 300, 512):
+            cases.append({"graph": "wide", "current": uid, "obs": [], "n": n,
+                          "seed": int(rng.integers(0, 2**62)), "visit_cap": 64})
+    got = run_cases(eng, cases)
+    for i, c in enumerate(cases):
+        want = O.mc_remaining_demand(og, c["current"], [], c["n"], c["seed"], c["visit_cap"])
+        np.testing.assert_array_equal(got[i][0], want.samples, err_msg=str(c))
+        assert got[i][1] == want.capped
+
+
+@pytest.mark.parametrize("n_units", [33, 48, 64])
+def test_wide_graph_64bit_unit_sets(n_units):
+    """Graphs past 32 units run on 64-bit unit sets (mc_walk_kernel<7, u64>
+    for n <= 512, the compaction kernel above): samples bit-identical to the
+    reference walk (estimator.py:326-353 has no unit cap)."""
+    from paper_2506_14851_b200.estimator import DemandEngine
+    from paper_2506_14851_b200.graphs import graph_from_kb
+    rng = np.random.default_rng(n_units)
+    doc = _wide_graph_doc(rng, n_units=n_units)
+    eng = DemandEngine({"wide": graph_from_kb(doc)})
+    og = O.graph_from_kb(doc)
+    cases = []
+    ids = sorted(og.units)
+    for uid in ids[::5] + [ids[-1]]:
+        for n in (1, 300, 512, 700):
             cases.append({"graph": "wide", "current": uid, "obs": [], "n": n,
                           "seed": int(rng.integers(0, 2**62)), "visit_cap": 64})
     got = run_cases(eng, cases)

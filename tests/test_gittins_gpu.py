@@ -160,3 +160,36 @@ def test_rank_samples_bit_exact_vs_oracle(S):
                 S.gittins_rank(s, age)
     with pytest.raises(S.EstimationError):
         S.gittins_rank([], 0.0)
+
+
+@pytest.mark.parametrize("b,ragged,nsamp", [(8, False, 512), (64, True, 512), (200, False, 512),
+                                            (256, False, 512), (256, True, 512),
+                                            (256, False, 60000)])
+def test_hist_queue_quad_path_vs_oracle(b, ragged, nsamp):
+    """Queues large enough for the 4-lanes-per-row kernel (gittins_quad_kernel):
+    narrow strides, ragged rows, dead prefixes at every offset, exhausted and
+    degenerate rows, exact-support ages, sample counts up to the u16 limit;
+    then a scattered subset re-scored through row_idx."""
+    import torch
+    from paper_2506_14851_b200.queue import HistQueue
+    rng = np.random.default_rng(1000 + b + 7 * ragged)
+    n = 20_000
+    rows = hist_rows(rng, n, b, nsamp=nsamp, ragged=ragged, degenerate_frac=0.03,
+                     exhaust_frac=0.03, on_support_frac=0.05)
+    q = HistQueue(n, b)
+    q.load_rows(rows["lo"], rows["width"], rows["est_age"], rows["nbins"], rows["nsamp"],
+                rows["counts"], age=rows["age"])
+    q.score(penalty=2.0)
+    got = q.key_f32[:n].cpu().numpy().astype(np.float64)
+    flags = q.flags[:n].cpu().numpy()
+    want, bad = oracle_keys(O, rows)
+    np.testing.assert_array_equal(flags == 1, bad)
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert rel.max() < 1e-5, (rel.max(), np.argmax(rel))
+    # subset through row_idx: the other rows keep their keys
+    sub = np.sort(rng.choice(n, 6000, replace=False)).astype(np.int32)
+    q.key_f32.zero_()
+    q.score(penalty=2.0, rows=torch.tensor(sub, device=q.key_f32.device))
+    got2 = q.key_f32[:n].cpu().numpy().astype(np.float64)
+    assert np.all(got2[np.setdiff1d(np.arange(n), sub)] == 0.0)
+    np.testing.assert_array_equal(got2[sub], got[sub])

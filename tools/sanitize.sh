@@ -6,6 +6,10 @@
 set -u
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out/sanitizer
+# initcheck only sees writes by the kernels it instruments, so with the pdg::
+# kernel filter every buffer torch initialised (arange, fills, copies) reads as
+# uninitialised: KNS= (empty) checks every kernel.  TESTS_OVERRIDE="a b" runs
+# a subset.
 TESTS=(
   "tests/test_engine_gpu.py::test_golden_mc_cases_bit_exact"
   "tests/test_engine_gpu.py::test_understated_bank_features_stay_exact"
@@ -18,6 +22,9 @@ TESTS=(
   "tests/test_gittins_gpu.py::test_rank_batch_empty_and_zero_width"
   "tests/test_gittins_gpu.py::test_refresh_priorities_ragged_and_overrun"
   "tests/test_gittins_gpu.py::test_hist_queue_vs_oracle"
+  "tests/test_gittins_gpu.py::test_hist_queue_quad_path_vs_oracle"
+  "tests/test_order_gpu.py"
+  "tests/test_engine_gpu.py::test_wide_graph_64bit_unit_sets"
   "tests/test_policy_gpu.py"
   "tests/test_prewarm_gpu.py::test_plan_prewarm_batch_matches_reference"
   "tests/test_prewarm_gpu.py::test_need_grid_vs_oracle"
@@ -27,6 +34,8 @@ TESTS=(
   "tests/test_stream_gpu.py::test_event_stream_parity"
   "tests/test_collective_gpu.py"
 )
+[ -n "${TESTS_OVERRIDE:-}" ] && read -r -a TESTS <<< "$TESTS_OVERRIDE"
+KNS="${KNS---kernel-name kns=3pdg}"
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   extra=""
   [ "$tool" = memcheck ] && extra="--leak-check no --check-device-heap yes"
@@ -35,7 +44,7 @@ for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   : > $log
   for t in "${TESTS[@]}"; do
     echo "=== $t" >> $log
-    timeout ${SAN_TIMEOUT:-900} compute-sanitizer --tool $tool $extra --kernel-name kns=3pdg \
+    timeout ${SAN_TIMEOUT:-900} compute-sanitizer --tool $tool $extra $KNS \
       --print-limit 50 --error-exitcode 99 \
       python -m pytest -q -x -p no:cacheprovider "$t" >> $log 2>&1
     echo "exit $?" >> $log
