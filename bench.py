@@ -1074,6 +1074,7 @@ def bench_llm(dev, n_apps=100_000, templates=256, reps=10, cpu_sample=200):
            "engine_ms": ms, "apps_per_s": n_apps / (ms / 1e3),
            "conditioned_frac": float((fl & 1).mean()),
            "replayed_serial": int(((fl & 4) != 0).sum()),
+           "redrawn_in_kernel": int(((fl & 8) != 0).sum()),
            "bank_features": int(eng.bank.features)}
     if cpu_sample:
         og = {k: O.graph_from_kb(v) for k, v in docs.items()}

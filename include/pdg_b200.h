@@ -219,16 +219,19 @@ typedef struct {
   int64_t stride;
   const int32_t* slot;            /* [N] row written for job i (NULL: row i)          */
   int32_t* capped;                /* [N] walks that hit the visit cap (optional)      */
-  uint8_t* flags;                 /* [N] bit0 conditioned, bit1 override, bit2 serial */
+  uint8_t* flags;                 /* [N] bit0 conditioned, bit1 override, bit2 serial,
+                                     bit3 Lemire rejection redrawn in the fast kernel */
   double* mean;                   /* [rows] RemainingDemand.mean() (optional; Python  */
                                   /*   sum() semantics, see pdg_policy_keys)          */
   double* worst;                  /* [rows] max(samples) = worst_case (optional)      */
 } pdg_mc_out;
 
 /* Scratch for pdg_mc_remaining_demand: pdg_mc_scratch_bytes(n, max_pairs,
- * pdg_mc_grid_warps()) + 4 * n_jobs bytes.  Applications whose walk hits a
- * numpy Lemire rejection are finished by a second, sequential kernel in the
- * same call (flags bit2). */
+ * pdg_mc_grid_warps()) + 4 * n_jobs bytes.  A numpy Lemire rejection (the
+ * bounded draw redrawn, shifting every later half) is handled inside the fast
+ * kernel for n <= 512 (the visit's bounded values are redrawn with the
+ * sequential generator; flags bit3); own-input visits and n > 512 hand the
+ * application to a second, sequential kernel in the same call (flags bit2). */
 int pdg_mc_grid_warps(void);
 size_t pdg_mc_scratch_bytes(int32_t n_samples, int32_t max_pairs, int32_t grid_warps);
 int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_jobs* jobs,

@@ -13,7 +13,6 @@
 // NCCL dependency; the communicator is the caller's (ncclComm_t as void*).
 #include <dlfcn.h>
 
-#include <cub/cub.cuh>
 
 #include "common.cuh"
 
@@ -37,11 +36,8 @@ AllGatherFn nccl_allgather() {
 using namespace pdg;
 
 extern "C" size_t pdg_rank_allgather_sort_temp_bytes(int64_t width, int32_t world) {
-  size_t bytes = 0;
   const int64_t n = width * int64_t(world);
-  cub::DeviceRadixSort::SortKeys(nullptr, bytes, static_cast<const uint64_t*>(nullptr),
-                                 static_cast<uint64_t*>(nullptr), n > 0 ? n : 1, 0, 64);
-  return bytes + 256;
+  return order_temp_bytes(n > 0 ? n : 1) + 256;
 }
 
 extern "C" int pdg_rank_allgather_sort(void* nccl_comm, const uint64_t* local_keys,
@@ -74,8 +70,6 @@ extern "C" int pdg_rank_allgather_sort(void* nccl_comm, const uint64_t* local_ke
     set_error("pdg_rank_allgather_sort: ncclAllGather failed (ncclResult_t %d)", r);
     return PDG_ECUDA;
   }
-  size_t tb = temp_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortKeys(temp, tb, gathered, sorted_keys,
-                                                 width * int64_t(world), begin_bit, 64, st);
-  return cuda_status(e, "pdg_rank_allgather_sort");
+  return order_sort(gathered, sorted_keys, nullptr, nullptr, width * int64_t(world), begin_bit,
+                    64, temp, temp_bytes, st);
 }

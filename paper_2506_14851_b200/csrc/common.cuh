@@ -32,6 +32,14 @@ int sm_count();
 // so the per-call cost of a launch is the launch alone.
 int launch_setup(const void* kern, int threads, size_t smem, int* per_sm);
 
+// K5's one-kernel stable radix sort (sort.cu), shared by pdg_order, the
+// cross-rank exchange and the dispatch planner: bits [begin_bit, end_bit) of
+// the u64 keys, u32 payload optional (slots_in = slots_out = nullptr).
+size_t order_temp_bytes(int64_t n);
+int order_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* slots_in,
+               uint32_t* slots_out, int64_t n, int begin_bit, int end_bit, void* temp,
+               size_t temp_bytes, cudaStream_t stream);
+
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---- exact float64 helpers (never contracted into FMA) --------------------

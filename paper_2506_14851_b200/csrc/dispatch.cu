@@ -19,7 +19,6 @@
 // the simulator applies them.
 #include <algorithm>
 
-#include <cub/cub.cuh>
 
 #include "common.cuh"
 
@@ -209,12 +208,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
 using namespace pdg;
 
 extern "C" size_t pdg_dispatch_temp_bytes(int64_t n, int32_t n_backends) {
-  size_t sort_tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (const uint64_t*)nullptr,
-                                  (uint64_t*)nullptr, (const uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, n > 0 ? n : 1, 0, 64);
+  const size_t sort_tmp = order_temp_bytes(n > 0 ? n : 1);
   const size_t nn = size_t(n > 0 ? n : 1);
-  // keys x2 (u64), idx x2 (u32), counts (nb), status, cub temp
+  // keys x2 (u64), idx x2 (u32), counts (nb), status, sort temp
   return 2 * nn * 8 + 2 * nn * 4 + size_t(n_backends) * 4 + 256 + sort_tmp + 1024;
 }
 
@@ -258,16 +254,13 @@ extern "C" int pdg_dispatch_plan(const int32_t* backend, const uint8_t* active,
     if (blocks > int64_t(sm_count()) * 8) blocks = int64_t(sm_count()) * 8;
     tie_keys_kernel<<<unsigned(blocks), threads, 0, st>>>(app_rank, stage, request, n, k0, i0);
     // LSD: tie-break fields, then the priority key, then the backend (stable)
-    e = cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, k0, k1, i0, i1, n, 0, 64, st);
-    if (e != cudaSuccess) return cuda_status(e, "pdg_dispatch_plan sort 1");
+    if (int r = order_sort(k0, k1, i0, i1, n, 0, 64, sort_tmp, sort_bytes, st)) return r;
     gather_key_kernel<<<unsigned(blocks), threads, 0, st>>>(key, i1, n, k0);
-    e = cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, k0, k1, i1, i0, n, 0, 64, st);
-    if (e != cudaSuccess) return cuda_status(e, "pdg_dispatch_plan sort 2");
+    if (int r = order_sort(k0, k1, i1, i0, n, 0, 64, sort_tmp, sort_bytes, st)) return r;
     gather_backend_kernel<<<unsigned(blocks), threads, 0, st>>>(backend, i0, n, k0, count);
     int bits = 1;
     while ((1 << bits) < n_backends) ++bits;
-    e = cub::DeviceRadixSort::SortPairs(sort_tmp, sort_bytes, k0, k1, i0, i1, n, 0, bits, st);
-    if (e != cudaSuccess) return cuda_status(e, "pdg_dispatch_plan sort 3");
+    if (int r = order_sort(k0, k1, i0, i1, n, 0, bits, sort_tmp, sort_bytes, st)) return r;
   }
   PlanArgs a{i1, count, active, key, slots, n_backends, hysteresis, preempt, ev_cap,
              ev_task, ev_kind, ev_count, status};

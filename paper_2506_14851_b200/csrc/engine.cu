@@ -83,6 +83,7 @@ struct EngineArgs {
   int32_t* serial_list;   // [n_jobs] apps left to mc_serial_kernel
   int32_t* serial_count;  // [1]
   int32_t* job_next;      // [1] dynamic job counter (mc_walk_kernel)
+  int32_t* redo_next;     // [1] dynamic counter over serial_list (careful mc_walk_kernel)
 };
 
 // distributions.py:107-118 with (lo, hi = last bucket edge, k)
@@ -122,6 +123,7 @@ struct Stream {
   U128 s, inc;
   bool pend;
   uint32_t pv;
+  bool redrawn;     // a Lemire rejection was redrawn inside a visit (flags bit 3)
 };
 
 // Reads words forward from a base state: word q is the output after q+1 steps.
@@ -520,7 +522,7 @@ __device__ double neumaier_mean(double* tot, int n, double* sb, int lane) {
 __device__ void write_result(const EngineArgs& a, int64_t job, double* tot,
                              const int8_t* cur, uint32_t* cnt, bool conditioned, bool has_ov,
                              bool replayed, int lane, int capped_walks = -1,
-                             double* mean_buf = nullptr) {
+                             double* mean_buf = nullptr, bool redrawn = false) {
   const int n = a.n;
   int capped = 0;
   double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
@@ -572,7 +574,8 @@ __device__ void write_result(const EngineArgs& a, int64_t job, double* tot,
     if (a.o.nsamp) a.o.nsamp[row] = n;
     if (a.o.capped) a.o.capped[job] = capped;
     if (a.o.flags)
-      a.o.flags[job] = (conditioned ? 1 : 0) | (has_ov ? 2 : 0) | (replayed ? 4 : 0);
+      a.o.flags[job] = (conditioned ? 1 : 0) | (has_ov ? 2 : 0) | (replayed ? 4 : 0) |
+                       (redrawn ? 8 : 0);
   }
   __syncwarp();
 }
@@ -720,6 +723,7 @@ __global__ void __launch_bounds__(32) mc_serial_kernel(EngineArgs a) {
   const int total = *a.serial_count;
   for (int li = blockIdx.x; li < total; li += gridDim.x) {
     const int64_t job = a.serial_list[li];
+    if (job < 0) continue;                       // finished by the careful walk kernel
     const int gbase = a.b.graph_base[a.j.graph[job]];
     const int u0 = a.j.unit[job];
     Pools ovp{nullptr, 0, nullptr, 0};
@@ -1024,11 +1028,56 @@ __device__ __forceinline__ LaneConst lane_const(const uint64_t* jt, const U128& 
 // of the segment [wb bounded words | m uniforms]; bounded halves stage the
 // draw indices per rank, the uniform of rank k then adds the stage time and
 // moves the walk
+// numpy's Lemire rejection inside a visit's bounded draws: the rejected half
+// is replaced by the next one, which shifts every later half of the visit.
+// Lane 0 redraws the visit's C bounded values with the sequential generator,
+// from the visit's first word P0 (state jumped from the application's seed),
+// and returns the number of words they consumed plus numpy's buffered half.
+// Out of line: it runs for ~1 visit in 10^6 and stays out of the hot code.
+// Returns words | pend << 31 | buffered half << 32.
+__device__ __noinline__ uint64_t redo_bounded(const EngineArgs& a, int job, uint32_t P0,
+                                              bool pin, uint32_t pv, uint32_t pa, uint32_t pb,
+                                              uint32_t mA, uint32_t C, uint16_t* ia,
+                                              uint16_t* ib) {
+  U128 st, inc;
+  pcg_seed(a.j.seed[job], st, inc);
+  if (P0) st = pcg_jump(a.b.jump, st, inc, P0);        // the next step yields word P0
+  bool pend = pin;
+  uint32_t hv = pv, words = 0;
+  auto next32 = [&]() -> uint32_t {                    // numpy next_uint32
+    if (pend) {
+      pend = false;
+      return hv;
+    }
+    st = pcg_step(st, inc);
+    ++words;
+    const uint64_t w = pcg_out(st);
+    pend = true;
+    hv = uint32_t(w >> 32);
+    return uint32_t(w);
+  };
+  for (uint32_t j = 0; j < C; ++j) {                   // buffered_bounded_lemire_uint32
+    const uint32_t P = j < mA ? pa : pb;
+    uint64_t mm = uint64_t(next32()) * P;
+    uint32_t left = uint32_t(mm);
+    if (left < P) {
+      const uint32_t thr = (0u - P) % P;
+      while (left < thr) {
+        mm = uint64_t(next32()) * P;
+        left = uint32_t(mm);
+      }
+    }
+    if (j < mA) ia[j] = uint16_t(mm >> 32);
+    else ib[j - mA] = uint16_t(mm >> 32);
+  }
+  return uint64_t(words) | (pend ? (1ull << 31) : 0ull) | (uint64_t(hv) << 32);
+}
+
 // SPEC: per-successor-count specialised, unrolled uniform loops (the lean
 // duration-only kernel); the multi-kind kernels take one generic loop, whose
 // smaller code keeps them out of instruction-cache misses
-template <bool LLM, typename M, bool SPEC>
-__device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const SuccTab& sc,
+template <bool LLM, typename M, bool SPEC, bool CAREFUL>
+__device__ bool visit_strided(const EngineArgs& a, int job, const UnitDesc& d, const SuccTab& sc,
                               const Pools& pl, uint32_t thr_a, uint32_t thr_b,
                               const WalkState& ws, uint32_t m, Stream& g, LaneStream& ls,
                               const LaneConst& lc, M& targets, int lane) {
@@ -1042,8 +1091,7 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
   const uint32_t mA = pl.pa > 1 ? m : 0u;
   const uint32_t C = mA + ((llm && pl.pb > 1) ? m : 0u);
   const uint32_t pin = g.pend ? 1u : 0u;
-  const uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
-  const uint32_t W = wb + m;
+  uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
   U128& st = ls.st;                               // one stride before word q
   bool rej = false;
   uint32_t pend_hi = 0;
@@ -1073,6 +1121,22 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
     else ws.ib[0] = uint16_t(lemire_t(g.pv, uint32_t(pl.pb), thr_b, rej));
   }
   __syncwarp();
+  bool redone = false;
+  uint64_t rd = 0;
+  if (__any_sync(kFull, rej)) {                   // a Lemire rejection shifted the halves
+    if constexpr (!CAREFUL) return false;        // the careful kernel redoes this app
+    if (lane == 0)
+      rd = redo_bounded(a, job, ls.P, pin != 0, g.pv, uint32_t(pl.pa), uint32_t(pl.pb), mA, C,
+                        ws.ia, ws.ib);
+    __syncwarp();
+    rd = __shfl_sync(kFull, rd, 0);
+    const uint32_t w2 = uint32_t(rd) & 0x7fffffffu;
+    for (; q < w2; q += 32) st = pcg_stride32(st, lc.c32);   // skip the extra words
+    wb = w2;
+    redone = true;
+    g.redrawn = true;
+  }
+  const uint32_t W = wb + m;
   const bool hb = C > mA;
   // random(m): stage time + successor; the pool loads of the next word are
   // issued before the current word is finished
@@ -1116,15 +1180,81 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
 #pragma unroll 1
     for (; q < W; q += 32) uniform(std::integral_constant<int, 4>{});
   }
-  if (__any_sync(kFull, rej)) return false;
   const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
   ls.P += W;
-  if (C) {
+  if (redone) {
+    g.pend = (rd >> 31) & 1u;
+    g.pv = uint32_t(rd >> 32);
+  } else if (C) {
     g.pend = ((pin + C) & 1u) != 0;
     if (g.pend) g.pv = pv;
   }
   __syncwarp();
   return true;
+}
+
+// The own-input visit's bounded draws after a Lemire rejection: lane 0
+// redraws them with the sequential generator from the visit's first word,
+// in numpy's order (estimator.py:275-283): every input index, then per input
+// bucket ascending the output indices of that bucket's members in walk order.
+// Rewrites tmp (i / prefill + o / decode) and bkt; returns words | pend << 31
+// | buffered half << 32.  Out of line, careful pass only.
+__device__ __noinline__ uint64_t redo_own(const EngineArgs& a, int job, uint32_t P0, bool pin,
+                                          uint32_t pv, const UnitDesc& d, const Pools& pl,
+                                          const Pools& pd, uint32_t m, double* tmp,
+                                          uint16_t* bkt) {
+  U128 st, inc;
+  pcg_seed(a.j.seed[job], st, inc);
+  if (P0) st = pcg_jump(a.b.jump, st, inc, P0);
+  bool pend = pin;
+  uint32_t hv = pv, words = 0;
+  auto next32 = [&]() -> uint32_t {
+    if (pend) {
+      pend = false;
+      return hv;
+    }
+    st = pcg_step(st, inc);
+    ++words;
+    const uint64_t w = pcg_out(st);
+    pend = true;
+    hv = uint32_t(w >> 32);
+    return uint32_t(w);
+  };
+  auto bounded = [&](uint32_t P) -> uint32_t {        // buffered_bounded_lemire_uint32
+    if (P <= 1) return 0u;
+    uint64_t mm = uint64_t(next32()) * P;
+    uint32_t left = uint32_t(mm);
+    if (left < P) {
+      const uint32_t thr = (0u - P) % P;
+      while (left < thr) {
+        mm = uint64_t(next32()) * P;
+        left = uint32_t(mm);
+      }
+    }
+    return uint32_t(mm >> 32);
+  };
+  const int K = d.ib_k;
+  const double blo = d.ib_lo, bhi = d.ib_hi;
+  const double bw = __ddiv_rn(dsub(bhi, blo), small_int_to_double(K));
+  auto bucket = [&](double v) -> int {
+    if (bhi == blo || v <= blo) return 0;
+    if (v >= bhi) return K - 1;
+    const int i = __double2int_rz(__ddiv_rn(dsub(v, blo), bw));
+    return i < K - 1 ? i : K - 1;
+  };
+  for (uint32_t k = 0; k < m; ++k) {                  // choice(inputs, m)
+    const uint32_t ia = bounded(uint32_t(pl.pa));
+    tmp[k] = pd.A[ia];
+    bkt[k] = uint16_t(bucket(pl.A[ia]));
+  }
+  for (int bb = 0; bb < K; ++bb) {                     // per bucket: choice(pool_b, m_b)
+    const int pln = a.b.pool_len[d.pool_off + bb];
+    const double* pool = pln > 0 ? a.b.vals_div + a.b.pool_off[d.pool_off + bb] : pd.B;
+    const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
+    for (uint32_t k = 0; k < m; ++k)
+      if (bkt[k] == bb) tmp[k] = dadd(tmp[k], pool[bounded(P)]);
+  }
+  return uint64_t(words) | (pend ? (1ull << 31) : 0ull) | (uint64_t(hv) << 32);
 }
 
 // own-input LLM unit: outputs drawn per input bucket, buckets ascending,
@@ -1134,8 +1264,8 @@ __device__ bool visit_strided(const EngineArgs& a, const UnitDesc& d, const Succ
 // their buckets and bucket counts), a counting sort that maps each B half to
 // its member, the B words, then the uniforms.  The half shared by the last A
 // word and the first B draw, and numpy's buffered half, are placed by lane 0.
-template <typename M>
-__device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab& sc,
+template <typename M, bool CAREFUL>
+__device__ bool visit_own(const EngineArgs& a, int job, const UnitDesc& d, const SuccTab& sc,
                           const Pools& pl, const Pools& pd, const WalkState& ws, uint32_t m,
                           Stream& g, LaneStream& ls, const LaneConst& lc, M& targets,
                           int lane) {
@@ -1242,7 +1372,7 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
   }
   __syncwarp();
   const uint32_t C = mA + eff_total;
-  const uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
+  uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
   auto b_draw = [&](uint32_t j, uint32_t h) {
     const uint32_t k = effl[j];
     const int bb = ws.bkt[k];
@@ -1267,7 +1397,20 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
     if (!mA && pin) b_draw(0, g.pv);
     else if (mA && ((mA - pin) & 1u)) b_draw(0, sh);
   }
-  if (__any_sync(kFull, rej)) return false;
+  bool redone = false;
+  uint64_t rd = 0;
+  if (__any_sync(kFull, rej)) {                   // a Lemire rejection shifted the halves
+    if constexpr (!CAREFUL) return false;        // the careful kernel redoes this app
+    __syncwarp();
+    if (lane == 0) rd = redo_own(a, job, ls.P, pin != 0, g.pv, d, pl, pd, m, ws.tmp, ws.bkt);
+    __syncwarp();
+    rd = __shfl_sync(kFull, rd, 0);
+    const uint32_t w2 = uint32_t(rd) & 0x7fffffffu;
+    for (; q < w2; q += 32) st = pcg_stride32(st, lc.c32);   // skip the extra words
+    wb = w2;
+    redone = true;
+    g.redrawn = true;
+  }
   __syncwarp();
   const uint32_t W = wb + m;
   for (; q < W; q += 32) {                        // random(m): successor + total
@@ -1280,7 +1423,10 @@ __device__ bool visit_own(const EngineArgs& a, const UnitDesc& d, const SuccTab&
   }
   const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
   ls.P += W;
-  if (C) {
+  if (redone) {
+    g.pend = (rd >> 31) & 1u;
+    g.pv = uint32_t(rd >> 32);
+  } else if (C) {
     g.pend = ((pin + C) & 1u) != 0;
     if (g.pend) g.pv = pv;
   }
@@ -1306,7 +1452,14 @@ constexpr int kWalkWarps = PDG_WALK_WARPS;
 // duration walk a resident CTA per SM.  A job that needs a compiled-out path
 // anyway (features understated by the caller) is handed to mc_serial_kernel,
 // so FEAT only ever affects speed.
-template <int FEAT, typename M = uint32_t>   // M: unit-set mask (uint64_t: > 32 units)
+// M: unit-set mask (uint64_t: > 32 units).  CAREFUL: the second pass over
+// the applications the first pass handed back (serial_list): a visit whose
+// bounded draws hit a numpy Lemire rejection is redrawn in place with the
+// sequential generator (redo_bounded) instead of abandoning the application;
+// what it cannot finish (own-input visits, compiled-out paths) stays in the
+// list for mc_serial_kernel.  Keeping the redo out of the first pass keeps its
+// registers and code out of the hot kernel.
+template <int FEAT, typename M = uint32_t, bool CAREFUL = false>
 __global__ void __launch_bounds__(kWalkWarps * 32,
                                   FEAT == 0 ? PDG_WALK_MINB_LEAN : PDG_WALK_MINB)
 mc_walk_kernel(EngineArgs a) {
@@ -1337,10 +1490,23 @@ mc_walk_kernel(EngineArgs a) {
   ws.kin_d = ws.kout + a.max_pairs;
   ws.kout_d = ws.kin_d + a.max_pairs;
   for (;;) {
-    int job = 0;
-    if (lane == 0) job = atomicAdd(a.job_next, 1);
-    job = __shfl_sync(kFull, job, 0);
-    if (job >= a.n_jobs) break;
+    int job = 0, li = 0;
+    if constexpr (CAREFUL) {
+      if (lane == 0) li = atomicAdd(a.redo_next, 1);
+      li = __shfl_sync(kFull, li, 0);
+      if (li >= *a.serial_count) break;
+      job = a.serial_list[li];
+    } else {
+      if (lane == 0) job = atomicAdd(a.job_next, 1);
+      job = __shfl_sync(kFull, job, 0);
+      if (job >= a.n_jobs) break;
+    }
+    // hand the application on (first pass: to the careful pass; careful pass:
+    // leave it in the list for mc_serial_kernel)
+    auto hand_on = [&]() {
+      if (!CAREFUL && lane == 0) a.serial_list[atomicAdd(a.serial_count, 1)] = int32_t(job);
+      __syncwarp();
+    };
     const int gi = a.j.graph[job];
     const int gbase = a.b.graph_base[gi];
     const int gn = a.b.graph_n[gi];
@@ -1349,6 +1515,7 @@ mc_walk_kernel(EngineArgs a) {
     pcg_seed(a.j.seed[job], g.s, g.inc);
     g.pend = false;
     g.pv = 0;
+    g.redrawn = false;
     Pools ovp{nullptr, 0, nullptr, 0};
     bool conditioned = false;
     int obs_up;
@@ -1356,8 +1523,7 @@ mc_walk_kernel(EngineArgs a) {
     job_obs(a, job, obs_up, obs);
     if (!kCond && obs_up >= 0 &&
         (reinterpret_cast<const UnitDesc*>(a.b.units)[gbase + u0].flags & F_ANYMASK)) {
-      if (lane == 0) a.serial_list[atomicAdd(a.serial_count, 1)] = int32_t(job);
-      __syncwarp();
+      hand_on();
       continue;                                  // K3 compiled out: serial path
     }
     const bool has_ov = kCond &&
@@ -1431,32 +1597,32 @@ mc_walk_kernel(EngineArgs a) {
         const Pools pd = pools_div(a, d, ov, ovd);
         M targets = 0;
         if (!(d.flags & F_LLM))
-          ok = visit_strided<false, M, kSpec>(a, d, succ_of(uc[u]), pd, thr_a_of(uc[u]), 0u,
+          ok = visit_strided<false, M, kSpec, CAREFUL>(a, job, d, succ_of(uc[u]), pd, thr_a_of(uc[u]), 0u,
                                               ws, m, g, ls, lc, targets, lane);
         else if (!kLLM)
           ok = false;                            // compiled out: serial path
         else if ((d.flags & F_OWN) && !ov)
-          ok = kOwn && visit_own(a, d, succ_of(uc[u]), pools_for(a, d, ov, ovp), pd, ws, m,
+          ok = kOwn && visit_own<M, CAREFUL>(a, job, d, succ_of(uc[u]), pools_for(a, d, ov, ovp), pd, ws, m,
                                  g, ls, lc, targets, lane);
         else {                                   // override pools: thresholds here
           const uint32_t ta = ov ? lemire_thr_of(uint32_t(pd.pa)) : thr_a_of(uc[u]);
           const uint32_t tb = ov ? lemire_thr_of(uint32_t(pd.pb)) : thr_b_of(uc[u]);
-          ok = visit_strided<true, M, kSpec>(a, d, succ_of(uc[u]), pd, ta, tb, ws, m, g, ls,
+          ok = visit_strided<true, M, kSpec, CAREFUL>(a, job, d, succ_of(uc[u]), pd, ta, tb, ws, m, g, ls,
                                              lc, targets, lane);
         }
         pending |= warp_or(targets);
       }
     }
-    if (!ok) {                     // Lemire rejection: leave it to mc_serial_kernel
-      if (lane == 0) a.serial_list[atomicAdd(a.serial_count, 1)] = int32_t(job);
-      __syncwarp();
+    if (!ok) {                     // Lemire rejection: careful pass / mc_serial_kernel
+      hand_on();
       continue;
     }
+    if (CAREFUL && lane == 0) a.serial_list[li] = -1;   // done here
     int capped = 0;
     for (int i = lane; i < gn * kWalkWords; i += 32) capped += __popc(ws.bits[i]);
     capped = warp_sum(capped);
     write_result(a, job, ws.tot, nullptr, ws.cnt, conditioned, has_ov, false, lane, capped,
-                 ws.tmp);
+                 ws.tmp, g.redrawn);
   }
 }
 
@@ -1539,9 +1705,10 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   char* tail = static_cast<char*>(scratch) + a.scratch_per_warp * size_t(grid_warps);
   a.serial_count = reinterpret_cast<int32_t*>(tail);
   a.job_next = reinterpret_cast<int32_t*>(tail + 4);
+  a.redo_next = reinterpret_cast<int32_t*>(tail + 8);
   a.serial_list = reinterpret_cast<int32_t*>(tail + 256);
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(a.serial_count, 0, 2 * sizeof(int32_t), st);
+  cudaError_t e = cudaMemsetAsync(a.serial_count, 0, 3 * sizeof(int32_t), st);
   if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(serial_count)");
   const bool sm = n_samples <= kSmemWalks;
   const size_t cnt_bytes = align16(size_t(a.counters) * 4);
@@ -1577,17 +1744,44 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
     const size_t smem = size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu);
     const size_t smem_plain = size_t(kWalkWarps) * walk_smem_bytes(a.counters, mu, false);
     int r = PDG_OK;
+    // the careful second pass over the handed-back applications: one CTA per
+    // SM, warps fetch list entries dynamically and exit at once when the
+    // first pass handed back nothing
+    auto careful = [&](auto kern, size_t sm_bytes) -> int {
+      int per_sm = 0;
+      if (int rc = launch_setup(reinterpret_cast<const void*>(kern), kWalkWarps * 32, sm_bytes,
+                                &per_sm))
+        return rc;
+      kern<<<unsigned(sm_count()), kWalkWarps * 32, sm_bytes, st>>>(a);
+      return launch_status("mc_walk_kernel (careful pass)");
+    };
     if (mu > 32) {                               // 64-bit unit sets, every unit kind
       r = launch(mc_walk_kernel<7, uint64_t>, kWalkWarps, smem);
+      if (!r) r = careful(mc_walk_kernel<7, uint64_t, true>, smem);
       if (r) return r;
       return finish();
     }
     switch (feat) {
-      case 0: r = launch(mc_walk_kernel<0>, kWalkWarps, smem_plain); break;
-      case 1: r = launch(mc_walk_kernel<1>, kWalkWarps, smem); break;
-      case 4: r = launch(mc_walk_kernel<4>, kWalkWarps, smem_plain); break;
-      case 5: r = launch(mc_walk_kernel<5>, kWalkWarps, smem); break;
-      default: r = launch(mc_walk_kernel<7>, kWalkWarps, smem); break;
+      case 0:
+        r = launch(mc_walk_kernel<0>, kWalkWarps, smem_plain);
+        if (!r) r = careful(mc_walk_kernel<0, uint32_t, true>, smem_plain);
+        break;
+      case 1:
+        r = launch(mc_walk_kernel<1>, kWalkWarps, smem);
+        if (!r) r = careful(mc_walk_kernel<1, uint32_t, true>, smem);
+        break;
+      case 4:
+        r = launch(mc_walk_kernel<4>, kWalkWarps, smem_plain);
+        if (!r) r = careful(mc_walk_kernel<4, uint32_t, true>, smem_plain);
+        break;
+      case 5:
+        r = launch(mc_walk_kernel<5>, kWalkWarps, smem);
+        if (!r) r = careful(mc_walk_kernel<5, uint32_t, true>, smem);
+        break;
+      default:
+        r = launch(mc_walk_kernel<7>, kWalkWarps, smem);
+        if (!r) r = careful(mc_walk_kernel<7, uint32_t, true>, smem);
+        break;
     }
     if (r) return r;
   } else if (small_idx(n_samples)) {

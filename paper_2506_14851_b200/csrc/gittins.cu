@@ -16,7 +16,6 @@
 //        u16 bucket counts (exact: p_j = count_j / n), d_j formed bit-exactly
 //        in float64 at the alive boundary, scans in int32 (S, T exact) and
 //        float32 (P); HBM-bound, 128-bit loads of 8 counts per lane.
-#include <cub/cub.cuh>
 #include <cstring>
 
 #include "common.cuh"
@@ -241,27 +240,29 @@ __global__ void __launch_bounds__(256, (CH == 1 ? 4 : 2)) gittins_hist_kernel(Hi
 }
 
 // ---------------------------------------------------------------------------
-// K1b, quad form for the queue's layout (rows of <= 256 buckets, 16-byte
-// aligned, zero counts past nbins).  Four lanes score one row: lane
-// l = 8g + r works on row r of an 8-row tile and owns two 32-bucket segments
-// of it, x = [32g, 32g+32) and y = [128+32g, 160+32g), which it scans
+// K1b, pair form for the queue's layout (rows of <= 256 buckets, 16-byte
+// aligned, zero counts past nbins).  Two lanes score one row: lane
+// l = 16g + r works on row r of a 16-row tile and owns two 64-bucket segments
+// of it, x = [64g, 64g+64) and y = [128+64g, 192+64g), which it scans
 // together as the two halves of packed f32x2 registers (sm_100 FADD2 / FFMA2 /
-// FMUL2: one issue slot per bucket pair).
+// FMUL2: one issue slot per bucket pair).  (Four lanes per row were tried:
+// the per-row work -- j0, segment sums, prefix -- then dominates.)
 //
-// Staging: each warp owns a ring of STAGES tiles in shared memory, filled by
-// TMA bulk copies (cp.async.bulk, one 2*stride-byte copy per row issued by
-// lanes 0..7) that complete on the slot's mbarrier one tile ahead of the one
-// being scored.  Rows are 528 B apart (33 x 16 B), so the eight lanes of a
-// quarter-warp (same g, rows 0..7) read eight different bank groups.
+// Staging: each warp stages its tile in shared memory with TMA bulk copies
+// (cp.async.bulk, one 2*stride-byte copy per row issued by lanes 0..15)
+// completing on an mbarrier; STAGES > 1 rings prefetch tiles ahead, but one
+// stage with 24 warps per SM measured faster (the other warps hide the copy).
+// Rows are 528 B apart (33 x 16 B), so the eight lanes of a quarter-warp
+// (same g, eight consecutive rows) read eight different bank groups.
 //
 // Per row (sched.py:102-129 with the 1/Z normalisation cancelled):
 //  * the first alive bucket j0 (d_j = fl(fl(mid_j + est) - age) > 0, values
 //    ascend) is bracketed by a float32 estimate and confirmed by four exact
-//    float64 tests, one per lane of the row (binary search if the estimate
+//    float64 tests, two per lane of the row (binary search if the estimate
 //    misses); counts of dead buckets are zeroed;
 //  * each segment's alive mass and its weighted mass sum_k (k - j0) m_k come
 //    from IADD3 / IDP2A over the packed u16 counts; a prefix over the row's
-//    eight segments (shuffles across g) gives every segment its start state;
+//    four segments (one shuffle across g) gives every segment its start state;
 //  * with t = j - j0, d_j = d0 + t*w, S_j the alive prefix mass and
 //    T_j = Z - S_j, the numerator P_j + d_j*T_j is exactly d0*Z + w*I_j with
 //    I_j = I_{j-1} + T_{j-1} (integer-valued floats, exact), so a bucket is
@@ -278,10 +279,10 @@ constexpr int kPairTileU4 = 16 * kPairPitchU4;         // 16 rows per tile
 #define PDG_PAIR_WARPS 4
 #endif
 #ifndef PDG_PAIR_STAGES
-#define PDG_PAIR_STAGES 2
+#define PDG_PAIR_STAGES 1
 #endif
 #ifndef PDG_PAIR_MINB
-#define PDG_PAIR_MINB 3
+#define PDG_PAIR_MINB 6
 #endif
 constexpr int kPairWarps = PDG_PAIR_WARPS;
 constexpr int kPairStages = PDG_PAIR_STAGES;
@@ -950,146 +951,4 @@ extern "C" int pdg_policy_keys(int32_t policy, const double* mean, const double*
   return launch_status("policy_keys_kernel");
 }
 
-// ---------------------------------------------------------------------------
-// K5b: incremental global order after a micro-batch of re-scored rows
-// (config 4).  The previous order minus the changed rows is merged with the
-// changed rows' new keys: O(n) streaming passes instead of a full radix sort.
-// Keys are the full packed (key << 32 | tiebreak) words, unique per row, so
-// the result is exactly the order pdg_order produces.
-// ---------------------------------------------------------------------------
-#include <cub/device/device_merge.cuh>
-
-namespace pdg {
-__global__ void mark_rows_kernel(const int32_t* __restrict__ rows, int64_t m,
-                                 uint8_t* __restrict__ mark, uint8_t v) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
-       i += int64_t(gridDim.x) * blockDim.x)
-    mark[rows[i]] = v;
-}
-
-__global__ void keep_flags_kernel(const uint32_t* __restrict__ slots, int64_t n,
-                                  const uint8_t* __restrict__ mark, uint8_t* __restrict__ keep) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    keep[i] = mark[slots[i]] ? 0 : 1;
-}
-
-__global__ void gather_rows_kernel(const int32_t* __restrict__ rows, int64_t m,
-                                   const uint64_t* __restrict__ keys, uint64_t* __restrict__ k,
-                                   uint32_t* __restrict__ s) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int32_t r = rows[i];
-    k[i] = keys[r];
-    s[i] = uint32_t(r);
-  }
-}
-
-struct KeyLess {
-  __device__ __forceinline__ bool operator()(uint64_t a, uint64_t b) const { return a < b; }
-};
-
-struct UpdateTemp {   // carve of the caller's temp buffer
-  uint8_t* keep;
-  uint64_t* ok;        // old kept keys
-  uint32_t* os;        // old kept slots
-  uint64_t* nk;        // new keys (unsorted, sorted)
-  uint64_t* nk2;
-  uint32_t* ns;
-  uint32_t* ns2;
-  int64_t* nsel;
-  void* cub;
-  size_t cub_bytes;
-};
-
-static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-
-static size_t update_cub_bytes(int64_t n, int64_t m) {
-  size_t a = 0, b = 0, c = 0, d = 0;
-  const int64_t nn = n > 0 ? n : 1, mm = m > 0 ? m : 1;
-  cub::DeviceSelect::Flagged(nullptr, a, (const uint64_t*)nullptr, (const uint8_t*)nullptr,
-                             (uint64_t*)nullptr, (int64_t*)nullptr, nn);
-  cub::DeviceSelect::Flagged(nullptr, b, (const uint32_t*)nullptr, (const uint8_t*)nullptr,
-                             (uint32_t*)nullptr, (int64_t*)nullptr, nn);
-  cub::DeviceRadixSort::SortPairs(nullptr, c, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, mm, 0, 64);
-  cub::DeviceMerge::MergePairs(nullptr, d, (const uint64_t*)nullptr, (const uint32_t*)nullptr,
-                               nn, (const uint64_t*)nullptr, (const uint32_t*)nullptr, mm,
-                               (uint64_t*)nullptr, (uint32_t*)nullptr, KeyLess{});
-  size_t r = a > b ? a : b;
-  r = r > c ? r : c;
-  return r > d ? r : d;
-}
-
-static UpdateTemp carve_update(void* temp, int64_t n, int64_t m) {
-  UpdateTemp t;
-  const size_t nn = size_t(n > 0 ? n : 1), mm = size_t(m > 0 ? m : 1);
-  char* p = static_cast<char*>(temp);
-  t.keep = reinterpret_cast<uint8_t*>(p);         p += align256(nn);
-  t.ok = reinterpret_cast<uint64_t*>(p);          p += align256(nn * 8);
-  t.os = reinterpret_cast<uint32_t*>(p);          p += align256(nn * 4);
-  t.nk = reinterpret_cast<uint64_t*>(p);          p += align256(mm * 8);
-  t.nk2 = reinterpret_cast<uint64_t*>(p);         p += align256(mm * 8);
-  t.ns = reinterpret_cast<uint32_t*>(p);          p += align256(mm * 4);
-  t.ns2 = reinterpret_cast<uint32_t*>(p);         p += align256(mm * 4);
-  t.nsel = reinterpret_cast<int64_t*>(p);         p += 256;
-  t.cub = p;
-  t.cub_bytes = update_cub_bytes(n, m);
-  return t;
-}
-}  // namespace pdg
-
-extern "C" size_t pdg_order_update_temp_bytes(int64_t n, int64_t m) {
-  using namespace pdg;
-  const size_t nn = size_t(n > 0 ? n : 1), mm = size_t(m > 0 ? m : 1);
-  return align256(nn) + align256(nn * 8) + align256(nn * 4) + 2 * align256(mm * 8) +
-         2 * align256(mm * 4) + 256 + update_cub_bytes(n, m) + 256;
-}
-
-extern "C" int pdg_order_update(const uint64_t* keys, const uint64_t* sorted_keys_in,
-                                const uint32_t* sorted_slots_in, int64_t n,
-                                const int32_t* rows, int64_t m, uint8_t* mark,
-                                uint64_t* sorted_keys_out, uint32_t* sorted_slots_out,
-                                void* temp, size_t temp_bytes, void* stream) {
-  using namespace pdg;
-  if (n < 0 || m < 0 || m > n || (n > 0 && (!keys || !sorted_keys_in || !sorted_slots_in ||
-                                            !mark || !sorted_keys_out || !sorted_slots_out)) ||
-      (m > 0 && !rows) || !temp) {
-    set_error("pdg_order_update: invalid arguments");
-    return PDG_EINVAL;
-  }
-  if (temp_bytes < pdg_order_update_temp_bytes(n, m)) {
-    set_error("pdg_order_update: temp_bytes %zu too small", temp_bytes);
-    return PDG_EINVAL;
-  }
-  if (n == 0) return PDG_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  UpdateTemp t = carve_update(temp, n, m);
-  const int threads = 256;
-  auto blocks = [&](int64_t x) {
-    int64_t b = (x + threads - 1) / threads;
-    const int64_t cap = int64_t(sm_count()) * 8;
-    return unsigned(b < 1 ? 1 : (b > cap ? cap : b));
-  };
-  if (m > 0) mark_rows_kernel<<<blocks(m), threads, 0, st>>>(rows, m, mark, 1);
-  keep_flags_kernel<<<blocks(n), threads, 0, st>>>(sorted_slots_in, n, mark, t.keep);
-  size_t cb = t.cub_bytes;
-  cudaError_t e = cub::DeviceSelect::Flagged(t.cub, cb, sorted_keys_in, t.keep, t.ok, t.nsel,
-                                             n, st);
-  if (e != cudaSuccess) return cuda_status(e, "pdg_order_update select keys");
-  cb = t.cub_bytes;
-  e = cub::DeviceSelect::Flagged(t.cub, cb, sorted_slots_in, t.keep, t.os, t.nsel, n, st);
-  if (e != cudaSuccess) return cuda_status(e, "pdg_order_update select slots");
-  if (m > 0) {
-    mark_rows_kernel<<<blocks(m), threads, 0, st>>>(rows, m, mark, 0);
-    gather_rows_kernel<<<blocks(m), threads, 0, st>>>(rows, m, keys, t.nk, t.ns);
-    cb = t.cub_bytes;
-    e = cub::DeviceRadixSort::SortPairs(t.cub, cb, t.nk, t.nk2, t.ns, t.ns2, m, 0, 64, st);
-    if (e != cudaSuccess) return cuda_status(e, "pdg_order_update sort batch");
-  }
-  cb = t.cub_bytes;
-  e = cub::DeviceMerge::MergePairs(t.cub, cb, t.ok, t.os, n - m, t.nk2, t.ns2, m,
-                                   sorted_keys_out, sorted_slots_out, KeyLess{}, st);
-  if (e != cudaSuccess) return cuda_status(e, "pdg_order_update merge");
-  return launch_status("pdg_order_update");
-}
+// K5b (pdg_order_update) lives in sort.cu

@@ -20,7 +20,9 @@
 //      every warp ranks its 128 consecutive keys with __match_any_sync (peer
 //      groups = equal digits), warps are combined per digit through a
 //      shared-memory count table, so equal digits keep input order (stable).
-// Three grid barriers per pass; 4 passes for begin_bit = 32, 8 for 0.
+// Three grid barriers per pass; 4 passes for begin_bit = 32, 8 for 0.  The
+// same kernel sorts the all-gathered keys of pdg_rank_allgather_sort and the
+// three stable passes of the dispatch planner (K6).
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -47,7 +49,8 @@ struct SortArgs {
   int64_t n;
   int64_t chunk;      // keys per CTA (multiple of kSortTile)
   int begin_bit;
-  int passes;
+  int end_bit;
+  int passes;         // ceil((end_bit - begin_bit) / 8); the last one writes kout
 };
 
 // exclusive scan of one value per thread over the CTA; returns the total
@@ -90,18 +93,22 @@ __global__ void __launch_bounds__(kSortThreads) order_sort_kernel(SortArgs a) {
   const int64_t c0 = int64_t(b) * a.chunk;
   const int64_t c1 = c0 + a.chunk < a.n ? c0 + a.chunk : a.n;
 
+  const bool payload = a.sin != nullptr;
   for (int p = 0; p < a.passes; ++p) {
-    const uint64_t* kr = p == 0 ? a.kin : ((p & 1) ? a.ktmp : a.kout);
-    const uint32_t* sr = p == 0 ? a.sin : ((p & 1) ? a.stmp : a.sout);
-    uint64_t* kw = (p & 1) ? a.kout : a.ktmp;
-    uint32_t* sw = (p & 1) ? a.sout : a.stmp;
+    // pass p writes kout when (passes - 1 - p) is even, so the last one does
+    const bool to_out = ((a.passes - 1 - p) & 1) == 0;
+    const uint64_t* kr = p == 0 ? a.kin : (to_out ? a.ktmp : a.kout);
+    const uint32_t* sr = p == 0 ? a.sin : (to_out ? a.stmp : a.sout);
+    uint64_t* kw = to_out ? a.kout : a.ktmp;
+    uint32_t* sw = to_out ? a.sout : a.stmp;
     const int shift = a.begin_bit + 8 * p;
+    const uint32_t dmask = a.end_bit - shift >= 8 ? 255u : (1u << (a.end_bit - shift)) - 1u;
 
     // A: digit histogram of this CTA's chunk
     hist[t] = 0u;
     __syncthreads();
     for (int64_t i = c0 + t; i < c1; i += kSortThreads)
-      atomicAdd(&hist[uint32_t(__ldcg(kr + i) >> shift) & 255u], 1u);
+      atomicAdd(&hist[uint32_t(__ldcg(kr + i) >> shift) & dmask], 1u);
     __syncthreads();
     a.H[size_t(t) * G + b] = hist[t];
     grid.sync();
@@ -143,8 +150,8 @@ __global__ void __launch_bounds__(kSortThreads) order_sort_kernel(SortArgs a) {
         const int64_t i = tb + int64_t(w) * kSortWarpKeys + 32 * s + lane;
         const bool valid = i < c1;
         key[s] = valid ? __ldcg(kr + i) : 0ull;
-        slot[s] = valid ? __ldcg(sr + i) : 0u;
-        const uint32_t d = valid ? uint32_t(key[s] >> shift) & 255u : 0x100u + lane;
+        slot[s] = (valid && payload) ? __ldcg(sr + i) : 0u;
+        const uint32_t d = valid ? uint32_t(key[s] >> shift) & dmask : 0x100u + lane;
         dig[s] = d;
         const unsigned peers = __match_any_sync(kFull, d);
         uint32_t v = 0;
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(kSortThreads) order_sort_kernel(SortArgs a) {
         if (d < 256u) {
           const uint32_t pos = off[d] + cnt[w][d] + rnk[s];
           kw[pos] = key[s];
-          sw[pos] = slot[s];
+          if (payload) sw[pos] = slot[s];
         }
       }
       __syncthreads();
@@ -185,44 +192,38 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // upper bound of the cooperative grid (8 CTAs of 256 threads per SM)
 static int sort_grid_cap() { return sm_count() * (2048 / kSortThreads); }
 
-}  // namespace pdg
-
-using namespace pdg;
-
-extern "C" size_t pdg_order_temp_bytes(int64_t n) {
+size_t order_temp_bytes(int64_t n) {
   if (n < 0) n = 0;
   const size_t G = size_t(sort_grid_cap());
   return align256(size_t(n) * 8) + align256(size_t(n) * 4) + align256(256 * G * 4) +
          align256(G * 4);
 }
 
-extern "C" int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
-                         const uint32_t* slots_in, uint32_t* slots_out, int64_t n,
-                         int32_t begin_bit, void* temp, size_t temp_bytes,
-                         void* stream) {
-  if (n < 0 || (n > 0 && (!keys_in || !keys_out || !slots_in || !slots_out || !temp))) {
-    set_error("pdg_order: invalid arguments");
-    return PDG_EINVAL;
+// Stable LSD radix sort of keys_in on bits [begin_bit, end_bit) into
+// keys_out, carrying slots (optional: both null for keys only).
+int order_sort(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* slots_in,
+               uint32_t* slots_out, int64_t n, int begin_bit, int end_bit, void* temp,
+               size_t temp_bytes, cudaStream_t stream) {
+  if (n == 0 || end_bit <= begin_bit) {
+    if (n > 0) {                                        // nothing to sort on: copy
+      cudaError_t e = cudaMemcpyAsync(keys_out, keys_in, size_t(n) * 8,
+                                      cudaMemcpyDeviceToDevice, stream);
+      if (e == cudaSuccess && slots_in)
+        e = cudaMemcpyAsync(slots_out, slots_in, size_t(n) * 4, cudaMemcpyDeviceToDevice,
+                            stream);
+      return cuda_status(e, "order_sort copy");
+    }
+    return PDG_OK;
   }
-  if (begin_bit != 0 && begin_bit != 32) {
-    set_error("pdg_order: begin_bit must be 0 or 32");
-    return PDG_EINVAL;
-  }
-  if (n > (int64_t(1) << 32) - 1) {
-    set_error("pdg_order: more than 2^32 - 1 keys");
-    return PDG_EUNSUPPORTED;
-  }
-  if (n == 0) return PDG_OK;
-  const size_t need = pdg_order_temp_bytes(n);
+  const size_t need = order_temp_bytes(n);
   if (temp_bytes < need) {
-    set_error("pdg_order: temp_bytes %zu < %zu", temp_bytes, need);
+    set_error("order_sort: temp_bytes %zu < %zu", temp_bytes, need);
     return PDG_EINVAL;
   }
   const int gcap = sort_grid_cap();
   int per_sm = 0;
-  const size_t dsmem = size_t(gcap) * 4;
   if (int r = launch_setup(reinterpret_cast<const void*>(order_sort_kernel), kSortThreads,
-                           dsmem, &per_sm))
+                           size_t(gcap) * 4, &per_sm))
     return r;
   int64_t G = int64_t(per_sm) * sm_count();
   if (G > gcap) G = gcap;
@@ -245,10 +246,299 @@ extern "C" int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
   a.chunk = ((tiles + G - 1) / G) * kSortTile;
   G = (n + a.chunk - 1) / a.chunk;                       // no CTA without keys
   a.begin_bit = begin_bit;
-  a.passes = (64 - begin_bit) / 8;
+  a.end_bit = end_bit;
+  a.passes = (end_bit - begin_bit + 7) / 8;
   void* args[] = {&a};
   cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(order_sort_kernel),
                                               dim3(unsigned(G)), dim3(kSortThreads), args,
-                                              size_t(G) * 4, (cudaStream_t)stream);
-  return cuda_status(e, "pdg_order (order_sort_kernel)");
+                                              size_t(G) * 4, stream);
+  return cuda_status(e, "order_sort_kernel");
+}
+
+}  // namespace pdg
+
+using namespace pdg;
+
+extern "C" size_t pdg_order_temp_bytes(int64_t n) { return order_temp_bytes(n); }
+
+extern "C" int pdg_order(const uint64_t* keys_in, uint64_t* keys_out,
+                         const uint32_t* slots_in, uint32_t* slots_out, int64_t n,
+                         int32_t begin_bit, void* temp, size_t temp_bytes,
+                         void* stream) {
+  if (n < 0 || (n > 0 && (!keys_in || !keys_out || !slots_in || !slots_out || !temp))) {
+    set_error("pdg_order: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (begin_bit != 0 && begin_bit != 32) {
+    set_error("pdg_order: begin_bit must be 0 or 32");
+    return PDG_EINVAL;
+  }
+  if (n > (int64_t(1) << 32) - 1) {
+    set_error("pdg_order: more than 2^32 - 1 keys");
+    return PDG_EUNSUPPORTED;
+  }
+  return order_sort(keys_in, keys_out, slots_in, slots_out, n, begin_bit, 64, temp,
+                    temp_bytes, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------
+// K5b: incremental order after re-scoring m rows (config 4), ONE cooperative
+// kernel instead of mark / select / sort / merge library passes.  With the
+// previous order O (n sorted unique keys + slots), the re-scored rows R and
+// their new keys B (unique too):
+//   P0  mark R; gather B (key, row)
+//   P1  per 1024-key tile of O: keep = !mark[slot], kept count per tile
+//   P2  unmark R; tile prefixes of the kept counts; rank B by counting
+//       (m <= kUpdRankMax: every CTA ranks a share of B against all of B in
+//       shared memory; larger batches arrive pre-sorted by order_sort)
+//   P3  a kept key k of O goes to (#kept before it) + (#B < k); the j-th
+//       smallest b of B goes to j + (#kept < b) = j + kept_prefix(lower_bound(O, b)),
+//       the prefix finished by one warp over the tile's keep bytes.
+// Same result as a full sort of the updated keys (all keys are unique).
+// ---------------------------------------------------------------------------
+namespace pdg {
+
+constexpr int kUpdTile = 1024;
+constexpr int kUpdRankMax = 4096;
+
+struct UpdArgs {
+  const uint64_t* keys;     // every row's packed key (new keys of R)
+  const uint64_t* ski;      // previous order
+  const uint32_t* ssi;
+  int64_t n;
+  const int32_t* rows;
+  int64_t m;
+  uint8_t* mark;
+  uint64_t* sko;
+  uint32_t* sso;
+  uint8_t* keep;
+  uint64_t* bk;             // gathered batch
+  uint32_t* bs;
+  uint64_t* bk2;            // sorted batch
+  uint32_t* bs2;
+  uint32_t* tc;             // kept per tile, then exclusive tile prefixes
+  uint32_t* S;              // kept per CTA
+  int64_t chunk;            // keys of O per CTA (multiple of kUpdTile)
+  int presorted;            // bk2 / bs2 given (m > kUpdRankMax)
+};
+
+__global__ void __launch_bounds__(kSortThreads) order_update_kernel(UpdArgs a) {
+  extern __shared__ __align__(16) unsigned char usm[];     // [G] u32 | batch keys
+  __shared__ uint32_t wsum[kSortWarps];
+  cg::grid_group grid = cg::this_grid();
+  const int G = int(gridDim.x), b = int(blockIdx.x), t = int(threadIdx.x);
+  const int lane = t & 31, w = t >> 5;
+  const int64_t gt = int64_t(b) * kSortThreads + t, gstride = int64_t(G) * kSortThreads;
+  const int64_t c0 = int64_t(b) * a.chunk;
+  const int64_t c1 = c0 + a.chunk < a.n ? c0 + a.chunk : a.n;
+  uint32_t* sS = reinterpret_cast<uint32_t*>(usm);
+  uint64_t* sB = reinterpret_cast<uint64_t*>(usm + ((size_t(G) * 4 + 15) & ~size_t(15)));
+
+  // P0
+  for (int64_t j = gt; j < a.m; j += gstride) {
+    const int32_t r = a.rows[j];
+    a.mark[r] = 1;
+    if (!a.presorted) {
+      a.bk[j] = a.keys[r];
+      a.bs[j] = uint32_t(r);
+    }
+  }
+  grid.sync();
+
+  // P1: keep flags and kept count per tile (4 keys per thread per tile)
+  uint32_t cta_kept = 0;
+  for (int64_t tb = c0; tb < c1; tb += kUpdTile) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int s = 0; s < kUpdTile / kSortThreads; ++s) {
+      const int64_t i = tb + int64_t(s) * kSortThreads + t;
+      if (i < c1) {
+        const uint8_t k = a.mark[__ldcg(a.ssi + i)] ? 0 : 1;
+        a.keep[i] = k;
+        c += k;
+      }
+    }
+    uint32_t ex;
+    const uint32_t tot = cta_excl_scan(c, ex, wsum);
+    if (t == 0) a.tc[tb / kUpdTile] = tot;
+    cta_kept += tot;
+  }
+  if (t == 0) a.S[b] = cta_kept;
+  grid.sync();
+
+  // P2: unmark; tile prefixes; rank the batch
+  for (int64_t j = gt; j < a.m; j += gstride) a.mark[a.rows[j]] = 0;
+  {
+    uint32_t carry = 0;
+    for (int base = 0; base < G; base += kSortThreads) {
+      const int i = base + t;
+      const uint32_t v = i < G ? __ldcg(a.S + i) : 0u;
+      uint32_t ex;
+      const uint32_t tot = cta_excl_scan(v, ex, wsum);
+      if (i < G) sS[i] = carry + ex;
+      carry += tot;
+    }
+    __syncthreads();
+    if (t == 0) {
+      uint32_t run = sS[b];
+      for (int64_t tb = c0; tb < c1; tb += kUpdTile) {
+        const uint32_t c = __ldcg(a.tc + tb / kUpdTile);
+        a.tc[tb / kUpdTile] = run;
+        run += c;
+      }
+    }
+  }
+  if (!a.presorted && a.m > 0) {
+    for (int64_t j = t; j < a.m; j += kSortThreads) sB[j] = __ldcg(a.bk + j);
+    __syncthreads();
+    for (int64_t j = gt; j < a.m; j += gstride) {
+      const uint64_t x = sB[j];
+      uint32_t rank = 0;
+      for (int64_t i = 0; i < a.m; ++i) rank += sB[i] < x ? 1u : 0u;
+      a.bk2[rank] = x;
+      a.bs2[rank] = __ldcg(a.bs + j);
+    }
+  }
+  grid.sync();
+
+  // P3: scatter the kept keys of O ...
+  for (int64_t tb = c0; tb < c1; tb += kUpdTile) {
+    const uint32_t base = __ldcg(a.tc + tb / kUpdTile);
+    const int64_t i0 = tb + int64_t(t) * (kUpdTile / kSortThreads);   // 4 consecutive keys
+    uint32_t c = 0;
+    uint8_t kp[kUpdTile / kSortThreads];
+#pragma unroll
+    for (int s = 0; s < kUpdTile / kSortThreads; ++s) {
+      kp[s] = (i0 + s < c1) ? __ldcg(a.keep + i0 + s) : 0;
+      c += kp[s];
+    }
+    uint32_t ex;
+    cta_excl_scan(c, ex, wsum);
+#pragma unroll
+    for (int s = 0; s < kUpdTile / kSortThreads; ++s) {
+      if (!kp[s]) continue;
+      const uint64_t k = __ldcg(a.ski + i0 + s);
+      int64_t lo = 0, hi = a.m;                          // #B < k
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldcg(a.bk2 + mid) < k) lo = mid + 1; else hi = mid;
+      }
+      const uint64_t pos = uint64_t(base) + ex + uint64_t(lo);
+      a.sko[pos] = k;
+      a.sso[pos] = __ldcg(a.ssi + i0 + s);
+      ++ex;
+    }
+  }
+  // ... and the batch: one warp per batch key
+  const int64_t gw = int64_t(b) * kSortWarps + w, nwarps = int64_t(G) * kSortWarps;
+  for (int64_t j = gw; j < a.m; j += nwarps) {
+    const uint64_t x = __ldcg(a.bk2 + j);
+    int64_t lo = 0, hi = a.n;                            // L = #O < x
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldcg(a.ski + mid) < x) lo = mid + 1; else hi = mid;
+    }
+    const int64_t tile = lo / kUpdTile, ts = tile * kUpdTile;
+    uint32_t c = 0;                                      // kept in [ts, lo)
+    for (int64_t i = ts + lane; i < lo; i += 32) c += __ldcg(a.keep + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    // (lo = n: every key of O is below x, so all n - m kept ones are)
+    const uint32_t before = lo < a.n ? __ldcg(a.tc + tile) + c : uint32_t(a.n - a.m);
+    if (lane == 0) {
+      const uint64_t pos = uint64_t(j) + before;
+      a.sko[pos] = x;
+      a.sso[pos] = __ldcg(a.bs2 + j);
+    }
+  }
+}
+
+__global__ void gather_batch_kernel(const int32_t* __restrict__ rows, int64_t m,
+                                    const uint64_t* __restrict__ keys, uint64_t* __restrict__ k,
+                                    uint32_t* __restrict__ s) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t r = rows[i];
+    k[i] = keys[r];
+    s[i] = uint32_t(r);
+  }
+}
+
+static size_t update_temp_bytes(int64_t n, int64_t m) {
+  const size_t nn = size_t(n > 0 ? n : 1), mm = size_t(m > 0 ? m : 1);
+  const size_t tiles = (nn + kUpdTile - 1) / kUpdTile;
+  const size_t G = size_t(sort_grid_cap());
+  return align256(nn) + 2 * align256(mm * 8) + 2 * align256(mm * 4) + align256(tiles * 4) +
+         align256(G * 4) + (m > kUpdRankMax ? order_temp_bytes(m) : 0) + 256;
+}
+
+}  // namespace pdg
+
+extern "C" size_t pdg_order_update_temp_bytes(int64_t n, int64_t m) {
+  return update_temp_bytes(n, m);
+}
+
+extern "C" int pdg_order_update(const uint64_t* keys, const uint64_t* sorted_keys_in,
+                                const uint32_t* sorted_slots_in, int64_t n,
+                                const int32_t* rows, int64_t m, uint8_t* mark,
+                                uint64_t* sorted_keys_out, uint32_t* sorted_slots_out,
+                                void* temp, size_t temp_bytes, void* stream) {
+  if (n < 0 || m < 0 || m > n || n > (int64_t(1) << 32) - 1 ||
+      (n > 0 && (!keys || !sorted_keys_in || !sorted_slots_in || !mark || !sorted_keys_out ||
+                 !sorted_slots_out)) ||
+      (m > 0 && !rows) || !temp) {
+    set_error("pdg_order_update: invalid arguments");
+    return PDG_EINVAL;
+  }
+  if (temp_bytes < update_temp_bytes(n, m)) {
+    set_error("pdg_order_update: temp_bytes %zu too small", temp_bytes);
+    return PDG_EINVAL;
+  }
+  if (n == 0) return PDG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t nn = size_t(n), mm = size_t(m > 0 ? m : 1);
+  const size_t tiles = (nn + kUpdTile - 1) / kUpdTile;
+  const int gcap = sort_grid_cap();
+  char* p = static_cast<char*>(temp);
+  UpdArgs a;
+  a.keys = keys;
+  a.ski = sorted_keys_in;
+  a.ssi = sorted_slots_in;
+  a.n = n;
+  a.rows = rows;
+  a.m = m;
+  a.mark = mark;
+  a.sko = sorted_keys_out;
+  a.sso = sorted_slots_out;
+  a.keep = reinterpret_cast<uint8_t*>(p);   p += align256(nn);
+  a.bk = reinterpret_cast<uint64_t*>(p);    p += align256(mm * 8);
+  a.bk2 = reinterpret_cast<uint64_t*>(p);   p += align256(mm * 8);
+  a.bs = reinterpret_cast<uint32_t*>(p);    p += align256(mm * 4);
+  a.bs2 = reinterpret_cast<uint32_t*>(p);   p += align256(mm * 4);
+  a.tc = reinterpret_cast<uint32_t*>(p);    p += align256(tiles * 4);
+  a.S = reinterpret_cast<uint32_t*>(p);     p += align256(size_t(gcap) * 4);
+  a.presorted = m > kUpdRankMax ? 1 : 0;
+  if (a.presorted) {                        // large batch: gather + one-kernel sort first
+    gather_batch_kernel<<<unsigned(sm_count()) * 4, 256, 0, st>>>(rows, m, keys, a.bk, a.bs);
+    if (int r = launch_status("gather_batch_kernel")) return r;
+    if (int r = order_sort(a.bk, a.bk2, a.bs, a.bs2, m, 0, 64, p, order_temp_bytes(m), st))
+      return r;
+  }
+  const size_t dsmem = ((size_t(gcap) * 4 + 15) & ~size_t(15)) +
+                       (a.presorted ? 0 : size_t(m) * 8);
+  int per_sm = 0;
+  if (int r = launch_setup(reinterpret_cast<const void*>(order_update_kernel), kSortThreads,
+                           dsmem, &per_sm))
+    return r;
+  int64_t G = int64_t(per_sm) * sm_count();
+  if (G > gcap) G = gcap;
+  const int64_t need_tiles = int64_t(tiles);
+  if (G > need_tiles) G = need_tiles;
+  a.chunk = ((need_tiles + G - 1) / G) * kUpdTile;
+  G = (n + a.chunk - 1) / a.chunk;
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(order_update_kernel),
+                                              dim3(unsigned(G)), dim3(kSortThreads), args,
+                                              dsmem, st);
+  return cuda_status(e, "pdg_order_update (order_update_kernel)");
 }

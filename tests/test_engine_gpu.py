@@ -183,7 +183,9 @@ def _rejecting_seed(P, n, steps, window=200):
 @pytest.mark.parametrize("n", [4000, 512, 96])      # mc_engine_kernel / mc_walk_kernel
 def test_lemire_rejection_replayed_exactly(n):
     """numpy rejects a bounded draw with probability < P/2^32; the engine's
-    warp vote must detect it and replay the application sequentially."""
+    warp vote must detect it and redraw the visit's bounded values with the
+    sequential generator (mc_walk_kernel) or replay the application
+    (mc_engine_kernel -> mc_serial_kernel)."""
     from paper_2506_14851_b200.estimator import DemandEngine
     from paper_2506_14851_b200.graphs import graph_from_kb
     P = max(range(900, 1001), key=lambda p: (2**32 - p) % p)
@@ -207,7 +209,10 @@ def test_lemire_rejection_replayed_exactly(n):
     got = run_cases(eng, case)
     want = O.mc_remaining_demand(og, "a", [], n, seed, steps)
     np.testing.assert_array_equal(got[0][0], want.samples)
-    assert got[0][2] & 4, "the sequential replay path was not exercised"
+    # n <= 512: redrawn inside the visit (flags bit 3); above: the sequential
+    # replay kernel (bit 2)
+    bit = 8 if n <= 512 else 4
+    assert got[0][2] & bit, "the rejection path was not exercised"
 
 
 def test_visit_cap_zero_and_empty_units(kb_graphs):

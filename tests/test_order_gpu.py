@@ -45,3 +45,41 @@ def test_order_matches_stable_argsort(n, begin_bit):
 def test_order_zero_length():
     got_k, got_s = _order(np.zeros(0, np.uint64), np.zeros(0, np.uint32), 32)
     assert got_k.size == 0 and got_s.size == 0
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (1000, 0), (1000, 1), (5000, 1000), (100_000, 1000),
+                                 (100_000, 4096), (200_000, 6000), (3000, 3000)])
+def test_order_update_equals_full_sort(n, m):
+    """K5b pdg_order_update (one cooperative kernel): the previous order minus
+    m re-scored rows merged with their new keys equals a full sort of the
+    updated keys; the mark buffer is left zeroed.  m > 4096 takes the
+    pre-sorted batch path."""
+    import torch
+    from paper_2506_14851_b200 import _lib
+    L = _lib.lib()
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(n * 7 + m)
+    fk = rng.choice(rng.uniform(0, 10, max(2, n // 20)).astype(np.float32), n)
+    keys = (fk.view(np.uint32).astype(np.uint64) << np.uint64(32)) | np.arange(n, dtype=np.uint64)
+    order = np.argsort(keys, kind="stable")
+    rows = rng.choice(n, m, replace=False).astype(np.int32)
+    new = keys.copy()
+    nf = rng.uniform(0, 10, m).astype(np.float32)
+    new[rows] = (nf.view(np.uint32).astype(np.uint64) << np.uint64(32)) | rows.astype(np.uint64)
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).to(dev)  # noqa: E731
+    k_all = t(new, np.int64)
+    ski, ssi = t(keys[order], np.int64), t(order.astype(np.uint32), np.int32)
+    rw = t(rows, np.int32) if m else torch.zeros(1, dtype=torch.int32, device=dev)
+    mark = torch.zeros(n, dtype=torch.uint8, device=dev)
+    sko, sso = torch.empty_like(ski), torch.empty_like(ssi)
+    tb = int(L.pdg_order_update_temp_bytes(n, m))
+    temp = torch.empty(max(tb, 16), dtype=torch.uint8, device=dev)
+    _lib.check(L.pdg_order_update(_lib.ptr(k_all), _lib.ptr(ski), _lib.ptr(ssi), n, _lib.ptr(rw),
+                                  m, _lib.ptr(mark), _lib.ptr(sko), _lib.ptr(sso),
+                                  _lib.ptr(temp), temp.numel(), _lib.stream_ptr()),
+               "pdg_order_update")
+    torch.cuda.synchronize()
+    want = np.argsort(new, kind="stable")
+    np.testing.assert_array_equal(sso.cpu().numpy().view(np.uint32), want.astype(np.uint32))
+    np.testing.assert_array_equal(sko.cpu().numpy().view(np.uint64), new[want])
+    assert int(mark.sum().item()) == 0

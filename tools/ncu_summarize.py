@@ -121,12 +121,13 @@ def launches():
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     apps = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
+    k1_rows = int(sys.argv[3]) if len(sys.argv) > 3 else 1_000_000   # K1b capture: 1M rows
     os.makedirs(PROF, exist_ok=True)
     js_path = os.path.join(PROF, "ncu_summary.json")
     summ = json.load(open(js_path)) if os.path.exists(js_path) else {}
     lines = [f"# ncu summary ({tag})", ""]
     # role -> report; bench.py reads the "engine" entry for roofline.traffic
-    for rep, role, n in (("engine.ncu-rep", "engine", apps), ("k1.ncu-rep", "k1", apps),
+    for rep, role, n in (("engine.ncu-rep", "engine", apps), ("k1.ncu-rep", "k1", k1_rows),
                          ("need.ncu-rep", "need", 1_000_000)):
         p = os.path.join(OUT, rep)
         if not os.path.exists(p):
@@ -149,19 +150,20 @@ def main():
         # the step's own kernels (engine, serial completion, K1, the radix
         # sort of K5): per-launch means, and the engine's share of their sum
         step = [(k, n, t) for k, n, t, _ in ls
-                if any(x in k for x in ("mc_walk", "mc_engine", "mc_serial", "gittins_rows",
-                                        "gittins_hist", "DeviceRadixSort"))]
+                if any(x in k for x in ("mc_walk", "mc_engine", "mc_serial", "gittins_pair",
+                                        "gittins_hist", "order_sort", "attained"))]
         if step:
             per = {}
             for k, n, t in step:
-                grp = ("engine" if ("mc_walk" in k or "mc_engine" in k) else
+                grp = ("careful" if "mc_walk" in k and ", 1>" in k else
+                       "engine" if ("mc_walk" in k or "mc_engine" in k) else
                        "serial" if "mc_serial" in k else
-                       "k1" if "gittins" in k else "sort")
+                       "k1" if "gittins" in k else
+                       "attained" if "attained" in k else "sort")
                 per.setdefault(grp, [0.0, 0])
                 per[grp][0] += t
-                # one histogram kernel per radix sort; one launch per step otherwise
-                if grp != "sort" or "Histogram" in k:
-                    per[grp][1] += n
+                # one launch per step per kernel (three attained-service kernels)
+                per[grp][1] += n if grp != "attained" else n / 3
             mean = {g: t / max(n, 1) for g, (t, n) in per.items()}
             tot = sum(mean.values()) or 1.0
             summ["launch_step_share"] = {g: m / tot for g, m in mean.items()}
