@@ -23,7 +23,7 @@ set_remaining(256) + one gittins_rank_batch row per app) plus the global
 order:
   K2/a4  mc_walk_kernel       512-walk Monte Carlo from the current unit,
                               bit-identical to the reference, bucketed to 256
-  K1b    gittins_quad_kernel  Gittins key + overrun penalty + packed sort key
+  K1b    gittins_pair_kernel  Gittins key + overrun penalty + packed sort key
   K5     radix sort           global order (after the all-gather when N > 1)
 Each step uses fresh per-app seeds (a genuine re-estimate, nothing cached).
 
@@ -748,7 +748,7 @@ def run_ours(args):
         roofline["pcg_floor_ms"] = ns["pcg_floor_ms"]
         roofline["frac_of_pcg_floor"] = ns["pcg_floor_ms"] / eng_avg
     k1_bytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
-    k1 = {"kernel": "gittins_quad_kernel", "avg_launch_ms": float(k1_ms.mean()),
+    k1 = {"kernel": "gittins_pair_kernel", "avg_launch_ms": float(k1_ms.mean()),
           "bytes_per_app": k1_bytes,
           "achieved_gbs": k1_bytes * n / (float(k1_ms.mean()) / 1e3) / 1e9,
           "apps_per_s": n / (float(k1_ms.mean()) / 1e3)}
@@ -1029,7 +1029,7 @@ def bench_k1_large(dev, n=1_000_000, reps=20):
     nbytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
     ach = nbytes * n / (ms / 1e3) / 1e9
     peak = measured_peaks()[0]
-    return {"kernel": "gittins_quad_kernel", "rows": n, "ms_per_launch": ms,
+    return {"kernel": "gittins_pair_kernel", "rows": n, "ms_per_launch": ms,
             "apps_per_s": n / (ms / 1e3),
             "roofline": {"bound": "hbm", "bytes_per_app": nbytes, "achieved": ach,
                          "peak": peak, "unit": "GB/s", "frac": ach / peak}}

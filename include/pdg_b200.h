@@ -228,10 +228,11 @@ typedef struct {
 
 /* Scratch for pdg_mc_remaining_demand: pdg_mc_scratch_bytes(n, max_pairs,
  * pdg_mc_grid_warps()) + 4 * n_jobs bytes.  A numpy Lemire rejection (the
- * bounded draw redrawn, shifting every later half) is handled inside the fast
- * kernel for n <= 512 (the visit's bounded values are redrawn with the
- * sequential generator; flags bit3); own-input visits and n > 512 hand the
- * application to a second, sequential kernel in the same call (flags bit2). */
+ * bounded draw redrawn, shifting every later half) is handled for n <= 512 by
+ * a second, careful launch of the walk kernel over the handed-back
+ * applications, which redraws the rejecting visit's bounded values with the
+ * sequential generator (flags bit3); for n > 512 the application is replayed
+ * by a sequential kernel in the same call (flags bit2). */
 int pdg_mc_grid_warps(void);
 size_t pdg_mc_scratch_bytes(int32_t n_samples, int32_t max_pairs, int32_t grid_warps);
 int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_jobs* jobs,

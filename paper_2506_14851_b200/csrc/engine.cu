@@ -1094,6 +1094,9 @@ __device__ bool visit_strided(const EngineArgs& a, int job, const UnitDesc& d, c
   uint32_t wb = C ? (C - pin + 1) >> 1 : 0u;
   U128& st = ls.st;                               // one stride before word q
   bool rej = false;
+  // duration units: the smallest low product word of the visit's draws; a
+  // rejection happened iff it is below the threshold (one VIMNMX per half)
+  uint32_t min_left = 0xffffffffu;
   uint32_t pend_hi = 0;
   uint32_t q = (uint32_t(lane) - ls.P) & 31u;
 #pragma unroll kUnrollB
@@ -1102,10 +1105,15 @@ __device__ bool visit_strided(const EngineArgs& a, int job, const UnitDesc& d, c
     const uint64_t wd = pcg_out(st);
     const uint32_t R = 2u * q + pin;
     if (!LLM) {                                   // every low half is an A draw
-      ws.ia[R] = uint16_t(lemire_t(uint32_t(wd), uint32_t(pl.pa), thr_a, rej));
-      if (R + 1 < mA)
-        ws.ia[R + 1] = uint16_t(lemire_t(uint32_t(wd >> 32), uint32_t(pl.pa), thr_a, rej));
-      else pend_hi = uint32_t(wd >> 32);
+      const uint64_t m0 = uint64_t(uint32_t(wd)) * uint32_t(pl.pa);
+      const uint64_t m1 = uint64_t(uint32_t(wd >> 32)) * uint32_t(pl.pa);
+      ws.ia[R] = uint16_t(m0 >> 32);
+      // the high half of the visit's last word may be numpy's buffered half
+      // rather than a draw: it is still stored (into the staging slack) and
+      // still counted -- a false alarm costs a careful-pass redo, nothing else
+      ws.ia[R + 1] = uint16_t(m1 >> 32);
+      min_left = min(min_left, min(uint32_t(m0), uint32_t(m1)));
+      pend_hi = uint32_t(wd >> 32);
     } else {
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
@@ -1120,6 +1128,7 @@ __device__ bool visit_strided(const EngineArgs& a, int job, const UnitDesc& d, c
     if (mA) ws.ia[0] = uint16_t(lemire_t(g.pv, uint32_t(pl.pa), thr_a, rej));
     else ws.ib[0] = uint16_t(lemire_t(g.pv, uint32_t(pl.pb), thr_b, rej));
   }
+  if (!LLM) rej |= min_left < thr_a;
   __syncwarp();
   bool redone = false;
   uint64_t rd = 0;
@@ -1755,35 +1764,23 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
       kern<<<unsigned(sm_count()), kWalkWarps * 32, sm_bytes, st>>>(a);
       return launch_status("mc_walk_kernel (careful pass)");
     };
+    // the careful pass always runs the full variant: it handles every unit
+    // kind and redraws every rejection, so nothing is left for the
+    // sequential replay kernel on this path
     if (mu > 32) {                               // 64-bit unit sets, every unit kind
       r = launch(mc_walk_kernel<7, uint64_t>, kWalkWarps, smem);
       if (!r) r = careful(mc_walk_kernel<7, uint64_t, true>, smem);
-      if (r) return r;
-      return finish();
+      return r;
     }
     switch (feat) {
-      case 0:
-        r = launch(mc_walk_kernel<0>, kWalkWarps, smem_plain);
-        if (!r) r = careful(mc_walk_kernel<0, uint32_t, true>, smem_plain);
-        break;
-      case 1:
-        r = launch(mc_walk_kernel<1>, kWalkWarps, smem);
-        if (!r) r = careful(mc_walk_kernel<1, uint32_t, true>, smem);
-        break;
-      case 4:
-        r = launch(mc_walk_kernel<4>, kWalkWarps, smem_plain);
-        if (!r) r = careful(mc_walk_kernel<4, uint32_t, true>, smem_plain);
-        break;
-      case 5:
-        r = launch(mc_walk_kernel<5>, kWalkWarps, smem);
-        if (!r) r = careful(mc_walk_kernel<5, uint32_t, true>, smem);
-        break;
-      default:
-        r = launch(mc_walk_kernel<7>, kWalkWarps, smem);
-        if (!r) r = careful(mc_walk_kernel<7, uint32_t, true>, smem);
-        break;
+      case 0: r = launch(mc_walk_kernel<0>, kWalkWarps, smem_plain); break;
+      case 1: r = launch(mc_walk_kernel<1>, kWalkWarps, smem); break;
+      case 4: r = launch(mc_walk_kernel<4>, kWalkWarps, smem_plain); break;
+      case 5: r = launch(mc_walk_kernel<5>, kWalkWarps, smem); break;
+      default: r = launch(mc_walk_kernel<7>, kWalkWarps, smem); break;
     }
-    if (r) return r;
+    if (!r) r = careful(mc_walk_kernel<7, uint32_t, true>, smem);
+    return r;
   } else if (small_idx(n_samples)) {
     if (int r = launch(mc_engine_kernel<uint16_t>, kWarps, size_t(kWarps) * cnt_bytes)) return r;
   } else {
