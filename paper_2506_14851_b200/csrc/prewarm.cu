@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_kernel(NeedArgs 
 #ifndef PDG_NEED_STCS
 #define PDG_NEED_STCS 1
 #endif
+
 template <typename T>
 __device__ __forceinline__ void need_st(T* p, T v) {
 #if PDG_NEED_STCS
@@ -449,16 +450,21 @@ __global__ void __launch_bounds__(kNeedWarps * 32) prewarm_need_batched_kernel(N
       if (t3 >= 0 && t3 == t0) { f0 += f3; t3 = -1; }
       if (t3 >= 0 && t3 == t1) { f1 += f3; t3 = -1; }
       if (t3 >= 0 && t3 == t2) { f2 += f3; t3 = -1; }
-      float4* row4 = reinterpret_cast<float4*>(a.need + app[b] * int64_t(TK));
+      {
+        float4* row4 = reinterpret_cast<float4*>(a.need + app[b] * int64_t(TK));
 #pragma unroll 4
-      for (int i = lane; i < (TK >> 2); i += 32) need_st(row4 + i, make_float4(0.f, 0.f, 0.f, 0.f));
-      __syncwarp();
+        for (int i = lane; i < (TK >> 2); i += 32)
+          need_st(row4 + i, make_float4(0.f, 0.f, 0.f, 0.f));
+        __syncwarp();
+        if (kwin >= 0) {
+          float* row = a.need + app[b] * int64_t(TK) + kwin;
+          if (t0 >= 0) need_st(row + t0 * K, f0);
+          if (t1 >= 0) need_st(row + t1 * K, f1);
+          if (t2 >= 0) need_st(row + t2 * K, f2);
+          if (t3 >= 0) need_st(row + t3 * K, f3);
+        }
+      }
       if (kwin >= 0) {
-        float* row = a.need + app[b] * int64_t(TK) + kwin;
-        if (t0 >= 0) need_st(row + t0 * K, f0);
-        if (t1 >= 0) need_st(row + t1 * K, f1);
-        if (t2 >= 0) need_st(row + t2 * K, f2);
-        if (t3 >= 0) need_st(row + t3 * K, f3);
         if (a.agg) {
           double* c = cagg + kwin;
           if (t0 >= 0) c[t0 * K] += double(f0);

@@ -16,7 +16,7 @@ for flags in "$@"; do
   echo "== $flags" >> gpurun_out/need_sweep.txt
   PDG_LIB_PATH=$out timeout 300 python -c "
 import json, torch, bench
-r = bench.bench_need(torch.device('cuda', 0))
+r = bench.bench_need(torch.device('cuda', 0), cpu=False)
 print(json.dumps({'ms': r['ms_per_launch'], 'frac': r['roofline']['frac']}))
 " >> gpurun_out/need_sweep.txt 2>&1
   i=$((i+1))
