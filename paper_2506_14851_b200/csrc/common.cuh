@@ -65,6 +65,25 @@ __device__ __forceinline__ double bucket_mid(double lo, double w, int j) {
 }
 
 // ---- warp primitives -------------------------------------------------------
+// u32 inclusive scan: shfl.up's validity predicate guards the add, so no
+// per-step lane compare or select (the engine runs one per unit visit)
+template <int O>
+__device__ __forceinline__ void scan_up_add(uint32_t& v) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+      "shfl.sync.up.b32 t|p, %0, %1, 0x0, 0xffffffff;\n\t"
+      "@p add.u32 %0, %0, t;\n\t}"
+      : "+r"(v)
+      : "n"(O));
+}
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
+  scan_up_add<1>(v);
+  scan_up_add<2>(v);
+  scan_up_add<4>(v);
+  scan_up_add<8>(v);
+  scan_up_add<16>(v);
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
 #pragma unroll

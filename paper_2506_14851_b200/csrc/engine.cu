@@ -912,10 +912,10 @@ static_assert(sizeof(UnitCache) == 112, "unit cache layout");
 // the same for banks without LLM units: only what a duration visit reads
 struct __align__(16) UnitCacheLean {
   uint64_t t0, t1, t2;
-  int32_t a_off, a_len, succ_off;
+  const double* pa;        // the unit's rate-divided A pool (vals_div + a_off)
+  int32_t a_len, succ_off;
   int16_t flags, ns;
   uint32_t thr_a;          // Lemire rejection threshold of the A pool
-  int32_t pad;
   int32_t n[4];            // successor units, one 16-byte load (no sign-extension per visit)
 };
 static_assert(sizeof(UnitCacheLean) == 64, "lean unit cache layout");
@@ -933,11 +933,21 @@ __device__ __forceinline__ UnitDesc desc_of(const UnitCache& c) { return c.d; }
 __device__ __forceinline__ UnitDesc desc_of(const UnitCacheLean& c) {
   UnitDesc d{};
   d.flags = c.flags;
-  d.a_off = c.a_off;
   d.a_len = c.a_len;
   d.succ_off = c.succ_off;
   d.succ_len = c.ns;
   return d;
+}
+// a visit's rate-divided pools: the lean cache holds the A pool's address
+// (duration units: no B pool, no override); the full one goes through the
+// descriptor and the K3 override
+__device__ __forceinline__ Pools pools_of(const EngineArgs& a, const UnitCache& c,
+                                          const UnitDesc& d, bool ov, const Pools& ovd) {
+  return pools_div(a, d, ov, ovd);
+}
+__device__ __forceinline__ Pools pools_of(const EngineArgs&, const UnitCacheLean& c,
+                                          const UnitDesc&, bool, const Pools&) {
+  return Pools{c.pa, c.a_len, nullptr, 0};
 }
 
 __device__ __forceinline__ uint32_t thr_a_of(const UnitCache& c) { return c.thr_a; }
@@ -986,7 +996,7 @@ __device__ __forceinline__ uint32_t take_members(const WalkState& ws, int u, int
   // kSmemWalks = 512: one 16-bit slice per lane
   uint32_t x = (bu[lane >> 1] >> ((lane & 1) << 4)) & 0xffffu;
   const uint32_t c = __popc(x);
-  const uint32_t incl = warp_incl_scan(c, lane);
+  const uint32_t incl = warp_incl_scan_u32(c);
   uint32_t o = incl - c;
   while (x) {
     const int b = __ffs(x) - 1;
@@ -1567,7 +1577,7 @@ mc_walk_kernel(EngineArgs a) {
       if constexpr (kLLM) {
         c.d = d;
       } else {
-        c.a_off = d.a_off;
+        c.pa = a.b.vals_div + d.a_off;
         c.a_len = d.a_len;
         c.succ_off = d.succ_off;
         c.flags = int16_t(d.flags);
@@ -1603,7 +1613,7 @@ mc_walk_kernel(EngineArgs a) {
         pending &= ~(M(1) << u);
         const UnitDesc d = desc_of(uc[u]);
         const bool ov = has_ov && u == u0;
-        const Pools pd = pools_div(a, d, ov, ovd);
+        const Pools pd = pools_of(a, uc[u], d, ov, ovd);
         M targets = 0;
         if (!(d.flags & F_LLM))
           ok = visit_strided<false, M, kSpec, CAREFUL>(a, job, d, succ_of(uc[u]), pd, thr_a_of(uc[u]), 0u,
