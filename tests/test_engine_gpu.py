@@ -309,3 +309,32 @@ def test_wide_graph_64bit_unit_sets(n_units):
         want = O.mc_remaining_demand(og, c["current"], [], c["n"], c["seed"], c["visit_cap"])
         np.testing.assert_array_equal(got[i][0], want.samples, err_msg=str(c))
         assert got[i][1] == want.capped
+
+
+@pytest.mark.parametrize("k", [2, 7, 64, 256, 1000])
+def test_bucketize_boundary_samples_exact(k):
+    """Bucketing divides by one reciprocal multiply and falls back to the exact
+    division near bucket boundaries (common.cuh trunc_div): samples placed on
+    and one or a few ulps around every boundary lo + j*w must land in the
+    bucket Python's int((s - lo) / w) picks (distributions.py:98-101)."""
+    from paper_2506_14851_b200.sched import bucketize_rows
+    rng = np.random.default_rng(k)
+    rows = []
+    for r in range(24):
+        lo = float(rng.uniform(-50, 500)) if r % 3 else 0.0
+        wt = float(rng.lognormal(0, 2))
+        j = np.arange(k + 1, dtype=np.float64)
+        base = lo + j * wt
+        s = np.concatenate([base, np.nextafter(base, np.inf), np.nextafter(base, -np.inf),
+                            base + 4 * np.spacing(base), base - 4 * np.spacing(base)])
+        s = s[(s >= lo) & (s <= base[-1])]
+        s = rng.permutation(s)[:1024]
+        s[0], s[1] = lo, base[-1]                     # pin min / max
+        rows.append(s)
+    n = min(len(x) for x in rows)
+    X = np.stack([x[:n] for x in rows])
+    lo, w, nb, cnt = bucketize_rows(X, k)
+    for i in range(len(X)):
+        want = O.bucketize(X[i], k)
+        assert lo[i] == want.lo and nb[i] == want.k
+        np.testing.assert_array_equal(cnt[i, :want.k], want.counts, err_msg=f"row {i}")
