@@ -1337,6 +1337,10 @@ __device__ bool visit_own(const EngineArgs& a, int job, const UnitDesc& d, const
     if (lane == 0) cnt[bb] = m;
   }
   __syncwarp();
+  // per input bucket: its output pool (own pool or the unit's B pool) and
+  // size, staged once per visit (the draws below read them from shared memory)
+  uint32_t* bsize = ws.cnt + 3 * a.max_unit_k;
+  const double** bpool = reinterpret_cast<const double**>(ws.cnt + 4 * a.max_unit_k);
   // bucket layout: all members by bucket (start), drawing members (effo)
   const int perb = (K + 31) >> 5;
   uint32_t la = 0, le = 0;
@@ -1345,6 +1349,8 @@ __device__ bool visit_own(const EngineArgs& a, int job, const UnitDesc& d, const
     if (bb < K) {
       const int pln = a.b.pool_len[d.pool_off + bb];
       const int P = pln > 0 ? pln : pl.pb;
+      bsize[bb] = uint32_t(P);
+      bpool[bb] = pln > 0 ? a.b.vals_div + a.b.pool_off[d.pool_off + bb] : pd.B;
       la += cnt[bb];
       le += P > 1 ? cnt[bb] : 0u;
     }
@@ -1356,8 +1362,7 @@ __device__ bool visit_own(const EngineArgs& a, int job, const UnitDesc& d, const
   for (int t = 0; t < perb; ++t) {
     const int bb = lane * perb + t;
     if (bb < K) {
-      const int pln = a.b.pool_len[d.pool_off + bb];
-      const int P = pln > 0 ? pln : pl.pb;
+      const uint32_t P = bsize[bb];
       const uint32_t c = cnt[bb];
       start[bb] = ra;
       effo[bb] = re;
@@ -1380,13 +1385,8 @@ __device__ bool visit_own(const EngineArgs& a, int job, const UnitDesc& d, const
     if (valid && (__ffs(peers) - 1) == lane) cnt[bb] = dest + __popc(peers);
     __syncwarp();
     if (valid) {
-      const int pln = a.b.pool_len[d.pool_off + bb];
-      if ((pln > 0 ? pln : pl.pb) > 1) {
-        effl[effo[bb] + dest + __popc(peers & lt) - start[bb]] = uint16_t(k);
-      } else {
-        const double* pool = pln > 0 ? a.b.vals_div + a.b.pool_off[d.pool_off + bb] : pd.B;
-        ws.tmp[k] = dadd(ws.tmp[k], pool[0]);
-      }
+      if (bsize[bb] > 1u) effl[effo[bb] + dest + __popc(peers & lt) - start[bb]] = uint16_t(k);
+      else ws.tmp[k] = dadd(ws.tmp[k], bpool[bb][0]);
     }
   }
   __syncwarp();
@@ -1395,10 +1395,7 @@ __device__ bool visit_own(const EngineArgs& a, int job, const UnitDesc& d, const
   auto b_draw = [&](uint32_t j, uint32_t h) {
     const uint32_t k = effl[j];
     const int bb = ws.bkt[k];
-    const int pln = a.b.pool_len[d.pool_off + bb];
-    const double* pool = pln > 0 ? a.b.vals_div + a.b.pool_off[d.pool_off + bb] : pd.B;
-    const uint32_t P = uint32_t(pln > 0 ? pln : pl.pb);
-    ws.tmp[k] = dadd(ws.tmp[k], pool[lemire(h, P, rej)]);   // + o / decode_rate
+    ws.tmp[k] = dadd(ws.tmp[k], bpool[bb][lemire(h, bsize[bb], rej)]);   // + o / decode_rate
   };
   const uint32_t sh = __shfl_sync(kFull, pend_hi, (ls.P + wA - 1) & 31u);
   for (; q < wb; q += 32) {                       // phase B: output draws
@@ -1716,7 +1713,9 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   a.cap = visit_cap;
   a.k_out = bucket_count;
   a.max_unit_k = max_unit_k;
-  const int c = bucket_count > 3 * max_unit_k ? bucket_count : 3 * max_unit_k;
+  // counters per warp: the output histogram, or the own-input visit's
+  // per-bucket count / start / offset / pool size (u32) and pool address (u64)
+  const int c = bucket_count > 6 * max_unit_k ? bucket_count : 6 * max_unit_k;
   a.counters = (c + 3) & ~3;
   a.max_pairs = max_pairs;
   a.scratch = static_cast<char*>(scratch);
