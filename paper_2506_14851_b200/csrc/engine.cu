@@ -855,9 +855,12 @@ __host__ __device__ inline size_t walk_union_bytes(int counters, bool llm = true
   const size_t c = size_t(counters) * 4, s = size_t(kSmemWalks) * (llm ? 4 : 2) + 64;
   return align16(c > s ? c : s);
 }
+// (+ for LLM banks: the own-input visit's input bucket and sort order per
+// member, 2 x 512 u16, after the unit cache)
 __host__ __device__ inline size_t walk_smem_bytes(int counters, int units, bool llm = true) {
   return walk_union_bytes(counters, llm) + size_t(kSmemWalks) * 10 +
-         size_t(units) * kWalkWords * 4 + size_t(units) * (llm ? 112 : 64);
+         size_t(units) * kWalkWords * 4 + size_t(units) * (llm ? 112 : 64) +
+         (llm ? size_t(kSmemWalks) * 4 : 0);
 }
 // global scratch per warp: [own-input arrays] [K3 pairs]
 __host__ __device__ inline size_t walk_gmem_bytes() {
@@ -1195,9 +1198,14 @@ __device__ bool visit_strided(const EngineArgs& a, int job, const UnitDesc& d, c
       case 3: uniforms(std::integral_constant<int, 3>{}); break;
       default: uniforms(std::integral_constant<int, 4>{}); break;
     }
-  } else {                     // one generic loop: less code in the big variants
+  } else {                     // two loops only: less code in the big variants
+    if (sc.ns <= 1) {          // (ns = 0: t0 = all ones, every word takes n0)
 #pragma unroll 1
-    for (; q < W; q += 32) uniform(std::integral_constant<int, 4>{});
+      for (; q < W; q += 32) uniform(std::integral_constant<int, 1>{});
+    } else {
+#pragma unroll 1
+      for (; q < W; q += 32) uniform(std::integral_constant<int, 4>{});
+    }
   }
   const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
   ls.P += W;
@@ -1499,7 +1507,12 @@ mc_walk_kernel(EngineArgs a) {
   Cache* const uc = reinterpret_cast<Cache*>(ws.bits + a.b.max_units * kWalkWords);
   ws.uc = uc;
   ws.tmp = reinterpret_cast<double*>(gs);
-  ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + kSmemWalks);
+  if constexpr (kLLM) {                          // own-input staging in shared memory
+    ws.bkt = reinterpret_cast<uint16_t*>(
+        reinterpret_cast<unsigned char*>(uc) + size_t(a.b.max_units) * sizeof(Cache));
+  } else {
+    ws.bkt = reinterpret_cast<uint16_t*>(ws.tmp + kSmemWalks);
+  }
   ws.osrt = ws.bkt + kSmemWalks;
   ws.kin = reinterpret_cast<double*>(gs + walk_gmem_bytes());
   ws.kout = ws.kin + a.max_pairs;
