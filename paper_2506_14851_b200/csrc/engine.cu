@@ -1198,14 +1198,9 @@ __device__ bool visit_strided(const EngineArgs& a, int job, const UnitDesc& d, c
       case 3: uniforms(std::integral_constant<int, 3>{}); break;
       default: uniforms(std::integral_constant<int, 4>{}); break;
     }
-  } else {                     // two loops only: less code in the big variants
-    if (sc.ns <= 1) {          // (ns = 0: t0 = all ones, every word takes n0)
+  } else {                     // one generic loop: less code in the big variants
 #pragma unroll 1
-      for (; q < W; q += 32) uniform(std::integral_constant<int, 1>{});
-    } else {
-#pragma unroll 1
-      for (; q < W; q += 32) uniform(std::integral_constant<int, 4>{});
-    }
+    for (; q < W; q += 32) uniform(std::integral_constant<int, 4>{});
   }
   const uint32_t pv = __shfl_sync(kFull, pend_hi, (ls.P + wb - 1) & 31u);
   ls.P += W;
