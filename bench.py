@@ -811,8 +811,13 @@ def run_ours(args):
                 "issue_active_frac": ns.get("issue_active_frac"),
                 "warp_instructions": ns.get("warp_instructions")}
     if ns.get("pcg_floor_ms") is not None:
+        # issue-time floors from the ncu capture (4 warp instructions / SM /
+        # cycle): the PCG64 stream alone, and every instruction the kernel ran
         roofline["pcg_floor_ms"] = ns["pcg_floor_ms"]
         roofline["frac_of_pcg_floor"] = ns["pcg_floor_ms"] / eng_avg
+    if ns.get("issue_floor_ms") is not None:
+        roofline["issue_floor_ms"] = ns["issue_floor_ms"]
+        roofline["issue_frac"] = ns["issue_floor_ms"] / eng_avg
     k1_bytes = 2 * q.stride + 4 * 8 + 4 + 4 + 4 + 1 + 8
     k1 = {"kernel": "gittins_pair_kernel", "avg_launch_ms": float(k1_ms.mean()),
           "bytes_per_app": k1_bytes,

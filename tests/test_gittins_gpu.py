@@ -193,3 +193,23 @@ def test_hist_queue_quad_path_vs_oracle(b, ragged, nsamp):
     got2 = q.key_f32[:n].cpu().numpy().astype(np.float64)
     assert np.all(got2[np.setdiff1d(np.arange(n), sub)] == 0.0)
     np.testing.assert_array_equal(got2[sub], got[sub])
+
+
+@pytest.mark.parametrize("n", [4736, 4741, 33_333])
+def test_hist_queue_pair_path_partial_tiles(n):
+    """Queue sizes at and just past the pair kernel's threshold and with a
+    partial last 16-row tile: every row scored, none written twice."""
+    from paper_2506_14851_b200.queue import HistQueue
+    rng = np.random.default_rng(n)
+    rows = hist_rows(rng, n, 256, degenerate_frac=0.02, exhaust_frac=0.02)
+    q = HistQueue(n + 37, 256)                     # capacity above n: rows past n untouched
+    q.load_rows(rows["lo"], rows["width"], rows["est_age"], rows["nbins"], rows["nsamp"],
+                rows["counts"], age=rows["age"])
+    q.key_f32.fill_(-1.0)
+    q.score(penalty=2.0, n=n)
+    got = q.key_f32.cpu().numpy().astype(np.float64)
+    want, bad = oracle_keys(O, rows)
+    rel = np.abs(got[:n] - want) / np.maximum(np.abs(want), 1e-30)
+    assert rel.max() < 1e-5, (rel.max(), np.argmax(rel))
+    assert np.all(got[n:] == -1.0)
+    np.testing.assert_array_equal(q.flags[:n].cpu().numpy() == 1, bad)

@@ -87,7 +87,35 @@ def summarize(rep, kernel, apps):
            "stalls_pct": stalls(d)}
     for k in METRICS:
         out[k] = num(d, k)
+    if kernel == "engine" and dur and inst:
+        # issue floors at 4 warp instructions per SM per cycle: all of the
+        # kernel's instructions, and only the PCG64 stream's (the 128-bit LCG
+        # step, the XSL-RR output and the Lemire draws, pcg64.cuh) -- the
+        # part no bookkeeping change can remove
+        rate = 4 * sms * (clk or 1.965e9)
+        pcg = pcg_instructions(rep)
+        out["issue_floor_ms"] = inst / rate * 1e3
+        if pcg:
+            out["pcg_warp_instructions"] = pcg
+            out["pcg_floor_ms"] = pcg / rate * 1e3
     return out
+
+
+def pcg_instructions(rep):
+    """Executed warp instructions attributed to pcg64.cuh source lines."""
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+                          "cuda,sass"], capture_output=True, text=True).stdout
+    f, tot = None, 0.0
+    for r in csv.reader(io.StringIO(txt)):
+        if len(r) >= 2 and r[0] == "File Path":
+            f = r[1].split("/")[-1]
+            continue
+        if f == "pcg64.cuh" and len(r) > 8 and r[0] not in ("", "Line No"):
+            try:
+                tot += float(r[7])
+            except ValueError:
+                pass
+    return tot or None
 
 
 def launches():
@@ -111,11 +139,17 @@ def launches():
         scale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6,
                  "ms": 1e-3}.get(r[mu], 1e-9)
         name = r[kn][:90]
-        a = agg.setdefault(name, [0, 0.0])
+        a = agg.setdefault(name, [0, 0.0, []])
         a[0] += 1
         a[1] += v * scale
-    tot = sum(t for _, t in agg.values()) or 1.0
-    return sorted([(k, n, t, t / tot) for k, (n, t) in agg.items()], key=lambda x: -x[2])
+        a[2].append(v * scale)
+    tot = sum(t for _, t, _ in agg.values()) or 1.0
+    MED.clear()
+    MED.update({k: sorted(x)[len(x) // 2] for k, (_, _, x) in agg.items()})
+    return sorted([(k, n, t, t / tot) for k, (n, t, _) in agg.items()], key=lambda x: -x[2])
+
+
+MED = {}   # kernel -> median launch time (the bench also runs 1M-app config-3 steps)
 
 
 def main():
@@ -154,7 +188,8 @@ def main():
                                         "gittins_hist", "order_sort", "attained"))]
         if step:
             per = {}
-            for k, n, t in step:
+            for k, n, _ in step:
+                t = MED[k] * n            # median launch: config-3's 1M-app steps excluded
                 grp = ("careful" if "mc_walk" in k and ", 1>" in k else
                        "engine" if ("mc_walk" in k or "mc_engine" in k) else
                        "serial" if "mc_serial" in k else
@@ -170,7 +205,8 @@ def main():
             lines += ["", "Step kernels, mean time per step (cold): " +
                       ", ".join(f"{g} {m * 1e3:.3f} ms" for g, m in mean.items()) +
                       f"; engine share {mean.get('engine', 0.0) / tot * 100:.1f}% "
-                      "(bench.py's live share_of_step must agree)"]
+                      "(bench.py's live share_of_step must agree; per-kernel medians, so "
+                      "the 1M-app config-3 launches in the same run do not count)"]
     summ["_tag"] = tag
     json.dump(summ, open(js_path, "w"), indent=1)
     open(os.path.join(PROF, f"{tag}_ncu.md"), "w").write("\n".join(lines) + "\n")
