@@ -824,6 +824,32 @@ def run_ours(args):
           "achieved_gbs": k1_bytes * n / (float(k1_ms.mean()) / 1e3) / 1e9,
           "apps_per_s": n / (float(k1_ms.mean()) / 1e3)}
 
+    # ---- steady-state refresh: the bucket-period re-rank of cached rows ----
+    # (simcore.py:636-640: no re-estimation, only K1b over the resident
+    # histograms at the current attained service + the global order)
+    ref_ev = []
+    for i in range(max(args.steps, 10)):
+        flush.zero_()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        update_age()
+        q.score(PENALTY)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, q.keys[:n])
+        _lib.check(L.pdg_order(_lib.ptr(gathered if world > 1 else q.keys[:n]),
+                               _lib.ptr(out_keys), _lib.ptr(gslots), _lib.ptr(out_slots),
+                               world * n, 32, _lib.ptr(temp), temp.numel(), _lib.stream_ptr()),
+                   "pdg_order")
+        e1.record(stream)
+        ref_ev.append((e0, e1))
+    torch.cuda.synchronize()
+    ref_ms = np.array([a_.elapsed_time(b_) for a_, b_ in ref_ev])
+    ref_p50 = max_over_ranks([float(np.median(ref_ms))], world, dev)[0]
+    periodic = {"p50_latency_ms": ref_p50, "apps_per_s": world * n / (ref_p50 / 1e3),
+                "what": "bucket-period refresh of the resident queue (simcore.py:636-640): "
+                        "attained service + K1b over the cached histograms + global order, "
+                        "no re-estimation; L2 flushed before each"}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -833,7 +859,8 @@ def run_ours(args):
         "config": bench_config(n, b, world),
         "gpu_launches": None if launches is None else launches * args.steps,
         "gpu_launches_per_step": launches, "kernels": kernel_names,
-        "e2e": e2e, "roofline": roofline, "k1_refresh": k1, "cuda_graph": graph, "clocks": clk,
+        "e2e": e2e, "roofline": roofline, "k1_refresh": k1, "periodic_refresh": periodic,
+        "cuda_graph": graph, "clocks": clk,
     }
 
     # ---- like-for-like CPU baseline (rank 0, N = 1): the same apps --------
