@@ -227,7 +227,7 @@ class DemandEngine:
         if st is None:
             nbytes = 64 + 8 * n + 16
             h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
-            d = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            d = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)   # padding read back too
             hv = h.numpy()
             st = self._one[n] = (h, d, hv)
         h, d, hv = st
