@@ -1,5 +1,6 @@
 """K5 timing (development tool): pdg_order on n packed keys, begin_bit 32,
-CUDA events, median of reps, L2 flushed between launches.  Run with
+CUDA events, mean of reps (the event clock ticks in 2.048 us), L2 flushed
+between launches.  Run with
 PDG_LIB_PATH pointing at another build to compare implementations.
 Usage: python tools/order_bench.py [n ...]"""
 import json
@@ -33,6 +34,7 @@ def bench(n, reps=30):
     ts = []
     for _ in range(reps):
         flush.zero_()
+        torch.cuda._sleep(200_000)              # stream busy while the host launches
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         run()
@@ -40,7 +42,7 @@ def bench(n, reps=30):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ok = bool(torch.all(ko[1:] >= ko[:-1]).item())
-    return {"n": n, "ms": float(np.median(ts)), "sorted": ok}
+    return {"n": n, "ms": float(np.mean(ts)), "sorted": ok}
 
 
 if __name__ == "__main__":
