@@ -107,8 +107,18 @@ __global__ void __launch_bounds__(kSortThreads) order_sort_kernel(SortArgs a) {
     // A: digit histogram of this CTA's chunk
     hist[t] = 0u;
     __syncthreads();
-    for (int64_t i = c0 + t; i < c1; i += kSortThreads)
-      atomicAdd(&hist[uint32_t(__ldcg(kr + i) >> shift) & dmask], 1u);
+    for (int64_t tb = c0; tb < c1; tb += kSortTile) {   // a tile's loads in flight together
+      uint64_t x[kSortSteps];
+#pragma unroll
+      for (int s = 0; s < kSortSteps; ++s) {
+        const int64_t i = tb + t + int64_t(s) * kSortThreads;
+        x[s] = i < c1 ? __ldcg(kr + i) : 0ull;
+      }
+#pragma unroll
+      for (int s = 0; s < kSortSteps; ++s)
+        if (tb + t + int64_t(s) * kSortThreads < c1)
+          atomicAdd(&hist[uint32_t(x[s] >> shift) & dmask], 1u);
+    }
     __syncthreads();
     a.H[size_t(t) * G + b] = hist[t];
     grid.sync();
@@ -145,12 +155,19 @@ __global__ void __launch_bounds__(kSortThreads) order_sort_kernel(SortArgs a) {
       __syncwarp();
       uint64_t key[kSortSteps];
       uint32_t slot[kSortSteps], dig[kSortSteps], rnk[kSortSteps];
+      // all of the lane's loads in flight before the first ranking step (the
+      // warp syncs between steps would otherwise serialise them)
 #pragma unroll
       for (int s = 0; s < kSortSteps; ++s) {
         const int64_t i = tb + int64_t(w) * kSortWarpKeys + 32 * s + lane;
         const bool valid = i < c1;
         key[s] = valid ? __ldcg(kr + i) : 0ull;
         slot[s] = (valid && payload) ? __ldcg(sr + i) : 0u;
+      }
+#pragma unroll
+      for (int s = 0; s < kSortSteps; ++s) {
+        const int64_t i = tb + int64_t(w) * kSortWarpKeys + 32 * s + lane;
+        const bool valid = i < c1;
         const uint32_t d = valid ? uint32_t(key[s] >> shift) & dmask : 0x100u + lane;
         dig[s] = d;
         const unsigned peers = __match_any_sync(kFull, d);
