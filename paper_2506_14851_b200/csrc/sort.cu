@@ -419,6 +419,13 @@ __global__ void __launch_bounds__(kSortThreads) order_update_kernel(UpdArgs a) {
   grid.sync();
 
   // P3: scatter the kept keys of O ...
+  // (a batch ranked here is staged back into shared memory once, so the
+  // per-key binary searches over it cost shared-memory, not L2, latency)
+  const bool bsm = !a.presorted && a.m > 0;
+  if (bsm) {
+    for (int64_t j = t; j < a.m; j += kSortThreads) sB[j] = __ldcg(a.bk2 + j);
+    __syncthreads();
+  }
   for (int64_t tb = c0; tb < c1; tb += kUpdTile) {
     const uint32_t base = __ldcg(a.tc + tb / kUpdTile);
     const int64_t i0 = tb + int64_t(t) * (kUpdTile / kSortThreads);   // 4 consecutive keys
@@ -431,18 +438,32 @@ __global__ void __launch_bounds__(kSortThreads) order_update_kernel(UpdArgs a) {
     }
     uint32_t ex;
     cta_excl_scan(c, ex, wsum);
+    uint64_t kk[kUpdTile / kSortThreads];
+    uint32_t ks[kUpdTile / kSortThreads];
+#pragma unroll
+    for (int s = 0; s < kUpdTile / kSortThreads; ++s) {   // loads in flight together
+      kk[s] = kp[s] ? __ldcg(a.ski + i0 + s) : 0ull;
+      ks[s] = kp[s] ? __ldcg(a.ssi + i0 + s) : 0u;
+    }
 #pragma unroll
     for (int s = 0; s < kUpdTile / kSortThreads; ++s) {
       if (!kp[s]) continue;
-      const uint64_t k = __ldcg(a.ski + i0 + s);
+      const uint64_t k = kk[s];
       int64_t lo = 0, hi = a.m;                          // #B < k
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (__ldcg(a.bk2 + mid) < k) lo = mid + 1; else hi = mid;
+      if (bsm) {
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (sB[mid] < k) lo = mid + 1; else hi = mid;
+        }
+      } else {
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldcg(a.bk2 + mid) < k) lo = mid + 1; else hi = mid;
+        }
       }
       const uint64_t pos = uint64_t(base) + ex + uint64_t(lo);
       a.sko[pos] = k;
-      a.sso[pos] = __ldcg(a.ssi + i0 + s);
+      a.sso[pos] = ks[s];
       ++ex;
     }
   }
@@ -450,10 +471,19 @@ __global__ void __launch_bounds__(kSortThreads) order_update_kernel(UpdArgs a) {
   const int64_t gw = int64_t(b) * kSortWarps + w, nwarps = int64_t(G) * kSortWarps;
   for (int64_t j = gw; j < a.m; j += nwarps) {
     const uint64_t x = __ldcg(a.bk2 + j);
-    int64_t lo = 0, hi = a.n;                            // L = #O < x
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (__ldcg(a.ski + mid) < x) lo = mid + 1; else hi = mid;
+    // L = #O < x by a 32-way search: every round the warp probes 32 evenly
+    // spaced keys of the candidate range [lo, hi] and keeps the gap the
+    // ballot points at (4 dependent rounds for 1M keys instead of 20)
+    int64_t lo = 0, hi = a.n;
+    while (hi > lo) {
+      const int64_t step = (hi - lo + 31) / 32;
+      const int64_t q = lo + int64_t(lane + 1) * step - 1;
+      const bool below = q < hi && __ldcg(a.ski + q) < x;
+      const int c = __popc(__ballot_sync(kFull, below));   // probes below x: a prefix
+      const int64_t nlo = lo + int64_t(c) * step;
+      const int64_t qc = lo + int64_t(c + 1) * step - 1;   // first probe >= x, if any
+      hi = qc < hi ? qc : hi;
+      lo = nlo < hi ? nlo : hi;
     }
     const int64_t tile = lo / kUpdTile, ts = tile * kUpdTile;
     uint32_t c = 0;                                      // kept in [ts, lo)
