@@ -286,6 +286,10 @@ constexpr int kPairTileU4 = 16 * kPairPitchU4;         // 16 rows per tile
 #endif
 constexpr int kPairWarps = PDG_PAIR_WARPS;
 constexpr int kPairStages = PDG_PAIR_STAGES;
+#ifndef PDG_PAIR_MIN_ROWS
+#define PDG_PAIR_MIN_ROWS 4736                          // 148 SMs x 32 rows
+#endif
+constexpr int64_t kPairMinRows = PDG_PAIR_MIN_ROWS;      // smaller batches: warp per row
 
 __device__ __forceinline__ float rcp_approx(float x) {    // MUFU.RCP, ~1 ulp; rcp(0) = +inf
   float r;
@@ -684,7 +688,7 @@ extern "C" int pdg_gittins_score_hist(const pdg_hist_rows* rows, const double* a
   const int64_t maxb = rows->stride;   // buckets per row are bounded by the stride
   // quad tiles pay off once every SM has tiles to stream; small
   // (incremental) batches take the warp-per-row kernel's lower latency
-  if (maxb <= 256 && n >= int64_t(sm_count()) * 16 * 2) {
+  if (maxb <= 256 && n >= kPairMinRows) {
     auto kern = gittins_pair_kernel<kPairWarps, kPairStages>;
     const size_t smem = size_t(kPairWarps) * kPairStages * kPairTileU4 * sizeof(uint4);
     int per_sm = 0;
