@@ -197,8 +197,9 @@ def main():
                        "attained" if "attained" in k else "sort")
                 per.setdefault(grp, [0.0, 0])
                 per[grp][0] += t
-                # one launch per step per kernel (three attained-service kernels)
-                per[grp][1] += n if grp != "attained" else n / 3
+                # one launch per step per kernel (the unfused attained service
+                # is three kernels per step)
+                per[grp][1] += n if (grp != "attained" or "fused" in k) else n / 3
             mean = {g: t / max(n, 1) for g, (t, n) in per.items()}
             tot = sum(mean.values()) or 1.0
             summ["launch_step_share"] = {g: m / tot for g, m in mean.items()}
