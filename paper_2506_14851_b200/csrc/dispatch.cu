@@ -17,6 +17,8 @@
 // can start more), and one thread replays the reference loops on those short
 // lists in shared memory, emitting the events (preempt / start) in the order
 // the simulator applies them.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 
@@ -291,7 +293,11 @@ extern "C" int pdg_dispatch_status(const void* temp, int64_t n, int32_t n_backen
 // the result does not depend on task order: bit-identical to the reference
 // loop (which returns the first of equal values; only +0/-0 could differ).
 // ---------------------------------------------------------------------------
+#ifndef PDG_ATTAINED_FUSED
+#define PDG_ATTAINED_FUSED 1
+#endif
 namespace pdg {
+constexpr bool kAttainedFused = PDG_ATTAINED_FUSED != 0;
 __device__ __forceinline__ double from_orderable_u64(uint64_t k) {
   const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double(static_cast<long long>(b));
@@ -331,6 +337,36 @@ __global__ void attained_final_kernel(const double* __restrict__ completed,
        a += int64_t(gridDim.x) * blockDim.x)
     age[a] = dadd(completed[a], from_orderable_u64(best[a]));
 }
+// the three phases in ONE cooperative kernel (grid barriers instead of two
+// kernel boundaries): init -> task maxima -> final sum
+__global__ void __launch_bounds__(256) attained_fused_kernel(
+    const double* __restrict__ completed, const double* __restrict__ progress, int64_t n,
+    const int32_t* __restrict__ app, const uint8_t* __restrict__ active,
+    const double* __restrict__ start, const double* __restrict__ cold,
+    const double* __restrict__ service, int64_t n_tasks, double now, uint64_t* best,
+    double* __restrict__ age) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t a = i0; a < n; a += stride) best[a] = orderable_u64(progress[a]);
+  if (n_tasks > 0) {
+    grid.sync();
+    for (int64_t t = i0; t < n_tasks; t += stride) {
+      const double st = start[t];
+      const int32_t a = app[t];
+      if (!active[t] || st != st || a < 0 || a >= n) continue;
+      const double x = dsub(now, dadd(st, cold[t]));
+      const double run = x > 0.0 ? x : 0.0;
+      const double sv = service[t];
+      const double v = run < sv ? run : sv;
+      atomicMax(reinterpret_cast<unsigned long long*>(best + a),
+                static_cast<unsigned long long>(orderable_u64(v)));
+    }
+  }
+  grid.sync();
+  for (int64_t a = i0; a < n; a += stride)
+    age[a] = dadd(completed[a], from_orderable_u64(__ldcg(best + a)));
+}
 }  // namespace pdg
 
 extern "C" int pdg_attained_service(const double* completed, const double* progress,
@@ -354,6 +390,20 @@ extern "C" int pdg_attained_service(const double* completed, const double* progr
   }
   cudaStream_t st = (cudaStream_t)stream;
   uint64_t* best = static_cast<uint64_t*>(temp);
+  if (kAttainedFused) {
+    int per_sm = 0;
+    if (int r = launch_setup(reinterpret_cast<const void*>(attained_fused_kernel), 256, 0,
+                             &per_sm))
+      return r;
+    const int64_t m = std::max(n_apps, n_tasks);
+    const int64_t g = std::min<int64_t>((m + 255) / 256, int64_t(per_sm) * sm_count());
+    void* args[] = {&completed, &progress, &n_apps, &task_app, &task_active, &task_start,
+                    &task_cold, &task_service, &n_tasks, &now, &best, &age_out};
+    return cuda_status(cudaLaunchCooperativeKernel(
+                           reinterpret_cast<const void*>(attained_fused_kernel),
+                           dim3(unsigned(g)), dim3(256), args, 0, st),
+                       "attained_fused_kernel");
+  }
   const int64_t cap = int64_t(sm_count()) * 8;
   auto grid = [&](int64_t m) { return unsigned(std::min<int64_t>((m + 255) / 256, cap)); };
   attained_init_kernel<<<grid(n_apps), 256, 0, st>>>(progress, n_apps, best);
