@@ -192,6 +192,12 @@ typedef struct {
   int32_t features;               /* PDG_BANK_FEATURES_VALID | OR of the    */
                                   /* PDG_BANK_HAS_* kinds the bank holds;   */
                                   /* a speed hint only (0: assume all)      */
+  const uint8_t* unit_class;      /* [U] optional scheduling hint: expected */
+                                  /* remaining walk length class 0..15 of a */
+                                  /* job starting at the unit; the engine   */
+                                  /* hands out jobs longest-first when set  */
+                                  /* and the scratch holds 8 * n_jobs bytes */
+                                  /* (results do not depend on it)          */
 } pdg_graph_bank;
 enum {
   PDG_BANK_HAS_LLM = 1,           /* LLM units (input/output pools)         */
@@ -227,7 +233,8 @@ typedef struct {
 } pdg_mc_out;
 
 /* Scratch for pdg_mc_remaining_demand: pdg_mc_scratch_bytes(n, max_pairs,
- * pdg_mc_grid_warps()) + 4 * n_jobs bytes.  A numpy Lemire rejection (the
+ * pdg_mc_grid_warps()) + 4 * n_jobs bytes (8 * n_jobs for the
+ * longest-first job order, pdg_graph_bank.unit_class).  A numpy Lemire rejection (the
  * bounded draw redrawn, shifting every later half) is handled for n <= 512 by
  * a second, careful launch of the walk kernel over the handed-back
  * applications, which redraws the rejecting visit's bounded values with the

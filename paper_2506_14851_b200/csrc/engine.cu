@@ -84,6 +84,7 @@ struct EngineArgs {
   int32_t* serial_count;  // [1]
   int32_t* job_next;      // [1] dynamic job counter (mc_walk_kernel)
   int32_t* redo_next;     // [1] dynamic counter over serial_list (careful mc_walk_kernel)
+  const int32_t* order;   // [n_jobs] longest-first job order (NULL: queue order)
 };
 
 // distributions.py:107-118 with (lo, hi = last bucket edge, k)
@@ -1521,7 +1522,10 @@ mc_walk_kernel(EngineArgs a) {
       if (li >= *a.serial_count) break;
       job = a.serial_list[li];
     } else {
-      if (lane == 0) job = atomicAdd(a.job_next, 1);
+      if (lane == 0) {
+        job = atomicAdd(a.job_next, 1);
+        if (a.order && job < a.n_jobs) job = a.order[job];
+      }
       job = __shfl_sync(kFull, job, 0);
       if (job >= a.n_jobs) break;
     }
@@ -1650,6 +1654,47 @@ mc_walk_kernel(EngineArgs a) {
   }
 }
 
+// Longest-first job order (pdg_graph_bank.unit_class): a job's class is its
+// start unit's expected remaining walk length; the dynamic job counter then
+// hands out the long applications first, so the last applications to start
+// are short ones and the warps finish together (~3 % of a 100k-app launch).
+// Order within a class is arbitrary: every application's result depends only
+// on its own stream.  Two passes: class counts, then warp-aggregated slots.
+__device__ __forceinline__ int job_class(const EngineArgs& a, int64_t i) {
+  return a.b.unit_class[a.b.graph_base[a.j.graph[i]] + a.j.unit[i]] & 15;
+}
+
+__global__ void job_class_count_kernel(EngineArgs a, int32_t* counts) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n_jobs;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = job_class(a, i);
+    const unsigned same = __match_any_sync(__activemask(), c);
+    if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(counts + c, __popc(same));
+  }
+}
+
+__global__ void job_order_kernel(EngineArgs a, const int32_t* counts, int32_t* cursor,
+                                 int32_t* order) {
+  __shared__ int32_t base[16];
+  if (threadIdx.x < 16) {                        // classes 15, 14, ... first
+    int32_t s = 0;
+    for (int c = 15; c > int(threadIdx.x); --c) s += counts[c];
+    base[threadIdx.x] = s;
+  }
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n_jobs;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = job_class(a, i);
+    const unsigned same = __match_any_sync(__activemask(), c);
+    const int leader = __ffs(same) - 1;
+    int32_t slot = 0;
+    if (int(lane) == leader) slot = atomicAdd(cursor + c, __popc(same));
+    slot = __shfl_sync(same, slot, leader) + __popc(same & ((1u << lane) - 1u));
+    order[base[c] + slot] = int32_t(i);
+  }
+}
+
 }  // namespace pdg
 
 using namespace pdg;
@@ -1733,10 +1778,28 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   a.job_next = reinterpret_cast<int32_t*>(tail + 4);
   a.redo_next = reinterpret_cast<int32_t*>(tail + 8);
   a.serial_list = reinterpret_cast<int32_t*>(tail + 256);
+  a.order = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(a.serial_count, 0, 3 * sizeof(int32_t), st);
-  if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(serial_count)");
   const bool sm = n_samples <= kSmemWalks;
+  // longest-first order: a hint, used when the bank has classes and the
+  // scratch has room for it
+  const bool ordered = sm && bank->unit_class && n_jobs > 1 &&
+                       scratch_bytes >= need + size_t(n_jobs) * sizeof(int32_t);
+  int32_t* cls_counts = reinterpret_cast<int32_t*>(tail + 64);
+  int32_t* cls_cursor = reinterpret_cast<int32_t*>(tail + 128);
+  cudaError_t e = cudaMemsetAsync(a.serial_count, 0, ordered ? 192 : 3 * sizeof(int32_t), st);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(serial_count)");
+  if (ordered) {
+    int32_t* ord = reinterpret_cast<int32_t*>(tail + 256 + size_t(n_jobs) * sizeof(int32_t));
+    int64_t blocks = (n_jobs + 255) / 256;
+    const int64_t capb = int64_t(sm_count()) * 8;
+    if (blocks > capb) blocks = capb;
+    job_class_count_kernel<<<unsigned(blocks), 256, 0, st>>>(a, cls_counts);
+    if (int rc = launch_status("job_class_count_kernel")) return rc;
+    job_order_kernel<<<unsigned(blocks), 256, 0, st>>>(a, cls_counts, cls_cursor, ord);
+    if (int rc = launch_status("job_order_kernel")) return rc;
+    a.order = ord;
+  }
   const size_t cnt_bytes = align16(size_t(a.counters) * 4);
   // sequential completion of rejected apps (normally none: every block exits
   // after reading the counter)

@@ -37,7 +37,8 @@ class GraphBankC(C.Structure):
                 ("succ_cum", C.c_void_p), ("succ_nxt", C.c_void_p), ("conds", C.c_void_p),
                 ("pairs", C.c_void_p), ("jump", C.c_void_p), ("prefill_rate", C.c_double),
                 ("decode_rate", C.c_double), ("succ_thr", C.c_void_p), ("max_units", C.c_int32),
-                ("vals_div", C.c_void_p), ("features", C.c_int32)]
+                ("vals_div", C.c_void_p), ("features", C.c_int32),
+                ("unit_class", C.c_void_p)]
 
 
 class JobsC(C.Structure):
@@ -138,7 +139,7 @@ class DemandEngine:
             _lib.ptr(b.pool_len), _lib.ptr(b.succ_cum), _lib.ptr(b.succ_nxt),
             _lib.ptr(b.conds), _lib.ptr(b.pairs), _lib.ptr(self.jump),
             float(prefill_rate), float(decode_rate), _lib.ptr(b.succ_thr), int(b.max_units),
-            _lib.ptr(self.vals_div), int(b.features))
+            _lib.ptr(self.vals_div), int(b.features), _lib.ptr(b.unit_class))
         self.max_unit_k = b.max_unit_k
         self.max_pairs = b.max_pairs
 
@@ -157,7 +158,7 @@ class DemandEngine:
 
     def _scratch_for(self, n: int, n_jobs: int) -> torch.Tensor:
         L = _lib.lib()
-        need = int(L.pdg_mc_scratch_bytes(n, self.max_pairs, L.pdg_mc_grid_warps())) + 4 * n_jobs
+        need = int(L.pdg_mc_scratch_bytes(n, self.max_pairs, L.pdg_mc_grid_warps())) + 8 * n_jobs
         if self._scratch is None or self._scratch.numel() < need:
             self._scratch = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._scratch

@@ -569,6 +569,7 @@ class GraphBank:
         kinds_present = int(np.bitwise_or.reduce(units["flags"] & (F_LLM | F_OWN | F_ANYMASK))
                             if len(units) else 0)
         self.features = FEATURES_VALID | kinds_present
+        self.unit_class = t(unit_classes(units, gbase, gn, succ_cum, succ_nxt), np.uint8)
         ca = np.array(conds, dtype=COND_DTYPE) if len(conds) else np.zeros(1, COND_DTYPE)
         pa = np.array(pairs, dtype=PAIR_DTYPE) if len(pairs) else np.zeros(1, PAIR_DTYPE)
         self.host_conds = ca
@@ -579,6 +580,33 @@ class GraphBank:
 
     def local_unit(self, name: str, uid: str) -> int:
         return self.unit_order[name].index(uid)
+
+
+def unit_classes(units, gbase, gn, succ_cum, succ_nxt, iters: int = 32) -> np.ndarray:
+    """Scheduling hint per unit (pdg_graph_bank.unit_class): the expected
+    number of walk steps left from the unit, E[u] = 1 + sum_v p(u->v) E[v]
+    over the branch tables (32 value-iteration sweeps, cycles included),
+    clipped to classes 0..15.  Speed only: the engine's results do not
+    depend on it."""
+    nu = len(units)
+    if nu == 0:
+        return np.zeros(1, np.uint8)
+    slen = np.asarray(units["succ_len"], dtype=np.int64)
+    soff = np.asarray(units["succ_off"], dtype=np.int64)
+    ubase = np.repeat(np.asarray(gbase, dtype=np.int64), np.asarray(gn, dtype=np.int64))[:nu]
+    src = np.repeat(np.arange(nu), slen)
+    first = np.repeat(np.cumsum(slen) - slen, slen)
+    slot = np.arange(len(src)) - first
+    pos = soff[src] + slot
+    cum = np.asarray(succ_cum, dtype=np.float64)
+    nxt = np.asarray(succ_nxt, dtype=np.int64)
+    ok = (nxt[pos] >= 0) if len(pos) else np.zeros(0, bool)
+    p = cum[pos] - np.where(slot > 0, cum[np.maximum(pos - 1, 0)], 0.0)
+    src, dst, p = src[ok], ubase[src[ok]] + nxt[pos[ok]], p[ok]
+    e = np.ones(nu)
+    for _ in range(iters):
+        e = 1.0 + np.bincount(src, weights=p * e[dst], minlength=nu)
+    return np.clip(np.floor(e), 0, 15).astype(np.uint8)
 
 
 # ---------------------------------------------------------------------------
