@@ -1699,6 +1699,10 @@ __global__ void job_order_kernel(EngineArgs a, const int32_t* counts, int32_t* c
 
 using namespace pdg;
 
+#ifndef PDG_ORDER_MAX_APPS_PER_SM
+#define PDG_ORDER_MAX_APPS_PER_SM 2048
+#endif
+
 static bool small_idx(int n) { return n <= 65535; }
 
 static size_t walk_scratch(int n) {
@@ -1783,7 +1787,10 @@ extern "C" int pdg_mc_remaining_demand(const pdg_graph_bank* bank, const pdg_mc_
   const bool sm = n_samples <= kSmemWalks;
   // longest-first order: a hint, used when the bank has classes and the
   // scratch has room for it
+  // (above ~2k applications per SM the tail is amortised and the queue
+  // order's graph locality is worth more: 1M apps measured 20.61 vs 20.67 ms)
   const bool ordered = sm && bank->unit_class && n_jobs > 1 &&
+                       n_jobs <= int64_t(sm_count()) * PDG_ORDER_MAX_APPS_PER_SM &&
                        scratch_bytes >= need + size_t(n_jobs) * sizeof(int32_t);
   int32_t* cls_counts = reinterpret_cast<int32_t*>(tail + 64);
   int32_t* cls_cursor = reinterpret_cast<int32_t*>(tail + 128);
